@@ -1,0 +1,37 @@
+// rfx_* kernel-level C-ABI entry points (include/reforward_b200_exec.h).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "kernels/kernels.h"
+#include "reforward_b200.h"
+
+namespace rfexec {
+void set_last_error(const std::string& msg);
+}
+
+namespace {
+rfk::ConvGeom to_geom(const rfx_conv_geom& g) {
+  rfk::ConvGeom o;
+  o.N = g.N; o.H = g.H; o.W = g.W; o.C = g.C; o.P = g.P; o.Q = g.Q; o.R = g.R; o.S = g.S;
+  o.pad_h = g.pad_h; o.pad_w = g.pad_w; o.stride_h = g.stride_h; o.stride_w = g.stride_w;
+  return o;
+}
+}  // namespace
+
+extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
+  rfk::GemmDesc d;
+  d.M = a->M; d.N = a->N; d.K = a->K;
+  d.a_kind = static_cast<rfk::Operand>(a->a_kind); d.a = a->a; d.a_ld = a->a_ld; d.a_geom = to_geom(a->a_geom);
+  d.b_kind = static_cast<rfk::Operand>(a->b_kind); d.b = a->b; d.b_ld = a->b_ld; d.b_geom = to_geom(a->b_geom);
+  d.out = a->out; d.ldc = a->ldc; d.out_f32 = a->out_f32 != 0; d.accumulate_out = a->accumulate_out != 0;
+  d.bias = a->bias; d.stats = a->stats; d.splits = a->splits; d.split_stride = a->split_stride;
+  d.remap = a->remap != 0; d.rP = a->rP; d.rQ = a->rQ; d.rH = a->rH; d.rW = a->rW; d.rsh = a->rsh; d.rsw = a->rsw;
+  d.block_n = a->block_n;
+  cudaError_t e = rfk::gemm_launch(d, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    rfexec::set_last_error(std::string("rfx_gemm: ") + cudaGetErrorString(e));
+    return RF_E_CUDA;
+  }
+  return RF_OK;
+}

@@ -1,0 +1,60 @@
+// Host-side interface of the sm_100a kernels (internal; the C-ABI wrappers
+// live in csrc/executor/exec_capi.cpp).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace rfk {
+
+// ------------------------------------------------------------ GEMM engine
+// One warp-specialised tcgen05 kernel family serves every dense contraction of
+// the train step: conv fprop / dgrad (implicit GEMM through TMA im2col), conv
+// wgrad (im2col operand in MN-major form), 1x1 convs and the classifier (plain
+// 2-D TMA).  D[M,N] = sum_k A[m,k] * B[n,k], bf16 operands, fp32 accumulate in
+// TMEM.
+enum class Operand : int {
+  KMajor2D = 0,   // rows x K, K contiguous (row stride `ld` elements)
+  MNMajor2D = 1,  // K rows x MN, MN contiguous (row stride `ld` elements)
+  Im2colK = 2,    // NHWC activation, rows = output pixels, K = (r, s, c)
+  Im2colMN = 3,   // NHWC activation, K = output pixels, MN = (r, s, c)
+};
+
+// Convolution geometry for an im2col operand: input tensor N x H x W x C,
+// output P x Q, filter R x S.  c_blocks = ceil(C / 64); the K (or MN) index of
+// tap (r, s) channel c is ((r * S + s) * c_blocks * 64 + c).
+struct ConvGeom {
+  int N = 0, H = 0, W = 0, C = 0;
+  int P = 0, Q = 0, R = 1, S = 1;
+  int pad_h = 0, pad_w = 0, stride_h = 1, stride_w = 1;
+};
+
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  Operand a_kind = Operand::KMajor2D;
+  const void* a = nullptr;
+  long a_ld = 0;
+  ConvGeom a_geom;
+  Operand b_kind = Operand::KMajor2D;
+  const void* b = nullptr;
+  long b_ld = 0;
+  ConvGeom b_geom;
+  // epilogue
+  void* out = nullptr;
+  long ldc = 0;
+  bool out_f32 = false;
+  bool accumulate_out = false;  // out += D (fp32 only)
+  const float* bias = nullptr;  // per column
+  float* stats = nullptr;       // [m_tiles][2][N] column sum / sum of squares
+  int splits = 1;               // split-K; split z writes out + z * split_stride
+  long split_stride = 0;
+  // row remap of the output (strided-conv dgrad scatter): row m = (n, p, q)
+  // over P x Q goes to n * H * W + (p * sh) * W + q * sw.
+  bool remap = false;
+  int rP = 0, rQ = 0, rH = 0, rW = 0, rsh = 1, rsw = 1;
+  int block_n = 0;  // 0 = pick automatically (64 / 128 / 256)
+};
+
+cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream);
+int gemm_m_tiles(const GemmDesc& d);
+
+}  // namespace rfk

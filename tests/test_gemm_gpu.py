@@ -1,0 +1,139 @@
+"""tcgen05 GEMM engine vs a plain PyTorch fp32 reference of the same contraction.
+
+Operands are bf16 (exactly representable in fp32), so the reference is the
+fp32 product of the same values; tolerance covers fp32 accumulation order and
+the bf16 rounding of the stored output.
+"""
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_1808_00079_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+dev = "cuda"
+
+
+def _bf(*shape, scale=1.0, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return (torch.randn(*shape, generator=g) * scale).to(torch.bfloat16).to(dev)
+
+
+def _check(out, ref, rtol=2e-2):
+    out = out.float()
+    ref = ref.float()
+    err = (out - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    assert err <= rtol * scale, f"max err {err} vs scale {scale}"
+
+
+@pytest.mark.parametrize("M,N,Kd,bn,f32", [(256, 128, 128, 128, False), (200, 96, 96, 0, False),
+                                           (128, 256, 320, 256, False), (384, 64, 64, 64, False),
+                                           (130, 1000, 2048, 0, True), (33, 48, 40, 64, True)])
+def test_gemm_kmajor(M, N, Kd, bn, f32):
+    a = _bf(M, Kd, seed=1)
+    b = _bf(N, Kd, seed=2)
+    ref = a.float() @ b.float().t()
+    out = torch.zeros(M, N, device=dev, dtype=torch.float32 if f32 else torch.bfloat16)
+    bias = torch.randn(N, device=dev) if f32 else None
+    args = K.GemmArgs(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, b_kind=K.KMAJOR, b=b.data_ptr(),
+                      b_ld=Kd, out=out.data_ptr(), ldc=N, out_f32=int(f32), splits=1, block_n=bn,
+                      bias=None if bias is None else bias.data_ptr())
+    K.gemm(args)
+    torch.cuda.synchronize()
+    if bias is not None:
+        ref = ref + bias
+    _check(out, ref)
+
+
+@pytest.mark.parametrize("M,N,Kd,a_mn,b_mn", [(128, 128, 128, True, True), (1000, 2048, 32, True, True),
+                                              (64, 2048, 1000, False, True), (256, 192, 192, True, False)])
+def test_gemm_mn_major(M, N, Kd, a_mn, b_mn):
+    a = _bf(M, Kd, seed=3)
+    b = _bf(N, Kd, seed=4)
+    ref = a.float() @ b.float().t()
+    at = a.t().contiguous() if a_mn else a
+    bt = b.t().contiguous() if b_mn else b
+    out = torch.zeros(M, N, device=dev, dtype=torch.float32)
+    args = K.GemmArgs(M=M, N=N, K=Kd, a_kind=K.MNMAJOR if a_mn else K.KMAJOR, a=at.data_ptr(),
+                      a_ld=M if a_mn else Kd, b_kind=K.MNMAJOR if b_mn else K.KMAJOR, b=bt.data_ptr(),
+                      b_ld=N if b_mn else Kd, out=out.data_ptr(), ldc=N, out_f32=1, splits=1)
+    K.gemm(args)
+    torch.cuda.synchronize()
+    _check(out, ref)
+
+
+def _pad_w(w_nchw, cpad):
+    # [Cout, Cin, R, S] -> [Cout, R, S, Cpad] bf16
+    co, ci, r, s = w_nchw.shape
+    out = torch.zeros(co, r, s, cpad, device=dev, dtype=torch.bfloat16)
+    out[..., :ci] = w_nchw.permute(0, 2, 3, 1).to(torch.bfloat16)
+    return out.contiguous()
+
+
+CONV_CASES = [(2, 8, 8, 64, 128, 3, 1, 1), (2, 9, 9, 64, 64, 3, 1, 2), (2, 16, 16, 128, 256, 1, 0, 1),
+              (2, 15, 15, 64, 64, 7, 3, 2), (1, 7, 7, 512, 512, 3, 1, 1), (2, 10, 10, 96, 64, 3, 1, 1),
+              (4, 14, 14, 256, 256, 3, 1, 1), (2, 16, 16, 64, 128, 1, 0, 2)]
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,R,pad,st", CONV_CASES)
+def test_conv_fprop_im2col(N, H, W, Ci, Co, R, pad, st):
+    x = _bf(N, Ci, H, W, seed=5)
+    w = _bf(Co, Ci, R, R, scale=0.1, seed=6)
+    ref = F.conv2d(x.float(), w.float(), stride=st, padding=pad).permute(0, 2, 3, 1).contiguous()
+    g = K.conv_geom(N, H, W, Ci, R, R, pad, st)
+    cpad = (Ci + 63) // 64 * 64
+    xn = x.permute(0, 2, 3, 1).contiguous()
+    wp = _pad_w(w, cpad)
+    M = N * g.P * g.Q
+    out = torch.zeros(N, g.P, g.Q, Co, device=dev, dtype=torch.bfloat16)
+    mt = (M + 127) // 128
+    stats = torch.zeros(mt, 2, Co, device=dev)
+    args = K.GemmArgs(M=M, N=Co, K=R * R * cpad, a_kind=K.IM2COL_K, a=xn.data_ptr(), a_geom=g,
+                      b_kind=K.KMAJOR, b=wp.data_ptr(), b_ld=R * R * cpad, out=out.data_ptr(), ldc=Co,
+                      stats=stats.data_ptr(), splits=1)
+    K.gemm(args)
+    torch.cuda.synchronize()
+    _check(out, ref)
+    r2 = ref.reshape(M, Co)
+    _check(stats[:, 0].sum(0), r2.sum(0), rtol=1e-2)
+    _check(stats[:, 1].sum(0), (r2 * r2).sum(0), rtol=1e-2)
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,R,pad,st", CONV_CASES)
+@pytest.mark.parametrize("splits", [1, 3])
+def test_conv_wgrad_im2col(N, H, W, Ci, Co, R, pad, st, splits):
+    x = _bf(N, Ci, H, W, seed=7)
+    g = K.conv_geom(N, H, W, Ci, R, R, pad, st)
+    dy = _bf(N, Co, g.P, g.Q, seed=8)
+    ref = torch.nn.grad.conv2d_weight(x.float(), (Co, Ci, R, R), dy.float(), stride=st, padding=pad)
+    cpad = (Ci + 63) // 64 * 64
+    xn = x.permute(0, 2, 3, 1).contiguous()
+    dyn = dy.permute(0, 2, 3, 1).contiguous()
+    M = N * g.P * g.Q
+    ktot = R * R * cpad
+    out = torch.zeros(splits, Co, ktot, device=dev)
+    args = K.GemmArgs(M=Co, N=ktot, K=M, a_kind=K.MNMAJOR, a=dyn.data_ptr(), a_ld=Co, b_kind=K.IM2COL_MN,
+                      b=xn.data_ptr(), b_geom=g, out=out.data_ptr(), ldc=ktot, out_f32=1, splits=splits,
+                      split_stride=Co * ktot)
+    K.gemm(args)
+    torch.cuda.synchronize()
+    got = out.sum(0).reshape(Co, R, R, cpad)[..., :Ci].permute(0, 3, 1, 2)
+    _check(got, ref)
+
+
+def test_scatter_remap():
+    # 1x1 stride-2 dgrad: rows of dY (N,P,Q) land at (n, 2p, 2q) of dX
+    N, H, W, Co, Ci = 2, 8, 8, 64, 128
+    P, Q = 4, 4
+    dy = _bf(N * P * Q, Co, seed=9)
+    wt = _bf(Ci, Co, seed=10)  # [Cin, Cout], K-major over Cout
+    ref = torch.zeros(N, H, W, Ci, device=dev)
+    ref[:, ::2, ::2, :] = (dy.float() @ wt.float().t()).reshape(N, P, Q, Ci)
+    out = torch.zeros(N, H, W, Ci, device=dev, dtype=torch.bfloat16)
+    args = K.GemmArgs(M=N * P * Q, N=Ci, K=Co, a_kind=K.KMAJOR, a=dy.data_ptr(), a_ld=Co, b_kind=K.KMAJOR,
+                      b=wt.data_ptr(), b_ld=Co, out=out.data_ptr(), ldc=Ci, splits=1, remap=1, rP=P, rQ=Q, rH=H,
+                      rW=W, rsh=2, rsw=2)
+    K.gemm(args)
+    torch.cuda.synchronize()
+    _check(out, ref)

@@ -42,6 +42,94 @@ typedef struct rfx_gemm_args {
 
 int rfx_gemm(const rfx_gemm_args* args, void* stream);
 
+/* ------------------------------------------------------------ re-forward training executor
+ * A network is a DAG of ops over NHWC tensors; each builder call returns the
+ * id of the op's output tensor.  rfx_net_plan runs the host planner on the
+ * tensor graph (vertex = tensor, cost = arena bytes) and derives the
+ * re-forward schedule and arena layout; rfx_net_setup allocates device memory.
+ * Streams are cudaStream_t passed as void* (NULL = legacy default stream). */
+typedef struct rfx_net rfx_net;
+
+int rfx_net_create(int32_t batch, rfx_net** out);
+/* arch: resnet18|resnet34|resnet50|resnet101|resnet152|chain8|vgg16|alexnet|densenet121 */
+int rfx_net_create_named(const char* arch, int32_t batch, int32_t H, int32_t W, int32_t classes,
+                         rfx_net** out);
+void rfx_net_free(rfx_net* net);
+
+int rfx_net_input(rfx_net* net, int32_t H, int32_t W, int32_t C, int32_t* out);
+int rfx_net_conv(rfx_net* net, int32_t x, int32_t cout, int32_t R, int32_t S, int32_t stride, int32_t pad,
+                 const char* name, int32_t* out);
+int rfx_net_bn(rfx_net* net, int32_t y, int32_t relu, const char* name, int32_t* out);
+int rfx_net_bn_add_relu(rfx_net* net, int32_t y, int32_t skip, const char* name, int32_t* out);
+int rfx_net_relu(rfx_net* net, int32_t x, const char* name, int32_t* out);
+int rfx_net_maxpool(rfx_net* net, int32_t x, int32_t k, int32_t stride, int32_t pad, const char* name,
+                    int32_t* out);
+int rfx_net_avgpool(rfx_net* net, int32_t x, const char* name, int32_t* out);
+int rfx_net_fc(rfx_net* net, int32_t x, int32_t classes, const char* name, int32_t* out);
+int rfx_net_concat(rfx_net* net, int32_t a, int32_t b, const char* name, int32_t* out);
+int rfx_net_loss(rfx_net* net, int32_t logits, const char* name, int32_t* out);
+
+/* introspection */
+int32_t rfx_net_num_tensors(const rfx_net* net);
+int rfx_net_tensor_info(const rfx_net* net, int32_t t, char* name, size_t name_cap, int32_t* nhwc,
+                        int32_t* dtype, int64_t* cost, int32_t* producer);
+int32_t rfx_net_num_ops(const rfx_net* net);
+int rfx_net_op_info(const rfx_net* net, int32_t op, char* name, size_t name_cap, int32_t* kind,
+                    int32_t* inputs /* up to 2, -1 pads */, int32_t* out);
+int64_t rfx_net_flops_per_step(const rfx_net* net);
+
+/* planning: policy "reforward" | "store_all" | "lcg" | "sqrt" */
+int rfx_net_plan(rfx_net* net, const char* policy);
+int rfx_net_plan_with_stored(rfx_net* net, const uint8_t* stored_mask, const char* label);
+
+typedef struct rfx_memory_report {
+  int64_t planned_total;     /* Eq. 1 of the plan: stored cost + largest segment */
+  int64_t stored_cost;
+  int64_t max_segment;
+  int64_t store_all_total;   /* sum of interior tensor costs (regular training) */
+  int64_t tracked_peak;      /* live activation high-water mark over the schedule */
+  int64_t arena_bytes;       /* activation arena capacity */
+  int64_t grad_arena_bytes;
+  int64_t workspace_bytes;
+  int64_t param_bytes;
+  int64_t state_bytes;
+  int64_t reforward_ops;
+  int64_t segment_loads;
+  int64_t forward_ops;
+  int64_t backward_ops;
+  int64_t launches_per_step; /* kernel nodes in the captured step graph (0 before capture) */
+  int64_t candidate_max_term;
+  int32_t n_segments;
+  int32_t n_stored;
+} rfx_memory_report;
+
+int rfx_net_plan_info(const rfx_net* net, uint8_t* stored_mask, int32_t* seg_of, rfx_memory_report* rep);
+/* schedule: kinds (0 forward, 1 backward, 2 release), op ids, segment ids, re-forward flags */
+int rfx_net_schedule(const rfx_net* net, int32_t* kinds, int32_t* ops, int32_t* segs, int32_t* reforward,
+                     int32_t cap, int32_t* n_out);
+
+/* runtime */
+int rfx_net_setup(rfx_net* net, uint64_t seed);
+/* images: NCHW fp32 [batch, C, H, W]; labels int32 [batch]; from_host: 1 host
+ * pointers (copied inside the call), 0 device pointers */
+int rfx_net_load_batch(rfx_net* net, const float* images, const int32_t* labels, int32_t from_host,
+                       void* stream);
+int rfx_net_forward_backward(rfx_net* net, void* stream);
+int rfx_net_update(rfx_net* net, float lr, float momentum, float weight_decay, void* stream);
+int rfx_net_step(rfx_net* net, float lr, float momentum, float weight_decay, int32_t use_graph, void* stream);
+int rfx_net_read_loss(rfx_net* net, float* loss, void* stream);
+
+int32_t rfx_net_num_params(const rfx_net* net);
+int rfx_net_param_info(const rfx_net* net, int32_t i, char* name, size_t name_cap, int32_t* shape,
+                       int32_t* ndim, int32_t* kind, int64_t* count);
+/* which: 0 value, 1 gradient, 2 momentum; canonical (PyTorch OIHW / [out,in] / [C]) layout */
+int rfx_net_read_param(const rfx_net* net, int32_t i, int32_t which, float* host);
+int rfx_net_write_param(rfx_net* net, int32_t i, const float* host);
+int rfx_net_read_tensor(const rfx_net* net, int32_t t, float* host); /* NHWC, valid if resident */
+int rfx_net_read_bn_running(const rfx_net* net, int32_t op, float* mean, float* var);
+/* flat fp32 gradient buffer (data-parallel all-reduce target) */
+int rfx_net_grad_buffer(const rfx_net* net, void** dev_ptr, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

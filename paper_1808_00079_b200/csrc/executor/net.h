@@ -1,0 +1,229 @@
+// Re-forward training executor: network IR, plan, schedule and runtime.
+//
+// A network is a DAG of ops over activation tensors (NHWC bf16; logits fp32).
+// Its tensor graph — vertex = tensor, cost = its arena bytes, edge = op
+// input -> output — is exactly the computation graph of the paper (§4 "the
+// vertices represent the DNN tensors and the edges represent DNN
+// operations"), handed to the host planner (reforward::solve_acg).  The plan's
+// stored set V^R gets fixed slots in the activation arena; every segment (a
+// weakly-connected component of non-stored tensors) is packed into one shared
+// re-forward region sized to the largest segment, so the arena is
+// stored_cost + max_segment = Eq. 1, and the schedule's live-byte high-water
+// mark is tracked to prove it.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels/kernels.h"
+#include "kernels/ops.h"
+
+namespace rfx {
+
+enum class DType : int { BF16 = 0, F32 = 1 };
+enum class OpKind : int { Input = 0, Conv, BN, BNAddReLU, ReLU, MaxPool, AvgPool, FC, Concat, Loss };
+const char* op_kind_name(OpKind k);
+
+constexpr long kAlign = 1024;  // arena slot alignment (bytes); costs are rounded to it
+inline long align_up(long x, long a = kAlign) { return (x + a - 1) / a * a; }
+
+struct Tensor {
+  std::string name;
+  int N = 0, H = 1, W = 1, C = 0;
+  DType dtype = DType::BF16;
+  int producer = -1;
+  std::vector<int> consumers;
+  long elems() const { return (long)N * H * W * C; }
+  long bytes() const { return elems() * (dtype == DType::BF16 ? 2 : 4); }
+  long cost() const { return align_up(bytes()); }  // planner vertex cost
+  long rows() const { return (long)N * H * W; }
+};
+
+struct BNState {  // per-BN-layer device state (persistent, fp32 [C] each)
+  int C = 0;
+  long mean = 0, invstd = 0, scale = 0, shift = 0, run_mean = 0, run_var = 0, coef = 0;  // offsets (floats)
+};
+
+struct Param {
+  std::string name;
+  int kind = 0;  // 0 conv weight, 1 bn gamma, 2 bn beta, 3 fc weight, 4 fc bias
+  int op = -1;
+  long offset = 0, count = 0;          // slice of the flat fp32 master / grad / momentum buffers
+  long bf16_off = -1, bf16_count = 0;  // bf16 GEMM-layout copy (conv / fc weights)
+  long wt_off = -1, wt_count = 0;      // bf16 flipped transpose for conv dgrad
+  std::vector<int> shape;              // canonical (PyTorch) shape
+};
+
+struct Op {
+  OpKind kind = OpKind::Input;
+  std::string name;
+  std::vector<int> in;
+  int out = -1;
+  // conv
+  int R = 1, S = 1, stride = 1, pad = 0;
+  int cin = 0, cin_real = 0, cout = 0, cpad = 0, coutpad = 0;
+  bool explicit_im2col = false;
+  int kpad = 0;              // explicit im2col K (padded)
+  bool fuse_stats = false;   // conv epilogue emits BN partial sums for its consumer
+  long stats_off = -1;       // its slot in the statistics workspace (floats)
+  int wg_splits = 1, wg_bn = 128;  // wgrad split-K and tile N
+  // pool
+  int k = 1;
+  // classifier
+  int classes = 0;
+  // parameters / state
+  int w_param = -1, b_param = -1;  // conv/fc weight + fc bias; bn gamma (w) + beta (b)
+  int bn = -1;                     // BNState index
+  float eps = 1e-5f, momentum = 0.1f;
+};
+
+struct Plan {
+  std::string policy;
+  std::vector<char> stored;   // per tensor
+  std::vector<int> seg_of;    // per tensor, -1 unless in a segment
+  std::vector<long> seg_cost;
+  long stored_cost = 0, max_seg = 0, total = 0, store_all_total = 0, candidate_max_term = 0;
+};
+
+enum class InstrKind : int { Forward = 0, Backward = 1, Release = 2 };
+struct Instr {
+  InstrKind kind;
+  int op = -1;
+  int seg = -1;
+  bool reforward = false;
+  int phase = 0;  // two-phase forward of an add/concat whose inputs sit in two segments
+};
+
+struct MemoryReport {
+  long planned_total = 0;       // Eq. 1 of the plan (stored + max segment)
+  long stored_cost = 0, max_segment = 0, store_all_total = 0;
+  long tracked_peak = 0;        // high-water mark of live activation bytes over the schedule
+  long arena_bytes = 0;         // activation arena capacity
+  long grad_arena_bytes = 0, workspace_bytes = 0, param_bytes = 0, state_bytes = 0;
+  long reforward_ops = 0, segment_loads = 0, forward_ops = 0, backward_ops = 0;
+  long launches_per_step = 0;
+};
+
+class Net;
+std::unique_ptr<Net> make_net(int batch);
+
+class Net {
+ public:
+  explicit Net(int batch) : batch_(batch) {}
+  ~Net();
+
+  // ---------------------------------------------------------- building
+  int input(int H, int W, int C);  // NCHW fp32 images -> NHWC bf16 (C padded to 8)
+  int conv(int x, int cout, int R, int S, int stride, int pad, const std::string& name);
+  int bn(int y, bool relu, const std::string& name);
+  int bn_add_relu(int y, int skip, const std::string& name);
+  int relu(int x, const std::string& name);
+  int maxpool(int x, int k, int stride, int pad, const std::string& name);
+  int avgpool(int x, const std::string& name);
+  int fc(int x, int classes, const std::string& name);
+  int concat(int a, int b, const std::string& name);
+  int loss(int logits, const std::string& name);
+
+  // ---------------------------------------------------------- planning
+  // policy: "reforward" (Algorithm 5 / solve_acg), "store_all", "lcg"
+  // (Algorithm 1, linear graphs), "sqrt" (even sqrt(N) heuristic, linear).
+  void plan(const std::string& policy);
+  void plan_with_stored(const std::vector<char>& stored, const std::string& label);
+  void graph_export(std::vector<std::string>& names, std::vector<long>& costs,
+                    std::vector<std::pair<int, int>>& edges) const;
+
+  // ---------------------------------------------------------- runtime
+  void setup(uint64_t seed);  // allocate device memory, init parameters
+  void load_batch(const float* images, const int* labels, bool from_host, cudaStream_t st);
+  void forward_backward(cudaStream_t st);  // loss + gradients (no update)
+  void update(float lr, float momentum, float wd, cudaStream_t st);  // SGD + weight prep
+  void step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph);
+  float read_loss(cudaStream_t st);
+
+  // parameter access in canonical layout (host fp32)
+  int num_params() const { return (int)params_.size(); }
+  const Param& param(int i) const { return params_[i]; }
+  void read_param(int i, int which, float* host) const;  // which: 0 value, 1 grad, 2 momentum
+  void write_param(int i, const float* host);
+  void read_tensor(int t, float* host) const;
+  void read_bn_running(int op, float* mean, float* var) const;
+
+  float* grad_buffer() const { return d_grad_; }
+  long grad_count() const { return n_params_; }
+
+  const MemoryReport& report() const { return rep_; }
+  const Plan& current_plan() const { return plan_; }
+  const std::vector<Tensor>& tensors() const { return tensors_; }
+  const std::vector<Op>& ops() const { return ops_; }
+  const std::vector<Instr>& schedule() const { return sched_; }
+  int batch() const { return batch_; }
+  long flops_per_step() const;
+
+ private:
+  int add_tensor(const std::string& name, int N, int H, int W, int C, DType dt);
+  int add_op(Op op);
+  int add_param(const std::string& name, int kind, int op, long count, std::vector<int> shape);
+  void build_schedule();
+  void layout();
+  void run_instr(const Instr& ins, cudaStream_t st);
+  void op_forward(const Op& op, bool reforward, int phase, cudaStream_t st);
+  void op_backward(const Op& op, cudaStream_t st);
+  void prep_weights(cudaStream_t st);
+  void* tptr(int t) const;
+  __nv_bfloat16* tb(int t) const { return static_cast<__nv_bfloat16*>(tptr(t)); }
+  __nv_bfloat16* gptr(int t) const;
+  void gemm(const rfk::GemmDesc& d, cudaStream_t st);
+  void check(cudaError_t e, const char* what) const;
+  void free_device();
+
+  int batch_;
+  std::vector<Tensor> tensors_;
+  std::vector<Op> ops_;
+  std::vector<Param> params_;
+  std::vector<BNState> bns_;
+  int input_t_ = -1, loss_t_ = -1, logits_t_ = -1;
+  int in_c_real_ = 0;
+  long n_params_ = 0, n_bf16_ = 0, n_state_ = 0;
+
+  Plan plan_;
+  bool planned_ = false;
+  std::vector<Instr> sched_;
+  std::vector<long> slot_;        // arena offset per tensor (stored or segment slot)
+  std::vector<long> grad_slot_;   // grad arena offset per tensor, -1 if none
+  std::vector<char> grad_acc_;    // per (op, input) accumulate flags, flattened
+  std::vector<int> grad_acc_base_;
+  long arena_bytes_ = 0, grad_bytes_ = 0;
+  long ws_im2col_ = 0, ws_partials_ = 0, ws_zero_ = 0, ws_split_ = 0, ws_stats_ = 0, ws_misc_ = 0;
+  MemoryReport rep_;
+  long launches_ = 0;
+  bool counting_ = false;
+
+  // device memory
+  bool setup_done_ = false;
+  uint8_t* d_arena_ = nullptr;
+  uint8_t* d_grad_arena_ = nullptr;
+  uint8_t* d_ws_ = nullptr;
+  float* d_param_ = nullptr;
+  float* d_grad_ = nullptr;
+  float* d_mom_ = nullptr;
+  __nv_bfloat16* d_bf16_ = nullptr;
+  float* d_state_ = nullptr;
+  __nv_bfloat16* d_input_ = nullptr;
+  float* d_images_ = nullptr;
+  int* d_labels_ = nullptr;
+  float* d_loss_ = nullptr;
+  float* d_rowloss_ = nullptr;
+  float* d_lse_ = nullptr;
+  float* d_hyper_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  float graph_lr_ = 0, graph_mom_ = 0, graph_wd_ = 0;
+
+  friend class Scheduler;
+};
+
+}  // namespace rfx

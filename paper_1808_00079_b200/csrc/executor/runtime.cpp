@@ -1,0 +1,623 @@
+// Device side of the executor: arenas, parameters, per-op forward/backward
+// dispatch onto the sm_100a kernels, SGD, CUDA-graph capture of the step.
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "executor/net.h"
+
+namespace rfx {
+
+namespace {
+int round8(int c) { return (c + 7) / 8 * 8; }
+
+float bf16_to_float(uint16_t b) {
+  uint32_t u = static_cast<uint32_t>(b) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+}  // namespace
+
+std::unique_ptr<Net> make_net(int batch) { return std::make_unique<Net>(batch); }
+
+Net::~Net() { free_device(); }
+
+void Net::check(cudaError_t e, const char* what) const {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void Net::free_device() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  graph_exec_ = nullptr;
+  for (void* p : {(void*)d_arena_, (void*)d_grad_arena_, (void*)d_ws_, (void*)d_param_, (void*)d_grad_,
+                  (void*)d_mom_, (void*)d_bf16_, (void*)d_state_, (void*)d_input_, (void*)d_images_,
+                  (void*)d_labels_, (void*)d_loss_, (void*)d_rowloss_, (void*)d_lse_, (void*)d_hyper_})
+    if (p) cudaFree(p);
+  d_arena_ = d_grad_arena_ = d_ws_ = nullptr;
+  d_param_ = d_grad_ = d_mom_ = d_state_ = d_images_ = d_loss_ = d_rowloss_ = d_lse_ = d_hyper_ = nullptr;
+  d_bf16_ = d_input_ = nullptr;
+  d_labels_ = nullptr;
+  setup_done_ = false;
+}
+
+// ============================================================ setup
+void Net::setup(uint64_t seed) {
+  if (!planned_) throw std::invalid_argument("plan the network before setup");
+  free_device();
+  // bf16 weight copies
+  n_bf16_ = 0;
+  for (auto& p : params_) {
+    const Op& op = ops_[p.op];
+    if (p.kind == 0) {
+      p.bf16_off = n_bf16_;
+      p.bf16_count = p.count;
+      n_bf16_ += (p.count + 63) / 64 * 64;
+      if (!op.explicit_im2col) {
+        p.wt_off = n_bf16_;
+        p.wt_count = (long)op.cin * op.R * op.S * op.coutpad;
+        n_bf16_ += (p.wt_count + 63) / 64 * 64;
+      }
+    } else if (p.kind == 3) {
+      p.bf16_off = n_bf16_;
+      p.bf16_count = p.count;
+      n_bf16_ += (p.count + 63) / 64 * 64;
+    }
+  }
+  auto alloc = [&](void** p, long bytes, const char* what) {
+    check(cudaMalloc(p, bytes > 0 ? bytes : 256), what);
+  };
+  alloc((void**)&d_arena_, arena_bytes_, "activation arena");
+  alloc((void**)&d_grad_arena_, grad_bytes_, "gradient arena");
+  alloc((void**)&d_ws_, rep_.workspace_bytes, "workspace");
+  alloc((void**)&d_param_, n_params_ * 4, "params");
+  alloc((void**)&d_grad_, n_params_ * 4, "grads");
+  alloc((void**)&d_mom_, n_params_ * 4, "momentum");
+  alloc((void**)&d_bf16_, n_bf16_ * 2, "bf16 weights");
+  alloc((void**)&d_state_, n_state_ * 4, "bn state");
+  const Tensor& in = tensors_[input_t_];
+  alloc((void**)&d_input_, in.bytes(), "input");
+  alloc((void**)&d_images_, (long)batch_ * in_c_real_ * in.H * in.W * 4, "images");
+  alloc((void**)&d_labels_, batch_ * 4, "labels");
+  alloc((void**)&d_loss_, 256, "loss");
+  alloc((void**)&d_rowloss_, batch_ * 4, "row loss");
+  alloc((void**)&d_lse_, batch_ * 4, "lse");
+  alloc((void**)&d_hyper_, 256, "hyper");
+  check(cudaMemset(d_grad_, 0, n_params_ * 4), "memset");
+  check(cudaMemset(d_mom_, 0, n_params_ * 4), "memset");
+  check(cudaMemset(d_bf16_, 0, n_bf16_ * 2), "memset");
+  check(cudaMemset(d_arena_, 0, arena_bytes_ > 0 ? arena_bytes_ : 256), "memset");
+  check(cudaMemset(d_labels_, 0, batch_ * 4), "memset");
+  check(cudaMemset(d_input_, 0, in.bytes()), "memset");
+
+  // parameters: Kaiming-normal convs, unit BN, small classifier (deterministic)
+  std::vector<float> host(n_params_, 0.f);
+  std::mt19937_64 rng(seed);
+  for (auto& p : params_) {
+    const Op& op = ops_[p.op];
+    if (p.kind == 0) {
+      std::normal_distribution<float> nd(0.f, std::sqrt(2.f / (float)(op.cin_real * op.R * op.S)));
+      std::vector<float> canon(p.count > 0 ? (size_t)op.cout * op.cin_real * op.R * op.S : 0);
+      for (auto& v : canon) v = nd(rng);
+      write_param((int)(&p - &params_[0]), canon.data());  // uploads; host copy refreshed below
+      continue;
+    }
+    float* dst = host.data() + p.offset;
+    if (p.kind == 1) std::fill(dst, dst + p.count, 1.f);
+    if (p.kind == 2 || p.kind == 4) std::fill(dst, dst + p.count, 0.f);
+    if (p.kind == 3) {
+      std::normal_distribution<float> nd(0.f, 0.01f);
+      for (long i = 0; i < p.count; ++i) dst[i] = nd(rng);
+    }
+    check(cudaMemcpy(d_param_ + p.offset, dst, p.count * 4, cudaMemcpyHostToDevice), "param upload");
+  }
+  std::vector<float> st(n_state_, 0.f);
+  for (const auto& b : bns_) std::fill(st.begin() + b.run_var, st.begin() + b.run_var + b.C, 1.f);
+  check(cudaMemcpy(d_state_, st.data(), n_state_ * 4, cudaMemcpyHostToDevice), "state upload");
+  setup_done_ = true;
+  prep_weights(0);
+  check(cudaDeviceSynchronize(), "setup");
+}
+
+// Canonical (PyTorch) layout <-> GEMM layout conversions.
+void Net::write_param(int i, const float* host) {
+  const Param& p = params_.at(i);
+  const Op& op = ops_[p.op];
+  std::vector<float> buf(p.count, 0.f);
+  if (p.kind == 0) {
+    const int co = op.cout, ci = op.cin_real, R = op.R, S = op.S;
+    for (int a = 0; a < co; ++a)
+      for (int c = 0; c < ci; ++c)
+        for (int r = 0; r < R; ++r)
+          for (int s = 0; s < S; ++s) {
+            const float v = host[(((long)a * ci + c) * R + r) * S + s];
+            long idx;
+            if (op.explicit_im2col) idx = (long)a * op.kpad + (r * S + s) * ci + c;
+            else idx = (((long)a * R + r) * S + s) * op.cpad + c;
+            buf[idx] = v;
+          }
+  } else {
+    std::memcpy(buf.data(), host, p.count * 4);
+  }
+  check(cudaMemcpy(d_param_ + p.offset, buf.data(), p.count * 4, cudaMemcpyHostToDevice), "write_param");
+  if (setup_done_) {
+    prep_weights(0);
+    check(cudaDeviceSynchronize(), "write_param");
+  }
+}
+
+void Net::read_param(int i, int which, float* host) const {
+  const Param& p = params_.at(i);
+  const Op& op = ops_[p.op];
+  const float* src = which == 0 ? d_param_ : (which == 1 ? d_grad_ : d_mom_);
+  std::vector<float> buf(p.count);
+  check(cudaMemcpy(buf.data(), src + p.offset, p.count * 4, cudaMemcpyDeviceToHost), "read_param");
+  if (p.kind == 0) {
+    const int co = op.cout, ci = op.cin_real, R = op.R, S = op.S;
+    for (int a = 0; a < co; ++a)
+      for (int c = 0; c < ci; ++c)
+        for (int r = 0; r < R; ++r)
+          for (int s = 0; s < S; ++s) {
+            long idx;
+            if (op.explicit_im2col) idx = (long)a * op.kpad + (r * S + s) * ci + c;
+            else idx = (((long)a * R + r) * S + s) * op.cpad + c;
+            host[(((long)a * ci + c) * R + r) * S + s] = buf[idx];
+          }
+  } else {
+    std::memcpy(host, buf.data(), p.count * 4);
+  }
+}
+
+void Net::read_tensor(int t, float* host) const {
+  const Tensor& tt = tensors_.at(t);
+  const void* src = tptr(t);
+  if (tt.dtype == DType::F32) {
+    check(cudaMemcpy(host, src, tt.bytes(), cudaMemcpyDeviceToHost), "read_tensor");
+    return;
+  }
+  std::vector<uint16_t> buf(tt.elems());
+  check(cudaMemcpy(buf.data(), src, tt.bytes(), cudaMemcpyDeviceToHost), "read_tensor");
+  for (long i = 0; i < tt.elems(); ++i) host[i] = bf16_to_float(buf[i]);
+}
+
+void Net::read_bn_running(int o, float* mean, float* var) const {
+  const Op& op = ops_.at(o);
+  if (op.bn < 0) throw std::invalid_argument("op has no batch norm");
+  const BNState& b = bns_[op.bn];
+  check(cudaMemcpy(mean, d_state_ + b.run_mean, b.C * 4, cudaMemcpyDeviceToHost), "bn state");
+  check(cudaMemcpy(var, d_state_ + b.run_var, b.C * 4, cudaMemcpyDeviceToHost), "bn state");
+}
+
+// ============================================================ addressing
+void* Net::tptr(int t) const {
+  if (t == input_t_) return d_input_;
+  if (t == loss_t_) return d_loss_;
+  if (slot_[t] < 0) throw std::runtime_error("tensor has no arena slot: " + tensors_[t].name);
+  return d_arena_ + slot_[t];
+}
+
+__nv_bfloat16* Net::gptr(int t) const {
+  if (grad_slot_[t] < 0) return nullptr;
+  return reinterpret_cast<__nv_bfloat16*>(d_grad_arena_ + grad_slot_[t]);
+}
+
+void Net::gemm(const rfk::GemmDesc& d, cudaStream_t st) { check(rfk::gemm_launch(d, st), "gemm"); }
+
+// ============================================================ op dispatch
+void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
+  uint8_t* ws = d_ws_;
+  __nv_bfloat16* ws_im2col = reinterpret_cast<__nv_bfloat16*>(ws);
+  float* ws_part = reinterpret_cast<float*>(ws + ws_im2col_);
+  float* ws_stats = reinterpret_cast<float*>(ws + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_);
+  switch (op.kind) {
+    case OpKind::Conv: {
+      const Tensor& x = tensors_[op.in[0]];
+      const Tensor& y = tensors_[op.out];
+      const Param& w = params_[op.w_param];
+      rfk::GemmDesc d;
+      d.M = (int)y.rows();
+      d.N = op.cout;
+      d.out = tptr(op.out);
+      d.ldc = op.cout;
+      d.b_kind = rfk::Operand::KMajor2D;
+      d.b = d_bf16_ + w.bf16_off;
+      if (op.explicit_im2col) {
+        rfk::ConvShape cs{x.N, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
+        check(rfk::im2col(tb(op.in[0]), cs, op.kpad, ws_im2col, st), "im2col");
+        d.a_kind = rfk::Operand::KMajor2D;
+        d.a = ws_im2col;
+        d.a_ld = op.kpad;
+        d.K = op.kpad;
+        d.b_ld = op.kpad;
+      } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0) {
+        d.a_kind = rfk::Operand::KMajor2D;
+        d.a = tptr(op.in[0]);
+        d.a_ld = op.cin;
+        d.K = op.cin;
+        d.b_ld = op.cpad;
+      } else {
+        d.a_kind = rfk::Operand::Im2colK;
+        d.a = tptr(op.in[0]);
+        d.a_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad, op.stride, op.stride};
+        d.K = op.R * op.S * op.cpad;
+        d.b_ld = (long)op.R * op.S * op.cpad;
+      }
+      if (op.fuse_stats && !reforward) d.stats = ws_stats + op.stats_off;
+      gemm(d, st);
+      break;
+    }
+    case OpKind::BN:
+    case OpKind::BNAddReLU: {
+      const Tensor& y = tensors_[op.in[0]];
+      const BNState& b = bns_[op.bn];
+      float* S = d_state_;
+      if (phase == 1) {  // residual add, phase 1: out <- skip (exact copy)
+        check(cudaMemcpyAsync(tptr(op.out), tptr(op.in[1]), y.bytes(), cudaMemcpyDeviceToDevice, st), "skip copy");
+        break;
+      }
+      if (!reforward) {
+        const Op& prod = ops_[y.producer];
+        const float* partials;
+        int parts;
+        if (prod.kind == OpKind::Conv && prod.fuse_stats) {
+          partials = ws_stats + prod.stats_off;
+          parts = (int)((y.rows() + 127) / 128);
+        } else {
+          parts = rfk::colstats_blocks(y.rows());
+          check(rfk::colstats(tb(op.in[0]), y.rows(), y.C, ws_part, parts, st), "colstats");
+          partials = ws_part;
+        }
+        check(rfk::bn_finalize(partials, parts, y.C, y.rows(), d_param_ + params_[op.w_param].offset,
+                               d_param_ + params_[op.b_param].offset, op.eps, S + b.mean, S + b.invstd, S + b.scale,
+                               S + b.shift, S + b.run_mean, S + b.run_var, op.momentum, true, st),
+              "bn_finalize");
+      }
+      const bool relu = op.kind == OpKind::BNAddReLU || op.k == 1;
+      const __nv_bfloat16* skip = op.kind == OpKind::BNAddReLU ? tb(op.in[1]) : nullptr;
+      if (phase == 2) skip = tb(op.out);  // phase 1 already placed the skip in the output slot
+      check(rfk::bn_apply(tb(op.in[0]), skip, S + b.scale, S + b.shift, relu, y.rows(), y.C, tb(op.out), st),
+            "bn_apply");
+      break;
+    }
+    case OpKind::ReLU:
+      check(rfk::relu_fwd(tb(op.in[0]), tensors_[op.out].elems(), tb(op.out), st), "relu");
+      break;
+    case OpKind::MaxPool: {
+      const Tensor& x = tensors_[op.in[0]];
+      const Tensor& y = tensors_[op.out];
+      rfk::PoolGeom g{x.N, x.H, x.W, x.C, y.H, y.W, op.k, op.stride, op.pad};
+      check(rfk::maxpool_fwd(tb(op.in[0]), g, tb(op.out), st), "maxpool");
+      break;
+    }
+    case OpKind::AvgPool: {
+      const Tensor& x = tensors_[op.in[0]];
+      check(rfk::avgpool_fwd(tb(op.in[0]), x.N, x.H * x.W, x.C, tb(op.out), st), "avgpool");
+      break;
+    }
+    case OpKind::FC: {
+      const Param& w = params_[op.w_param];
+      rfk::GemmDesc d;
+      d.M = batch_;
+      d.N = op.classes;
+      d.K = op.cin;
+      d.a_kind = rfk::Operand::KMajor2D;
+      d.a = tptr(op.in[0]);
+      d.a_ld = op.cin;
+      d.b_kind = rfk::Operand::KMajor2D;
+      d.b = d_bf16_ + w.bf16_off;
+      d.b_ld = op.cin;
+      d.out = tptr(op.out);
+      d.ldc = op.classes;
+      d.out_f32 = true;
+      d.bias = d_param_ + params_[op.b_param].offset;
+      gemm(d, st);
+      break;
+    }
+    case OpKind::Concat: {
+      const Tensor& a = tensors_[op.in[0]];
+      const Tensor& b2 = tensors_[op.in[1]];
+      check(rfk::concat(phase == 2 ? nullptr : tb(op.in[0]), a.C, phase == 1 ? nullptr : tb(op.in[1]), b2.C, a.rows(),
+                        tb(op.out), st),
+            "concat");
+      break;
+    }
+    case OpKind::Loss:
+      check(rfk::softmax_ce_fwd(static_cast<const float*>(tptr(op.in[0])), d_labels_, batch_, op.classes, d_rowloss_,
+                                d_lse_, d_loss_, st),
+            "loss");
+      break;
+    case OpKind::Input:
+      break;
+  }
+}
+
+void Net::op_backward(const Op& op, cudaStream_t st) {
+  const int oid = (int)(&op - &ops_[0]);
+  auto acc = [&](int i) { return grad_acc_[grad_acc_base_[oid] + i] != 0; };
+  uint8_t* ws = d_ws_;
+  __nv_bfloat16* ws_im2col = reinterpret_cast<__nv_bfloat16*>(ws);
+  float* ws_part = reinterpret_cast<float*>(ws + ws_im2col_);
+  __nv_bfloat16* ws_zero = reinterpret_cast<__nv_bfloat16*>(ws + ws_im2col_ + ws_partials_);
+  float* ws_split = reinterpret_cast<float*>(ws + ws_im2col_ + ws_partials_ + ws_zero_);
+  __nv_bfloat16* ws_misc =
+      reinterpret_cast<__nv_bfloat16*>(ws + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_);
+  switch (op.kind) {
+    case OpKind::Conv: {
+      const Tensor& x = tensors_[op.in[0]];
+      const Tensor& y = tensors_[op.out];
+      const Param& w = params_[op.w_param];
+      const __nv_bfloat16* dy = gptr(op.out);
+      // ---- dgrad
+      __nv_bfloat16* dx = gptr(op.in[0]);
+      if (op.in[0] != input_t_ && dx) {
+        if (op.explicit_im2col) throw std::runtime_error("dgrad of an explicit-im2col conv is not supported");
+        rfk::GemmDesc d;
+        d.N = op.cin;
+        d.b_kind = rfk::Operand::KMajor2D;
+        d.b = d_bf16_ + w.wt_off;
+        d.out = dx;
+        d.ldc = op.cin;
+        d.accumulate_out = acc(0);
+        if (op.R == 1 && op.S == 1 && op.pad == 0) {
+          d.M = (int)y.rows();
+          d.K = op.cout;
+          d.a_kind = rfk::Operand::KMajor2D;
+          d.a = dy;
+          d.a_ld = op.cout;
+          d.b_ld = op.coutpad;
+          if (op.stride > 1) {
+            if (!acc(0)) check(cudaMemsetAsync(dx, 0, x.bytes(), st), "memset");
+            d.accumulate_out = acc(0);
+            d.remap = true;
+            d.rP = y.H;
+            d.rQ = y.W;
+            d.rH = x.H;
+            d.rW = x.W;
+            d.rsh = d.rsw = op.stride;
+          }
+        } else {
+          d.M = (int)x.rows();
+          d.K = op.R * op.S * op.coutpad;
+          d.b_ld = (long)op.R * op.S * op.coutpad;
+          d.a_kind = rfk::Operand::Im2colK;
+          const int pd = op.R - 1 - op.pad;
+          if (op.stride == 1) {
+            d.a = dy;
+            d.a_geom = rfk::ConvGeom{y.N, y.H, y.W, op.cout, x.H, x.W, op.R, op.S, pd, pd, 1, 1};
+          } else {
+            const int Hu = x.H - op.R + 1 + 2 * op.pad, Wu = x.W - op.S + 1 + 2 * op.pad;
+            check(rfk::zero_insert(dy, y.N, y.H, y.W, op.cout, Hu, Wu, op.stride, ws_zero, st), "zero_insert");
+            d.a = ws_zero;
+            d.a_geom = rfk::ConvGeom{y.N, Hu, Wu, op.cout, x.H, x.W, op.R, op.S, pd, pd, 1, 1};
+          }
+        }
+        gemm(d, st);
+      }
+      // ---- wgrad
+      const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
+      float* dW = d_grad_ + w.offset;
+      rfk::GemmDesc d;
+      d.M = op.cout;
+      d.N = (int)kw;
+      d.K = (int)y.rows();
+      d.a_kind = rfk::Operand::MNMajor2D;
+      d.a = dy;
+      d.a_ld = op.cout;
+      d.out_f32 = true;
+      d.ldc = kw;
+      d.block_n = op.wg_bn;
+      if (op.explicit_im2col) {
+        rfk::ConvShape cs{x.N, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
+        check(rfk::im2col(tb(op.in[0]), cs, op.kpad, ws_im2col, st), "im2col");
+        d.b_kind = rfk::Operand::MNMajor2D;
+        d.b = ws_im2col;
+        d.b_ld = op.kpad;
+      } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0) {
+        d.b_kind = rfk::Operand::MNMajor2D;
+        d.b = tptr(op.in[0]);
+        d.b_ld = op.cin;
+        d.b_extent = op.cin;
+      } else {
+        d.b_kind = rfk::Operand::Im2colMN;
+        d.b = tptr(op.in[0]);
+        d.b_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad, op.stride, op.stride};
+      }
+      if (op.wg_splits > 1) {
+        d.splits = op.wg_splits;
+        d.out = ws_split;
+        d.split_stride = (long)op.cout * kw;
+        gemm(d, st);
+        check(rfk::reduce_splits(ws_split, op.wg_splits, (long)op.cout * kw, dW, false, st), "reduce_splits");
+      } else {
+        d.out = dW;
+        gemm(d, st);
+      }
+      break;
+    }
+    case OpKind::BN:
+    case OpKind::BNAddReLU: {
+      const Tensor& y = tensors_[op.in[0]];
+      const BNState& b = bns_[op.bn];
+      float* S = d_state_;
+      const bool add = op.kind == OpKind::BNAddReLU;
+      const int mode = add ? 2 : (op.k == 1 ? 1 : 0);
+      const int blocks = rfk::colstats_blocks(y.rows());
+      __nv_bfloat16* dskip = add ? gptr(op.in[1]) : nullptr;
+      check(rfk::bn_backward(tb(op.in[0]), gptr(op.out), add ? tb(op.out) : nullptr, mode,
+                             d_param_ + params_[op.w_param].offset, S + b.mean, S + b.invstd, S + b.scale,
+                             S + b.shift, y.rows(), y.C, ws_part, blocks, S + b.coef,
+                             d_grad_ + params_[op.w_param].offset, d_grad_ + params_[op.b_param].offset,
+                             gptr(op.in[0]), acc(0), dskip, add ? acc(1) : false, st),
+            "bn_backward");
+      break;
+    }
+    case OpKind::ReLU:
+      check(rfk::relu_bwd(tb(op.out), gptr(op.out), tensors_[op.out].elems(), gptr(op.in[0]), acc(0), st),
+            "relu_bwd");
+      break;
+    case OpKind::MaxPool: {
+      const Tensor& x = tensors_[op.in[0]];
+      const Tensor& y = tensors_[op.out];
+      rfk::PoolGeom g{x.N, x.H, x.W, x.C, y.H, y.W, op.k, op.stride, op.pad};
+      check(rfk::maxpool_bwd(tb(op.in[0]), tb(op.out), gptr(op.out), g, gptr(op.in[0]), acc(0), st), "maxpool_bwd");
+      break;
+    }
+    case OpKind::AvgPool: {
+      const Tensor& x = tensors_[op.in[0]];
+      check(rfk::avgpool_bwd(gptr(op.out), x.N, x.H * x.W, x.C, gptr(op.in[0]), acc(0), st), "avgpool_bwd");
+      break;
+    }
+    case OpKind::FC: {
+      const Param& w = params_[op.w_param];
+      const float* dlog = reinterpret_cast<const float*>(gptr(op.out));
+      const int ldd = round8(op.classes);
+      // bf16 copy of dlogits with 16-byte aligned rows for TMA
+      check(cudaMemsetAsync(ws_misc, 0, (long)batch_ * ldd * 2, st), "memset");
+      check(rfk::cast_f32_bf16_2d(dlog, batch_, op.classes, ldd, ws_misc, st), "cast");
+      check(rfk::colsum_f32(dlog, batch_, op.classes, d_grad_ + params_[op.b_param].offset, false, st), "db");
+      __nv_bfloat16* dx = gptr(op.in[0]);
+      if (dx) {
+        rfk::GemmDesc d;
+        d.M = batch_;
+        d.N = op.cin;
+        d.K = op.classes;
+        d.a_kind = rfk::Operand::KMajor2D;
+        d.a = ws_misc;
+        d.a_ld = ldd;
+        d.b_kind = rfk::Operand::MNMajor2D;
+        d.b = d_bf16_ + w.bf16_off;
+        d.b_ld = op.cin;
+        d.out = dx;
+        d.ldc = op.cin;
+        d.accumulate_out = acc(0);
+        gemm(d, st);
+      }
+      rfk::GemmDesc d;
+      d.M = op.classes;
+      d.N = op.cin;
+      d.K = batch_;
+      d.a_kind = rfk::Operand::MNMajor2D;
+      d.a = ws_misc;
+      d.a_ld = ldd;
+      d.b_kind = rfk::Operand::MNMajor2D;
+      d.b = tptr(op.in[0]);
+      d.b_ld = op.cin;
+      d.out = d_grad_ + w.offset;
+      d.ldc = op.cin;
+      d.out_f32 = true;
+      gemm(d, st);
+      break;
+    }
+    case OpKind::Concat: {
+      const Tensor& a = tensors_[op.in[0]];
+      const Tensor& b2 = tensors_[op.in[1]];
+      check(rfk::split_grad(gptr(op.out), a.C, b2.C, a.rows(), gptr(op.in[0]), acc(0), gptr(op.in[1]), acc(1), st),
+            "split_grad");
+      break;
+    }
+    case OpKind::Loss:
+      check(rfk::softmax_ce_bwd(static_cast<const float*>(tptr(op.in[0])), d_labels_, d_lse_, batch_, op.classes,
+                                reinterpret_cast<float*>(gptr(op.in[0])), st),
+            "loss_bwd");
+      break;
+    case OpKind::Input:
+      break;
+  }
+}
+
+void Net::run_instr(const Instr& ins, cudaStream_t st) {
+  if (ins.kind == InstrKind::Forward) op_forward(ops_[ins.op], ins.reforward, ins.phase, st);
+  else if (ins.kind == InstrKind::Backward) op_backward(ops_[ins.op], st);
+}
+
+// ============================================================ step
+void Net::prep_weights(cudaStream_t st) {
+  for (const auto& p : params_) {
+    const Op& op = ops_[p.op];
+    if (p.kind == 0) {
+      if (op.explicit_im2col)
+        check(rfk::conv_weight_prep(d_param_ + p.offset, op.cout, 1, 1, op.kpad, op.kpad, op.coutpad,
+                                    d_bf16_ + p.bf16_off, nullptr, st),
+              "weight prep");
+      else
+        check(rfk::conv_weight_prep(d_param_ + p.offset, op.cout, op.R, op.S, op.cpad, op.cin, op.coutpad,
+                                    d_bf16_ + p.bf16_off, d_bf16_ + p.wt_off, st),
+              "weight prep");
+    } else if (p.kind == 3) {
+      check(rfk::cast_f32_bf16(d_param_ + p.offset, p.count, d_bf16_ + p.bf16_off, st), "fc weight cast");
+    }
+  }
+}
+
+void Net::load_batch(const float* images, const int* labels, bool from_host, cudaStream_t st) {
+  if (!setup_done_) throw std::invalid_argument("setup the network first");
+  const Tensor& in = tensors_[input_t_];
+  const long nimg = (long)batch_ * in_c_real_ * in.H * in.W;
+  const float* src = images;
+  if (from_host) {
+    check(cudaMemcpyAsync(d_images_, images, nimg * 4, cudaMemcpyHostToDevice, st), "h2d images");
+    src = d_images_;
+  }
+  check(cudaMemcpyAsync(d_labels_, labels, batch_ * 4, from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                        st),
+        "labels");
+  check(rfk::pack_input(src, batch_, in_c_real_, in.H, in.W, in.C, d_input_, st), "pack_input");
+}
+
+void Net::forward_backward(cudaStream_t st) {
+  if (!setup_done_) throw std::invalid_argument("setup the network first");
+  for (const auto& ins : sched_) run_instr(ins, st);
+}
+
+void Net::update(float lr, float momentum, float wd, cudaStream_t st) {
+  check(rfk::sgd_update(d_param_, d_grad_, d_mom_, n_params_, lr, momentum, wd, st), "sgd");
+  prep_weights(st);
+}
+
+void Net::step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph) {
+  if (!use_graph) {
+    forward_backward(st);
+    update(lr, momentum, wd, st);
+    return;
+  }
+  if (!graph_exec_ || lr != graph_lr_ || momentum != graph_mom_ || wd != graph_wd_) {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+    cudaStream_t cap;
+    check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream");
+    check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+    forward_backward(cap);
+    update(lr, momentum, wd, cap);
+    cudaGraph_t g;
+    check(cudaStreamEndCapture(cap, &g), "end capture");
+    size_t nn = 0;
+    check(cudaGraphGetNodes(g, nullptr, &nn), "graph nodes");
+    std::vector<cudaGraphNode_t> nodes(nn);
+    check(cudaGraphGetNodes(g, nodes.data(), &nn), "graph nodes");
+    long kernels = 0;
+    for (auto n : nodes) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(n, &t);
+      if (t == cudaGraphNodeTypeKernel) ++kernels;
+    }
+    rep_.launches_per_step = kernels;
+    check(cudaGraphInstantiate(&graph_exec_, g, 0), "instantiate");
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    graph_lr_ = lr;
+    graph_mom_ = momentum;
+    graph_wd_ = wd;
+  }
+  check(cudaGraphLaunch(graph_exec_, st), "graph launch");
+}
+
+float Net::read_loss(cudaStream_t st) {
+  float v = 0.f;
+  check(cudaMemcpyAsync(&v, d_loss_, 4, cudaMemcpyDeviceToHost, st), "loss d2h");
+  check(cudaStreamSynchronize(st), "sync");
+  return v;
+}
+
+}  // namespace rfx

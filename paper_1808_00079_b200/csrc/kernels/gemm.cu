@@ -236,6 +236,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         } else {
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long)blockIdx.z * p.split_stride +
                                out_row * p.ldc + col0;
+          if (p.accumulate_out) {
+            if (col0 + 32 <= p.N) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 8) {
+                const uint4 o = *reinterpret_cast<const uint4*>(dst + i);
+                const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&o);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float2 f = __bfloat1622float2(ob[j]);
+                  v[i + 2 * j] += f.x;
+                  v[i + 2 * j + 1] += f.y;
+                }
+              }
+            } else {
+              for (int i = 0; i < 32 && col0 + i < p.N; ++i) v[i] += __bfloat162float(dst[i]);
+            }
+          }
           if (col0 + 32 <= p.N) {
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
@@ -416,7 +433,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
                      64, bn);
       break;
     case Operand::MNMajor2D:
-      ok = encode_2d(&kp.tb, d.b, d.N, d.K, d.b_ld, 64, 64);
+      ok = encode_2d(&kp.tb, d.b, d.b_extent > 0 ? d.b_extent : d.N, d.K, d.b_ld, 64, 64);
       break;
     case Operand::Im2colMN:
       geo = &d.b_geom;

@@ -38,11 +38,12 @@ struct GemmDesc {
   const void* b = nullptr;
   long b_ld = 0;
   ConvGeom b_geom;
+  long b_extent = 0;  // valid MN extent of an MN-major B (0 = N)
   // epilogue
   void* out = nullptr;
   long ldc = 0;
   bool out_f32 = false;
-  bool accumulate_out = false;  // out += D (fp32 only)
+  bool accumulate_out = false;  // out += D (fp32 or bf16)
   const float* bias = nullptr;  // per column
   float* stats = nullptr;       // [m_tiles][2][N] column sum / sum of squares
   int splits = 1;               // split-K; split z writes out + z * split_stride

@@ -1,0 +1,897 @@
+// HBM-streaming kernels of the train step (everything that is not a dense
+// contraction): BatchNorm statistics / apply / backward, ReLU, pooling,
+// softmax cross-entropy, SGD, weight layout transforms, input packing.
+//
+// All activations are NHWC bf16 with C % 8 == 0, so one 16-byte vector is 8
+// consecutive channels of one pixel.  Every reduction is a fixed-shape tree
+// (no atomics): results are bit-reproducible run to run, which is what makes
+// re-forward gradients bit-identical to store-all gradients.
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "kernels/ops.h"
+
+namespace rfk {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+
+__device__ __forceinline__ uint4 ldg16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+
+int grid_for(long work, int per_block, int cap = 148 * 16) {
+  long g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<int>(g);
+}
+
+// ------------------------------------------------------------ column reductions
+// Layout of a reduction launch over an [M, C] bf16 matrix: a block owns a
+// contiguous slab of rows; its threads are arranged as (rows_per_pass x tpr)
+// with tpr = C / 8 vector lanes per row.  Each thread accumulates its 8
+// channels over its rows; threads sharing channels are then summed in smem in
+// a fixed order and the block writes partials[block][2][C].
+struct RedShape {
+  int tpr;            // threads per row (C / 8), <= 256
+  int rows_per_pass;  // 256 / tpr
+};
+
+__device__ __forceinline__ RedShape red_shape(int C) {
+  RedShape s;
+  s.tpr = C / 8;
+  s.rows_per_pass = kThreads / s.tpr;
+  return s;
+}
+
+// mode: 0 = plain column sum / sum of squares of x
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) colstats_kernel(const __nv_bfloat16* __restrict__ x, long M, int C,
+                                                            long rows_per_block, float* __restrict__ partials) {
+  // handles C <= 2048 per pass; channel chunks via blockIdx.y
+  __shared__ float sh[2][kThreads][8];
+  const int cchunk = blockIdx.y;  // chunk of 2048 channels
+  const int Cc = min(2048, C - cchunk * 2048);
+  const RedShape s = red_shape(Cc);
+  const int t = threadIdx.x;
+  const int lane = t % s.tpr, rgrp = t / s.tpr;
+  float a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = b[i] = 0.f;
+  const long r0 = (long)blockIdx.x * rows_per_block;
+  const long r1 = min(M, r0 + rows_per_block);
+  if (rgrp < s.rows_per_pass) {
+    for (long r = r0 + rgrp; r < r1; r += s.rows_per_pass) {
+      float f[8];
+      unpack8(ldg16(x + r * C + cchunk * 2048 + lane * 8), f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        a[i] += f[i];
+        b[i] += f[i] * f[i];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    sh[0][t][i] = a[i];
+    sh[1][t][i] = b[i];
+  }
+  __syncthreads();
+  if (t < s.tpr) {
+    for (int g = 1; g < s.rows_per_pass; ++g)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        a[i] += sh[0][g * s.tpr + t][i];
+        b[i] += sh[1][g * s.tpr + t][i];
+      }
+    float* out = partials + (long)blockIdx.x * 2 * C + cchunk * 2048 + t * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      out[i] = a[i];
+      out[C + i] = b[i];
+    }
+  }
+}
+
+// Sum `parts` partial rows [parts][2][C] in a fixed tree: channel per
+// threadIdx.x (32 wide), partial subsets per threadIdx.y (8 deep).
+__device__ __forceinline__ void sum_partials(const float* __restrict__ partials, int parts, int C, int c, float& s0,
+                                             float& s1) {
+  __shared__ float sh0[8][33], sh1[8][33];
+  float a = 0.f, b = 0.f;
+  if (c < C)
+    for (int p = threadIdx.y; p < parts; p += 8) {
+      a += partials[(long)p * 2 * C + c];
+      b += partials[(long)p * 2 * C + C + c];
+    }
+  sh0[threadIdx.y][threadIdx.x] = a;
+  sh1[threadIdx.y][threadIdx.x] = b;
+  __syncthreads();
+  s0 = ((sh0[0][threadIdx.x] + sh0[1][threadIdx.x]) + (sh0[2][threadIdx.x] + sh0[3][threadIdx.x])) +
+       ((sh0[4][threadIdx.x] + sh0[5][threadIdx.x]) + (sh0[6][threadIdx.x] + sh0[7][threadIdx.x]));
+  s1 = ((sh1[0][threadIdx.x] + sh1[1][threadIdx.x]) + (sh1[2][threadIdx.x] + sh1[3][threadIdx.x])) +
+       ((sh1[4][threadIdx.x] + sh1[5][threadIdx.x]) + (sh1[6][threadIdx.x] + sh1[7][threadIdx.x]));
+}
+
+__global__ void bn_finalize_kernel(const float* __restrict__ partials, int parts, int C, float count,
+                                   const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                                   float* __restrict__ mean, float* __restrict__ invstd, float* __restrict__ scale,
+                                   float* __restrict__ shift, float* __restrict__ run_mean, float* __restrict__ run_var,
+                                   float momentum, int update_running) {
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  float s0, s1;
+  sum_partials(partials, parts, C, c, s0, s1);
+  if (threadIdx.y != 0 || c >= C) return;
+  const float mu = s0 / count;
+  const float var = fmaxf(s1 / count - mu * mu, 0.f);
+  const float is = rsqrtf(var + eps);
+  mean[c] = mu;
+  invstd[c] = is;
+  const float sc = gamma[c] * is;
+  scale[c] = sc;
+  shift[c] = beta[c] - mu * sc;
+  if (update_running) {
+    const float unbiased = count > 1.f ? var * count / (count - 1.f) : var;
+    run_mean[c] = (1.f - momentum) * run_mean[c] + momentum * mu;
+    run_var[c] = (1.f - momentum) * run_var[c] + momentum * unbiased;
+  }
+}
+
+// out = [relu](y * scale + shift [+ skip])
+// (skip may alias out: each element is read before it is written)
+__global__ void __launch_bounds__(kThreads) bn_apply_kernel(const __nv_bfloat16* __restrict__ y,
+                                                           const __nv_bfloat16* skip, const float* __restrict__ scale,
+                                                           const float* __restrict__ shift, int relu, long nvec, int C,
+                                                           __nv_bfloat16* out) {
+  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    const int c0 = (int)((v * 8) % C);
+    float f[8];
+    unpack8(ldg16(y + v * 8), f);
+    float k[8];
+    if (skip) unpack8(*reinterpret_cast<const uint4*>(skip + v * 8), k);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float o = f[i] * __ldg(scale + c0 + i) + __ldg(shift + c0 + i);
+      if (skip) o += k[i];
+      f[i] = relu ? fmaxf(o, 0.f) : o;
+    }
+    *reinterpret_cast<uint4*>(out + v * 8) = pack8(f);
+  }
+}
+
+// Backward reduction: g = dout * mask, accumulate sum(g) and sum(g * xhat).
+// mask mode: 0 none, 1 relu of (y*scale+shift), 2 relu of stored output (out>0)
+__global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(
+    const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
+    int mask_mode, const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ scale,
+    const float* __restrict__ shift, long M, int C, long rows_per_block, float* __restrict__ partials) {
+  __shared__ float sh[2][kThreads][8];
+  const int cchunk = blockIdx.y;
+  const int Cc = min(2048, C - cchunk * 2048);
+  const RedShape s = red_shape(Cc);
+  const int t = threadIdx.x;
+  const int lane = t % s.tpr, rgrp = t / s.tpr;
+  const int c0 = cchunk * 2048 + lane * 8;
+  float a[8], b[8], mu[8], is[8], sc[8], sf[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = b[i] = 0.f;
+    if (rgrp < s.rows_per_pass) {
+      mu[i] = mean[c0 + i];
+      is[i] = invstd[c0 + i];
+      sc[i] = scale[c0 + i];
+      sf[i] = shift[c0 + i];
+    }
+  }
+  const long r0 = (long)blockIdx.x * rows_per_block;
+  const long r1 = min(M, r0 + rows_per_block);
+  if (rgrp < s.rows_per_pass) {
+    for (long r = r0 + rgrp; r < r1; r += s.rows_per_pass) {
+      const long off = r * C + c0;
+      float fy[8], fd[8], fo[8];
+      unpack8(ldg16(y + off), fy);
+      unpack8(ldg16(dout + off), fd);
+      if (mask_mode == 2) unpack8(ldg16(out + off), fo);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float g = fd[i];
+        if (mask_mode == 1) g = (fy[i] * sc[i] + sf[i] > 0.f) ? g : 0.f;
+        if (mask_mode == 2) g = (fo[i] > 0.f) ? g : 0.f;
+        a[i] += g;
+        b[i] += g * (fy[i] - mu[i]) * is[i];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    sh[0][t][i] = a[i];
+    sh[1][t][i] = b[i];
+  }
+  __syncthreads();
+  if (t < s.tpr) {
+    for (int gi = 1; gi < s.rows_per_pass; ++gi)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        a[i] += sh[0][gi * s.tpr + t][i];
+        b[i] += sh[1][gi * s.tpr + t][i];
+      }
+    float* o = partials + (long)blockIdx.x * 2 * C + cchunk * 2048 + t * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      o[i] = a[i];
+      o[C + i] = b[i];
+    }
+  }
+}
+
+// dbeta = sum g, dgamma = sum g*xhat; dy = k1*g + k2*y + k3
+__global__ void bn_bwd_finalize_kernel(const float* __restrict__ partials, int parts, int C, float count,
+                                       const float* __restrict__ gamma, const float* __restrict__ mean,
+                                       const float* __restrict__ invstd, float* __restrict__ dgamma,
+                                       float* __restrict__ dbeta, float* __restrict__ coef) {
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  float sg, sgx;
+  sum_partials(partials, parts, C, c, sg, sgx);
+  if (threadIdx.y != 0 || c >= C) return;
+  dbeta[c] = sg;
+  dgamma[c] = sgx;
+  const float is = invstd[c];
+  const float k1 = gamma[c] * is;
+  const float k2 = -k1 * is * sgx / count;
+  const float k3 = -k1 * sg / count - k2 * mean[c];
+  coef[c] = k1;
+  coef[C + c] = k2;
+  coef[2 * C + c] = k3;
+}
+
+__global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(
+    const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
+    int mask_mode, const float* __restrict__ scale, const float* __restrict__ shift, const float* __restrict__ coef,
+    long nvec, int C, __nv_bfloat16* __restrict__ dy, int acc_dy, __nv_bfloat16* __restrict__ dskip, int acc_dskip) {
+  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    const int c0 = (int)((v * 8) % C);
+    const long off = v * 8;
+    float fy[8], fd[8], fo[8], r[8], sk[8];
+    unpack8(ldg16(y + off), fy);
+    unpack8(ldg16(dout + off), fd);
+    if (mask_mode == 2) unpack8(ldg16(out + off), fo);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float g = fd[i];
+      if (mask_mode == 1) g = (fy[i] * __ldg(scale + c0 + i) + __ldg(shift + c0 + i) > 0.f) ? g : 0.f;
+      if (mask_mode == 2) g = (fo[i] > 0.f) ? g : 0.f;
+      sk[i] = g;
+      r[i] = __ldg(coef + c0 + i) * g + __ldg(coef + C + c0 + i) * fy[i] + __ldg(coef + 2 * C + c0 + i);
+    }
+    if (acc_dy) {
+      float prev[8];
+      unpack8(*reinterpret_cast<const uint4*>(dy + off), prev);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) r[i] += prev[i];
+    }
+    *reinterpret_cast<uint4*>(dy + off) = pack8(r);
+    if (dskip) {
+      if (acc_dskip) {
+        float prev[8];
+        unpack8(*reinterpret_cast<const uint4*>(dskip + off), prev);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sk[i] += prev[i];
+      }
+      *reinterpret_cast<uint4*>(dskip + off) = pack8(sk);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) relu_fwd_kernel(const __nv_bfloat16* __restrict__ x, long nvec,
+                                                           __nv_bfloat16* __restrict__ y) {
+  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    float f[8];
+    unpack8(ldg16(x + v * 8), f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = fmaxf(f[i], 0.f);
+    *reinterpret_cast<uint4*>(y + v * 8) = pack8(f);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) relu_bwd_kernel(const __nv_bfloat16* __restrict__ y,
+                                                           const __nv_bfloat16* __restrict__ dy, long nvec,
+                                                           __nv_bfloat16* __restrict__ dx, int acc) {
+  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    float fy[8], fd[8];
+    unpack8(ldg16(y + v * 8), fy);
+    unpack8(ldg16(dy + v * 8), fd);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) fd[i] = fy[i] > 0.f ? fd[i] : 0.f;
+    if (acc) {
+      float p[8];
+      unpack8(*reinterpret_cast<const uint4*>(dx + v * 8), p);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fd[i] += p[i];
+    }
+    *reinterpret_cast<uint4*>(dx + v * 8) = pack8(fd);
+  }
+}
+
+// ------------------------------------------------------------ pooling
+__global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, PoolGeom g,
+                                                              __nv_bfloat16* __restrict__ y) {
+  const int cv = g.C / 8;
+  const long total = (long)g.N * g.P * g.Q * cv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    long t = i / cv;
+    const int q = (int)(t % g.Q);
+    t /= g.Q;
+    const int p = (int)(t % g.P);
+    const int n = (int)(t / g.P);
+    float m[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = -INFINITY;
+    for (int r = 0; r < g.k; ++r) {
+      const int h = p * g.stride - g.pad + r;
+      if (h < 0 || h >= g.H) continue;
+      for (int s = 0; s < g.k; ++s) {
+        const int w = q * g.stride - g.pad + s;
+        if (w < 0 || w >= g.W) continue;
+        float f[8];
+        unpack8(ldg16(x + (((long)n * g.H + h) * g.W + w) * g.C + c8 * 8), f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m[k] = fmaxf(m[k], f[k]);
+      }
+    }
+    *reinterpret_cast<uint4*>(y + i * 8) = pack8(m);
+  }
+}
+
+// Gather form: each input element collects dy from every window whose first
+// maximum it is (windows scanned in row-major order, ties to the first hit).
+__global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ y,
+                                                              const __nv_bfloat16* __restrict__ dy, PoolGeom g,
+                                                              __nv_bfloat16* __restrict__ dx, int acc) {
+  const int cv = g.C / 8;
+  const long total = (long)g.N * g.H * g.W * cv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    long t = i / cv;
+    const int w = (int)(t % g.W);
+    t /= g.W;
+    const int h = (int)(t % g.H);
+    const int n = (int)(t / g.H);
+    float xv[8], acc_v[8];
+    unpack8(ldg16(x + i * 8), xv);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc_v[k] = 0.f;
+    // windows p with p*stride - pad <= h <= p*stride - pad + k - 1
+    const int p_lo = max(0, (h + g.pad - g.k + g.stride) / g.stride);
+    const int p_hi = min(g.P - 1, (h + g.pad) / g.stride);
+    const int q_lo = max(0, (w + g.pad - g.k + g.stride) / g.stride);
+    const int q_hi = min(g.Q - 1, (w + g.pad) / g.stride);
+    for (int p = p_lo; p <= p_hi; ++p)
+      for (int q = q_lo; q <= q_hi; ++q) {
+        const long o = (((long)n * g.P + p) * g.Q + q) * g.C + c8 * 8;
+        float yv[8], dv[8];
+        unpack8(ldg16(y + o), yv);
+        unpack8(ldg16(dy + o), dv);
+        // is (h, w) the first position in this window holding the max?
+        bool first[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) first[k] = xv[k] == yv[k];
+        const int h0 = p * g.stride - g.pad, w0 = q * g.stride - g.pad;
+        for (int r = 0; r < g.k; ++r) {
+          const int hh = h0 + r;
+          if (hh < 0 || hh >= g.H) continue;
+          for (int s = 0; s < g.k; ++s) {
+            const int ww = w0 + s;
+            if (ww < 0 || ww >= g.W) continue;
+            if (hh > h || (hh == h && ww >= w)) {
+              r = g.k;
+              break;
+            }
+            float e[8];
+            unpack8(ldg16(x + (((long)n * g.H + hh) * g.W + ww) * g.C + c8 * 8), e);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (e[k] == yv[k]) first[k] = false;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (first[k]) acc_v[k] += dv[k];
+      }
+    if (acc) {
+      float pv[8];
+      unpack8(*reinterpret_cast<const uint4*>(dx + i * 8), pv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc_v[k] += pv[k];
+    }
+    *reinterpret_cast<uint4*>(dx + i * 8) = pack8(acc_v);
+  }
+}
+
+// global average pool: block per (n, 256-channel chunk); fixed-order sums
+__global__ void __launch_bounds__(kThreads) avgpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int HW, int C,
+                                                              __nv_bfloat16* __restrict__ out) {
+  const int n = blockIdx.x;
+  const int c = blockIdx.y * kThreads + threadIdx.x;
+  if (c >= C) return;
+  float s = 0.f;
+  const __nv_bfloat16* p = x + (long)n * HW * C + c;
+  for (int i = 0; i < HW; ++i) s += __bfloat162float(p[(long)i * C]);
+  out[(long)n * C + c] = __float2bfloat16_rn(s / (float)HW);
+}
+
+__global__ void __launch_bounds__(kThreads) avgpool_bwd_kernel(const __nv_bfloat16* __restrict__ dout, int HW, int C,
+                                                              long nvec, __nv_bfloat16* __restrict__ dx, int acc) {
+  const float inv = 1.f / (float)HW;
+  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    const long e = v * 8;
+    const int c0 = (int)(e % C);
+    const long n = e / ((long)HW * C);
+    float f[8];
+    unpack8(ldg16(dout + n * C + c0), f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] *= inv;
+    if (acc) {
+      float p[8];
+      unpack8(*reinterpret_cast<const uint4*>(dx + e), p);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] += p[i];
+    }
+    *reinterpret_cast<uint4*>(dx + e) = pack8(f);
+  }
+}
+
+// ------------------------------------------------------------ loss
+// One block per row: logsumexp in fp32; lse[n] saved for the backward.
+__global__ void __launch_bounds__(kThreads) softmax_ce_fwd_kernel(const float* __restrict__ logits,
+                                                                 const int* __restrict__ labels, int K,
+                                                                 float* __restrict__ row_loss,
+                                                                 float* __restrict__ lse_out) {
+  __shared__ float red[kThreads];
+  const int n = blockIdx.x;
+  const float* z = logits + (long)n * K;
+  float m = -INFINITY;
+  for (int k = threadIdx.x; k < K; k += kThreads) m = fmaxf(m, z[k]);
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  m = red[0];
+  __syncthreads();
+  float e = 0.f;
+  for (int k = threadIdx.x; k < K; k += kThreads) e += expf(z[k] - m);
+  red[threadIdx.x] = e;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const float lse = m + logf(red[0]);
+    lse_out[n] = lse;
+    row_loss[n] = lse - z[labels[n]];
+  }
+}
+
+__global__ void mean_kernel(const float* __restrict__ v, int n, float* __restrict__ out) {
+  __shared__ float red[kThreads];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += kThreads) s += v[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = kThreads / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0] / (float)n;
+}
+
+// dlogits = (softmax - onehot) / N ; fp32 and a bf16 copy [N, ldb]
+__global__ void __launch_bounds__(kThreads) softmax_ce_bwd_kernel(const float* __restrict__ logits,
+                                                                 const int* __restrict__ labels,
+                                                                 const float* __restrict__ lse, int Nrows, int K,
+                                                                 float* __restrict__ dlogits) {
+  const long total = (long)Nrows * K;
+  const float invn = 1.f / (float)Nrows;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int n = (int)(i / K), k = (int)(i % K);
+    float p = expf(logits[i] - lse[n]);
+    if (k == labels[n]) p -= 1.f;
+    dlogits[i] = p * invn;
+  }
+}
+
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ x, long n, __nv_bfloat16* __restrict__ y) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+
+// fp32 [R, C] -> bf16 [R, ldo] (pad columns untouched)
+__global__ void cast_f32_bf16_2d_kernel(const float* __restrict__ x, int R, int C, int ldo,
+                                        __nv_bfloat16* __restrict__ y) {
+  const long total = (long)R * C;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x)
+    y[(i / C) * ldo + (i % C)] = __float2bfloat16_rn(x[i]);
+}
+
+// column sums of a bf16 [R, C] matrix, fixed order
+__global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ x, int R, int C, float* __restrict__ out,
+                                   int acc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s = 0.f;
+  for (int r = 0; r < R; ++r) s += __bfloat162float(x[(long)r * C + c]);
+  out[c] = acc ? out[c] + s : s;
+}
+
+// column sums of an fp32 [R, C] matrix (bias gradient), fixed order
+__global__ void colsum_f32_kernel(const float* __restrict__ x, int R, int C, float* __restrict__ out, int acc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s = 0.f;
+  for (int r = 0; r < R; ++r) s += x[(long)r * C + c];
+  out[c] = acc ? out[c] + s : s;
+}
+
+// sum of split-K partials [splits][n] -> out (fixed order)
+__global__ void reduce_splits_kernel(const float* __restrict__ parts, int splits, long n, float* __restrict__ out,
+                                     int acc) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += parts[(long)z * n + i];
+    out[i] = acc ? out[i] + s : s;
+  }
+}
+
+// ------------------------------------------------------------ optimizer + layouts
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m, long n, float lr,
+                           float momentum, float wd) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const float d = g[i] + wd * w[i];
+    const float v = momentum * m[i] + d;
+    m[i] = v;
+    w[i] = w[i] - lr * v;
+  }
+}
+
+// fp32 [Cout][R][S][Cpad] -> bf16 same layout, and bf16 flipped transpose
+// Wt[ci][R-1-r][S-1-s][co] with co padded to CoutPad.
+__global__ void conv_weight_prep_kernel(const float* __restrict__ w, int Cout, int R, int S, int Cpad, int Cin,
+                                        int CoutPad, __nv_bfloat16* __restrict__ wb, __nv_bfloat16* __restrict__ wt) {
+  const long total = (long)Cout * R * S * Cpad;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cpad);
+    long t = i / Cpad;
+    const int s = (int)(t % S);
+    t /= S;
+    const int r = (int)(t % R);
+    const int co = (int)(t / R);
+    const __nv_bfloat16 v = __float2bfloat16_rn(w[i]);
+    wb[i] = v;
+    if (wt && c < Cin) wt[(((long)c * R + (R - 1 - r)) * S + (S - 1 - s)) * CoutPad + co] = v;
+  }
+}
+
+// NCHW fp32 -> NHWC bf16 with zero channel padding to Cpad
+__global__ void pack_input_kernel(const float* __restrict__ x, int N, int C, int H, int W, int Cpad,
+                                  __nv_bfloat16* __restrict__ out) {
+  const long total = (long)N * H * W * Cpad;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Cpad);
+    long t = i / Cpad;
+    const int w = (int)(t % W);
+    t /= W;
+    const int h = (int)(t % H);
+    const int n = (int)(t / H);
+    const float v = c < C ? x[(((long)n * C + c) * H + h) * W + w] : 0.f;
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// explicit im2col for thin-channel convs: out[m][k], k = (r*S + s)*C + c, K
+// padded with zeros to Kpad.
+__global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x, ConvShape g, int Kpad,
+                              __nv_bfloat16* __restrict__ out) {
+  const long total = (long)g.N * g.P * g.Q * Kpad;
+  const int Kreal = g.R * g.S * g.C;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int k = (int)(i % Kpad);
+    const long m = i / Kpad;
+    float v = 0.f;
+    if (k < Kreal) {
+      const int c = k % g.C;
+      const int rs = k / g.C;
+      const int s = rs % g.S, r = rs / g.S;
+      const int q = (int)(m % g.Q);
+      const long t = m / g.Q;
+      const int p = (int)(t % g.P);
+      const int n = (int)(t / g.P);
+      const int h = p * g.stride - g.pad + r, w = q * g.stride - g.pad + s;
+      if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = __bfloat162float(x[(((long)n * g.H + h) * g.W + w) * g.Cs + c]);
+    }
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// zero-inserted (stride-dilated) copy of dy: U[n][p*s][q*s] = dy[n][p][q]
+__global__ void __launch_bounds__(kThreads) zero_insert_kernel(const __nv_bfloat16* __restrict__ dy, int N, int P,
+                                                              int Q, int C, int Hu, int Wu, int stride,
+                                                              __nv_bfloat16* __restrict__ u) {
+  const int cv = C / 8;
+  const long total = (long)N * Hu * Wu * cv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    long t = i / cv;
+    const int w = (int)(t % Wu);
+    t /= Wu;
+    const int h = (int)(t % Hu);
+    const int n = (int)(t / Hu);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (h % stride == 0 && w % stride == 0 && h / stride < P && w / stride < Q)
+      v = ldg16(dy + (((long)n * P + h / stride) * Q + w / stride) * C + c8 * 8);
+    *reinterpret_cast<uint4*>(u + i * 8) = v;
+  }
+}
+
+// channel concat c = [a | b] and its backward
+__global__ void __launch_bounds__(kThreads) concat_kernel(const __nv_bfloat16* __restrict__ a, int Ca,
+                                                         const __nv_bfloat16* __restrict__ b, int Cb, long M,
+                                                         __nv_bfloat16* __restrict__ c) {
+  const int Cc = Ca + Cb, cv = Cc / 8;
+  const long total = M * cv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long m = i / cv;
+    const int ch = (int)(i % cv) * 8;
+    if (ch < Ca) {
+      if (a) *reinterpret_cast<uint4*>(c + m * Cc + ch) = ldg16(a + m * Ca + ch);
+    } else if (b) {
+      *reinterpret_cast<uint4*>(c + m * Cc + ch) = ldg16(b + m * Cb + (ch - Ca));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) split_grad_kernel(const __nv_bfloat16* __restrict__ dc, int Ca, int Cb,
+                                                             long M, __nv_bfloat16* __restrict__ da, int acc_a,
+                                                             __nv_bfloat16* __restrict__ db, int acc_b) {
+  const int Cc = Ca + Cb, cv = Cc / 8;
+  const long total = M * cv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long m = i / cv;
+    const int ch = (int)(i % cv) * 8;
+    float f[8];
+    unpack8(ldg16(dc + m * Cc + ch), f);
+    __nv_bfloat16* dst;
+    int acc;
+    if (ch < Ca) {
+      dst = da ? da + m * Ca + ch : nullptr;
+      acc = acc_a;
+    } else {
+      dst = db ? db + m * Cb + (ch - Ca) : nullptr;
+      acc = acc_b;
+    }
+    if (!dst) continue;
+    if (acc) {
+      float p[8];
+      unpack8(*reinterpret_cast<const uint4*>(dst), p);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) f[k] += p[k];
+    }
+    *reinterpret_cast<uint4*>(dst) = pack8(f);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) add_bf16_kernel(const __nv_bfloat16* __restrict__ a, long nvec,
+                                                           __nv_bfloat16* __restrict__ dst) {
+  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    float x[8], y[8];
+    unpack8(ldg16(a + v * 8), x);
+    unpack8(*reinterpret_cast<const uint4*>(dst + v * 8), y);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) y[i] += x[i];
+    *reinterpret_cast<uint4*>(dst + v * 8) = pack8(y);
+  }
+}
+
+long rows_per_block_for(long M, int blocks) { return (M + blocks - 1) / blocks; }
+
+}  // namespace
+
+// ============================================================ launchers
+int colstats_blocks(long M) {
+  // enough blocks to fill the chip, each with >= 64 rows
+  long b = (M + 63) / 64;
+  if (b > 148 * 4) b = 148 * 4;
+  return (int)(b < 1 ? 1 : b);
+}
+
+cudaError_t colstats(const __nv_bfloat16* x, long M, int C, float* partials, int blocks, cudaStream_t st) {
+  if (C % 8 || (C > 2048 && C % 2048)) return cudaErrorInvalidValue;
+  dim3 grid(blocks, (C + 2047) / 2048);
+  colstats_kernel<0><<<grid, kThreads, 0, st>>>(x, M, C, rows_per_block_for(M, blocks), partials);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_finalize(const float* partials, int parts, int C, long count, const float* gamma, const float* beta,
+                        float eps, float* mean, float* invstd, float* scale, float* shift, float* run_mean,
+                        float* run_var, float momentum, bool update_running, cudaStream_t st) {
+  bn_finalize_kernel<<<(C + 31) / 32, dim3(32, 8), 0, st>>>(partials, parts, C, (float)count, gamma, beta, eps, mean,
+                                                            invstd, scale, shift, run_mean, run_var, momentum,
+                                                            update_running ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_apply(const __nv_bfloat16* y, const __nv_bfloat16* skip, const float* scale, const float* shift,
+                     bool relu, long M, int C, __nv_bfloat16* out, cudaStream_t st) {
+  const long nvec = M * C / 8;
+  bn_apply_kernel<<<grid_for(nvec, kThreads * 4), kThreads, 0, st>>>(y, skip, scale, shift, relu ? 1 : 0, nvec, C, out);
+  return cudaGetLastError();
+}
+
+cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const __nv_bfloat16* out, int mask_mode,
+                        const float* gamma, const float* mean, const float* invstd, const float* scale,
+                        const float* shift, long M, int C, float* partials, int blocks, float* coef, float* dgamma,
+                        float* dbeta, __nv_bfloat16* dy, bool acc_dy, __nv_bfloat16* dskip, bool acc_dskip,
+                        cudaStream_t st) {
+  if (C % 8 || (C > 2048 && C % 2048)) return cudaErrorInvalidValue;
+  dim3 grid(blocks, (C + 2047) / 2048);
+  bn_bwd_reduce_kernel<<<grid, kThreads, 0, st>>>(y, dout, out, mask_mode, mean, invstd, scale, shift, M, C,
+                                                  rows_per_block_for(M, blocks), partials);
+  bn_bwd_finalize_kernel<<<(C + 31) / 32, dim3(32, 8), 0, st>>>(partials, blocks, C, (float)M, gamma, mean, invstd,
+                                                                dgamma, dbeta, coef);
+  const long nvec = M * C / 8;
+  bn_bwd_apply_kernel<<<grid_for(nvec, kThreads * 4), kThreads, 0, st>>>(y, dout, out, mask_mode, scale, shift, coef,
+                                                                         nvec, C, dy, acc_dy ? 1 : 0, dskip,
+                                                                         acc_dskip ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t relu_fwd(const __nv_bfloat16* x, long n, __nv_bfloat16* y, cudaStream_t st) {
+  relu_fwd_kernel<<<grid_for(n / 8, kThreads * 4), kThreads, 0, st>>>(x, n / 8, y);
+  return cudaGetLastError();
+}
+
+cudaError_t relu_bwd(const __nv_bfloat16* y, const __nv_bfloat16* dy, long n, __nv_bfloat16* dx, bool acc,
+                     cudaStream_t st) {
+  relu_bwd_kernel<<<grid_for(n / 8, kThreads * 4), kThreads, 0, st>>>(y, dy, n / 8, dx, acc ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st) {
+  const long work = (long)g.N * g.P * g.Q * (g.C / 8);
+  maxpool_fwd_kernel<<<grid_for(work, kThreads * 2), kThreads, 0, st>>>(x, g, y);
+  return cudaGetLastError();
+}
+
+cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __nv_bfloat16* dy, const PoolGeom& g,
+                        __nv_bfloat16* dx, bool acc, cudaStream_t st) {
+  const long work = (long)g.N * g.H * g.W * (g.C / 8);
+  maxpool_bwd_kernel<<<grid_for(work, kThreads * 2), kThreads, 0, st>>>(x, y, dy, g, dx, acc ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t avgpool_fwd(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, cudaStream_t st) {
+  avgpool_fwd_kernel<<<dim3(N, (C + kThreads - 1) / kThreads), kThreads, 0, st>>>(x, HW, C, out);
+  return cudaGetLastError();
+}
+
+cudaError_t avgpool_bwd(const __nv_bfloat16* dout, int N, int HW, int C, __nv_bfloat16* dx, bool acc,
+                        cudaStream_t st) {
+  const long nvec = (long)N * HW * C / 8;
+  avgpool_bwd_kernel<<<grid_for(nvec, kThreads * 4), kThreads, 0, st>>>(dout, HW, C, nvec, dx, acc ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_ce_fwd(const float* logits, const int* labels, int N, int K, float* row_loss, float* lse,
+                           float* loss, cudaStream_t st) {
+  softmax_ce_fwd_kernel<<<N, kThreads, 0, st>>>(logits, labels, K, row_loss, lse);
+  mean_kernel<<<1, kThreads, 0, st>>>(row_loss, N, loss);
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_ce_bwd(const float* logits, const int* labels, const float* lse, int N, int K, float* dlogits,
+                           cudaStream_t st) {
+  softmax_ce_bwd_kernel<<<grid_for((long)N * K, kThreads), kThreads, 0, st>>>(logits, labels, lse, N, K, dlogits);
+  return cudaGetLastError();
+}
+
+cudaError_t cast_f32_bf16(const float* x, long n, __nv_bfloat16* y, cudaStream_t st) {
+  cast_f32_bf16_kernel<<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(x, n, y);
+  return cudaGetLastError();
+}
+
+cudaError_t cast_f32_bf16_2d(const float* x, int R, int C, int ldo, __nv_bfloat16* y, cudaStream_t st) {
+  cast_f32_bf16_2d_kernel<<<grid_for((long)R * C, kThreads * 4), kThreads, 0, st>>>(x, R, C, ldo, y);
+  return cudaGetLastError();
+}
+
+cudaError_t colsum_bf16(const __nv_bfloat16* x, int R, int C, float* out, bool acc, cudaStream_t st) {
+  colsum_bf16_kernel<<<(C + kThreads - 1) / kThreads, kThreads, 0, st>>>(x, R, C, out, acc ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaStream_t st) {
+  colsum_f32_kernel<<<(C + kThreads - 1) / kThreads, kThreads, 0, st>>>(x, R, C, out, acc ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bool acc, cudaStream_t st) {
+  reduce_splits_kernel<<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(parts, splits, n, out, acc ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, float momentum, float wd,
+                       cudaStream_t st) {
+  sgd_kernel<<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(w, g, m, n, lr, momentum, wd);
+  return cudaGetLastError();
+}
+
+cudaError_t conv_weight_prep(const float* w, int Cout, int R, int S, int Cpad, int Cin, int CoutPad,
+                             __nv_bfloat16* wb, __nv_bfloat16* wt, cudaStream_t st) {
+  const long total = (long)Cout * R * S * Cpad;
+  conv_weight_prep_kernel<<<grid_for(total, kThreads * 4), kThreads, 0, st>>>(w, Cout, R, S, Cpad, Cin, CoutPad, wb,
+                                                                              wt);
+  return cudaGetLastError();
+}
+
+cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __nv_bfloat16* out, cudaStream_t st) {
+  const long total = (long)N * H * W * Cpad;
+  pack_input_kernel<<<grid_for(total, kThreads * 4), kThreads, 0, st>>>(x, N, C, H, W, Cpad, out);
+  return cudaGetLastError();
+}
+
+cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st) {
+  const long total = (long)g.N * g.P * g.Q * Kpad;
+  im2col_kernel<<<grid_for(total, kThreads * 4), kThreads, 0, st>>>(x, g, Kpad, out);
+  return cudaGetLastError();
+}
+
+cudaError_t zero_insert(const __nv_bfloat16* dy, int N, int P, int Q, int C, int Hu, int Wu, int stride,
+                        __nv_bfloat16* u, cudaStream_t st) {
+  const long work = (long)N * Hu * Wu * (C / 8);
+  zero_insert_kernel<<<grid_for(work, kThreads * 4), kThreads, 0, st>>>(dy, N, P, Q, C, Hu, Wu, stride, u);
+  return cudaGetLastError();
+}
+
+cudaError_t concat(const __nv_bfloat16* a, int Ca, const __nv_bfloat16* b, int Cb, long M, __nv_bfloat16* c,
+                   cudaStream_t st) {
+  const long work = M * ((Ca + Cb) / 8);
+  concat_kernel<<<grid_for(work, kThreads * 4), kThreads, 0, st>>>(a, Ca, b, Cb, M, c);
+  return cudaGetLastError();
+}
+
+cudaError_t split_grad(const __nv_bfloat16* dc, int Ca, int Cb, long M, __nv_bfloat16* da, bool acc_a,
+                       __nv_bfloat16* db, bool acc_b, cudaStream_t st) {
+  const long work = M * ((Ca + Cb) / 8);
+  split_grad_kernel<<<grid_for(work, kThreads * 4), kThreads, 0, st>>>(dc, Ca, Cb, M, da, acc_a ? 1 : 0, db,
+                                                                       acc_b ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t add_bf16(const __nv_bfloat16* a, long n, __nv_bfloat16* dst, cudaStream_t st) {
+  add_bf16_kernel<<<grid_for(n / 8, kThreads * 4), kThreads, 0, st>>>(a, n / 8, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace rfk

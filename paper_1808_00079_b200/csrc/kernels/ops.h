@@ -1,0 +1,61 @@
+// Launchers of the non-GEMM kernels (csrc/kernels/ops.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace rfk {
+
+struct PoolGeom {
+  int N, H, W, C, P, Q, k, stride, pad;
+};
+
+struct ConvShape {  // for the explicit im2col path
+  int N, H, W, C, Cs /*channel stride of x*/, P, Q, R, S, stride, pad;
+};
+
+int colstats_blocks(long M);
+cudaError_t colstats(const __nv_bfloat16* x, long M, int C, float* partials, int blocks, cudaStream_t st);
+cudaError_t bn_finalize(const float* partials, int parts, int C, long count, const float* gamma, const float* beta,
+                        float eps, float* mean, float* invstd, float* scale, float* shift, float* run_mean,
+                        float* run_var, float momentum, bool update_running, cudaStream_t st);
+cudaError_t bn_apply(const __nv_bfloat16* y, const __nv_bfloat16* skip, const float* scale, const float* shift,
+                     bool relu, long M, int C, __nv_bfloat16* out, cudaStream_t st);
+// mask_mode: 0 none (plain BN), 1 relu(bn(y)), 2 relu via stored output (> 0)
+cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const __nv_bfloat16* out, int mask_mode,
+                        const float* gamma, const float* mean, const float* invstd, const float* scale,
+                        const float* shift, long M, int C, float* partials, int blocks, float* coef, float* dgamma,
+                        float* dbeta, __nv_bfloat16* dy, bool acc_dy, __nv_bfloat16* dskip, bool acc_dskip,
+                        cudaStream_t st);
+cudaError_t relu_fwd(const __nv_bfloat16* x, long n, __nv_bfloat16* y, cudaStream_t st);
+cudaError_t relu_bwd(const __nv_bfloat16* y, const __nv_bfloat16* dy, long n, __nv_bfloat16* dx, bool acc,
+                     cudaStream_t st);
+cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st);
+cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __nv_bfloat16* dy, const PoolGeom& g,
+                        __nv_bfloat16* dx, bool acc, cudaStream_t st);
+cudaError_t avgpool_fwd(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, cudaStream_t st);
+cudaError_t avgpool_bwd(const __nv_bfloat16* dout, int N, int HW, int C, __nv_bfloat16* dx, bool acc,
+                        cudaStream_t st);
+cudaError_t softmax_ce_fwd(const float* logits, const int* labels, int N, int K, float* row_loss, float* lse,
+                           float* loss, cudaStream_t st);
+cudaError_t softmax_ce_bwd(const float* logits, const int* labels, const float* lse, int N, int K, float* dlogits,
+                           cudaStream_t st);
+cudaError_t cast_f32_bf16(const float* x, long n, __nv_bfloat16* y, cudaStream_t st);
+cudaError_t cast_f32_bf16_2d(const float* x, int R, int C, int ldo, __nv_bfloat16* y, cudaStream_t st);
+cudaError_t colsum_bf16(const __nv_bfloat16* x, int R, int C, float* out, bool acc, cudaStream_t st);
+cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaStream_t st);
+cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bool acc, cudaStream_t st);
+cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, float momentum, float wd,
+                       cudaStream_t st);
+cudaError_t conv_weight_prep(const float* w, int Cout, int R, int S, int Cpad, int Cin, int CoutPad,
+                             __nv_bfloat16* wb, __nv_bfloat16* wt, cudaStream_t st);
+cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __nv_bfloat16* out, cudaStream_t st);
+cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st);
+cudaError_t zero_insert(const __nv_bfloat16* dy, int N, int P, int Q, int C, int Hu, int Wu, int stride,
+                        __nv_bfloat16* u, cudaStream_t st);
+cudaError_t concat(const __nv_bfloat16* a, int Ca, const __nv_bfloat16* b, int Cb, long M, __nv_bfloat16* c,
+                   cudaStream_t st);
+cudaError_t split_grad(const __nv_bfloat16* dc, int Ca, int Cb, long M, __nv_bfloat16* da, bool acc_a,
+                       __nv_bfloat16* db, bool acc_b, cudaStream_t st);
+cudaError_t add_bf16(const __nv_bfloat16* a, long n, __nv_bfloat16* dst, cudaStream_t st);
+
+}  // namespace rfk

@@ -1,0 +1,348 @@
+"""Python face of the re-forward training executor (rfx_net_* C-ABI).
+
+    net = ReforwardNet.named("resnet50", batch=32)
+    net.plan("reforward")          # host planner on the tensor graph
+    net.setup(seed=0)              # device arenas + parameters
+    net.load_batch(images, labels) # NCHW fp32 + int32 (host or device tensors)
+    net.step(lr=0.1)               # forward (stored tensors only) + backward
+                                   # (per-segment re-forward) + SGD, on sm_100a
+
+The executor owns its device memory (activation arena sized to the planner's
+Eq. 1 total); torch is only used to hand in host/device buffers and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from ._lib import load_library
+
+OP_KINDS = ["input", "conv", "bn", "bn_add_relu", "relu", "maxpool", "avgpool", "fc", "concat", "loss"]
+POLICIES = ("reforward", "store_all", "lcg", "sqrt")
+
+
+class MemoryReport(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "planned_total", "stored_cost", "max_segment", "store_all_total", "tracked_peak", "arena_bytes",
+        "grad_arena_bytes", "workspace_bytes", "param_bytes", "state_bytes", "reforward_ops", "segment_loads",
+        "forward_ops", "backward_ops", "launches_per_step", "candidate_max_term")] + [
+        ("n_segments", C.c_int32), ("n_stored", C.c_int32)]
+
+    def as_dict(self) -> Dict[str, int]:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_SIGS = {
+    "rfx_net_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "rfx_net_create_named": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                       C.POINTER(C.c_void_p)]),
+    "rfx_net_free": (None, [C.c_void_p]),
+    "rfx_net_input": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]),
+    "rfx_net_conv": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                               C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_bn": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_bn_add_relu": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_relu": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_maxpool": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p,
+                                  C.POINTER(C.c_int32)]),
+    "rfx_net_avgpool": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_fc": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_concat": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_loss": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_num_tensors": (C.c_int32, [C.c_void_p]),
+    "rfx_net_tensor_info": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+    "rfx_net_num_ops": (C.c_int32, [C.c_void_p]),
+    "rfx_net_op_info": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "rfx_net_flops_per_step": (C.c_int64, [C.c_void_p]),
+    "rfx_net_plan": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "rfx_net_plan_with_stored": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_char_p]),
+    "rfx_net_plan_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_int32),
+                                    C.POINTER(MemoryReport)]),
+    "rfx_net_schedule": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
+    "rfx_net_setup": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "rfx_net_load_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "rfx_net_forward_backward": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "rfx_net_update": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_void_p]),
+    "rfx_net_step": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_int32, C.c_void_p]),
+    "rfx_net_read_loss": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_void_p]),
+    "rfx_net_num_params": (C.c_int32, [C.c_void_p]),
+    "rfx_net_param_info": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    "rfx_net_read_param": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "rfx_net_write_param": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "rfx_net_read_tensor": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "rfx_net_read_bn_running": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "rfx_net_grad_buffer": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "rf_last_error": (C.c_char_p, []),
+}
+
+_bound = None
+
+
+def _lib():
+    global _bound
+    if _bound is None:
+        L = load_library()
+        for n, (r, a) in _SIGS.items():
+            f = getattr(L, n)
+            f.restype = r
+            f.argtypes = a
+        _bound = L
+    return _bound
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise RuntimeError(f"rfx error {rc}: {_lib().rf_last_error().decode()}")
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    return stream if isinstance(stream, int) else stream.cuda_stream
+
+
+@dataclass
+class TensorInfo:
+    id: int
+    name: str
+    shape: Tuple[int, int, int, int]
+    dtype: str
+    cost: int
+    producer: int
+
+
+@dataclass
+class OpInfo:
+    id: int
+    name: str
+    kind: str
+    inputs: List[int]
+    out: int
+
+
+@dataclass
+class ParamInfo:
+    index: int
+    name: str
+    shape: Tuple[int, ...]
+    kind: int
+    count: int
+
+
+class ReforwardNet:
+    """Handle on one rfx_net (network + plan + device state)."""
+
+    def __init__(self, batch: int, handle: Optional[C.c_void_p] = None):
+        self.L = _lib()
+        self.batch = batch
+        if handle is None:
+            handle = C.c_void_p()
+            _check(self.L.rfx_net_create(batch, C.byref(handle)))
+        self.h = handle
+
+    @classmethod
+    def named(cls, arch: str, batch: int, H: int = 224, W: int = 224, classes: int = 1000) -> "ReforwardNet":
+        h = C.c_void_p()
+        _check(_lib().rfx_net_create_named(arch.encode(), batch, H, W, classes, C.byref(h)))
+        return cls(batch, h)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.rfx_net_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ building
+    def _op(self, fn, *args) -> int:
+        out = C.c_int32()
+        _check(fn(self.h, *args, C.byref(out)))
+        return out.value
+
+    def input(self, H, W, Cin):
+        return self._op(self.L.rfx_net_input, H, W, Cin)
+
+    def conv(self, x, cout, k, stride=1, pad=0, name="conv", R=None, S=None):
+        return self._op(self.L.rfx_net_conv, x, cout, R or k, S or k, stride, pad, name.encode())
+
+    def bn(self, y, relu=True, name="bn"):
+        return self._op(self.L.rfx_net_bn, y, int(relu), name.encode())
+
+    def bn_add_relu(self, y, skip, name="bn_add"):
+        return self._op(self.L.rfx_net_bn_add_relu, y, skip, name.encode())
+
+    def relu(self, x, name="relu"):
+        return self._op(self.L.rfx_net_relu, x, name.encode())
+
+    def maxpool(self, x, k, stride, pad, name="maxpool"):
+        return self._op(self.L.rfx_net_maxpool, x, k, stride, pad, name.encode())
+
+    def avgpool(self, x, name="avgpool"):
+        return self._op(self.L.rfx_net_avgpool, x, name.encode())
+
+    def fc(self, x, classes, name="fc"):
+        return self._op(self.L.rfx_net_fc, x, classes, name.encode())
+
+    def concat(self, a, b, name="concat"):
+        return self._op(self.L.rfx_net_concat, a, b, name.encode())
+
+    def loss(self, logits, name="loss"):
+        return self._op(self.L.rfx_net_loss, logits, name.encode())
+
+    # ------------------------------------------------------------ introspection
+    def tensors(self) -> List[TensorInfo]:
+        out = []
+        for t in range(self.L.rfx_net_num_tensors(self.h)):
+            name = C.create_string_buffer(256)
+            shp = (C.c_int32 * 4)()
+            dt, cost, prod = C.c_int32(), C.c_int64(), C.c_int32()
+            _check(self.L.rfx_net_tensor_info(self.h, t, name, 256, shp, C.byref(dt), C.byref(cost), C.byref(prod)))
+            out.append(TensorInfo(t, name.value.decode(), tuple(shp), "bf16" if dt.value == 0 else "f32", cost.value,
+                                  prod.value))
+        return out
+
+    def ops(self) -> List[OpInfo]:
+        out = []
+        for o in range(self.L.rfx_net_num_ops(self.h)):
+            name = C.create_string_buffer(256)
+            kind, ins, ot = C.c_int32(), (C.c_int32 * 2)(), C.c_int32()
+            _check(self.L.rfx_net_op_info(self.h, o, name, 256, C.byref(kind), ins, C.byref(ot)))
+            out.append(OpInfo(o, name.value.decode(), OP_KINDS[kind.value], [i for i in ins if i >= 0], ot.value))
+        return out
+
+    def graph(self) -> Tuple[List[Tuple[str, int]], List[Tuple[str, str]]]:
+        """The tensor graph handed to the planner: (name, cost) vertices, named edges."""
+        ts = self.tensors()
+        verts = [(t.name, t.cost) for t in ts]
+        edges = [(ts[i].name, ts[o.out].name) for o in self.ops() for i in o.inputs]
+        return verts, edges
+
+    def flops_per_step(self) -> int:
+        return self.L.rfx_net_flops_per_step(self.h)
+
+    # ------------------------------------------------------------ planning
+    def plan(self, policy: str = "reforward") -> MemoryReport:
+        _check(self.L.rfx_net_plan(self.h, policy.encode()))
+        return self.report()
+
+    def plan_with_stored(self, stored: Sequence[int], label: str = "custom") -> MemoryReport:
+        n = self.L.rfx_net_num_tensors(self.h)
+        m = (C.c_uint8 * n)()
+        for v in stored:
+            m[v] = 1
+        _check(self.L.rfx_net_plan_with_stored(self.h, m, label.encode()))
+        return self.report()
+
+    def report(self) -> MemoryReport:
+        r = MemoryReport()
+        _check(self.L.rfx_net_plan_info(self.h, None, None, C.byref(r)))
+        return r
+
+    def plan_sets(self) -> Tuple[List[int], List[int]]:
+        n = self.L.rfx_net_num_tensors(self.h)
+        m = (C.c_uint8 * n)()
+        s = (C.c_int32 * n)()
+        _check(self.L.rfx_net_plan_info(self.h, m, s, None))
+        return [i for i in range(n) if m[i]], list(s)
+
+    def schedule(self) -> List[Tuple[str, int, int, bool]]:
+        n = C.c_int32()
+        _check(self.L.rfx_net_schedule(self.h, None, None, None, None, 0, C.byref(n)))
+        k, o, s, r = [(C.c_int32 * max(n.value, 1))() for _ in range(4)]
+        _check(self.L.rfx_net_schedule(self.h, k, o, s, r, n.value, C.byref(n)))
+        names = ["forward", "backward", "release"]
+        return [(names[k[i]], o[i], s[i], bool(r[i])) for i in range(n.value)]
+
+    # ------------------------------------------------------------ runtime
+    def setup(self, seed: int = 0) -> None:
+        _check(self.L.rfx_net_setup(self.h, seed))
+
+    def load_batch(self, images, labels, stream=None) -> None:
+        """images: float32 NCHW, labels: int32 [batch]; torch tensors (host or cuda) or numpy."""
+        import numpy as np
+        try:
+            import torch
+        except Exception:  # pragma: no cover
+            torch = None
+        if torch is not None and isinstance(images, torch.Tensor):
+            assert images.dtype == torch.float32 and images.is_contiguous()
+            assert labels.dtype == torch.int32 and labels.is_contiguous()
+            from_host = int(not images.is_cuda)
+            _check(self.L.rfx_net_load_batch(self.h, C.c_void_p(images.data_ptr()), C.c_void_p(labels.data_ptr()),
+                                             from_host, _stream(stream)))
+            return
+        im = np.ascontiguousarray(images, dtype=np.float32)
+        lb = np.ascontiguousarray(labels, dtype=np.int32)
+        _check(self.L.rfx_net_load_batch(self.h, im.ctypes.data_as(C.c_void_p), lb.ctypes.data_as(C.c_void_p), 1,
+                                         _stream(stream)))
+
+    def forward_backward(self, stream=None) -> None:
+        _check(self.L.rfx_net_forward_backward(self.h, _stream(stream)))
+
+    def update(self, lr=0.1, momentum=0.9, weight_decay=0.0, stream=None) -> None:
+        _check(self.L.rfx_net_update(self.h, lr, momentum, weight_decay, _stream(stream)))
+
+    def step(self, lr=0.1, momentum=0.9, weight_decay=0.0, use_graph=True, stream=None) -> None:
+        _check(self.L.rfx_net_step(self.h, lr, momentum, weight_decay, int(use_graph), _stream(stream)))
+
+    def read_loss(self, stream=None) -> float:
+        v = C.c_float()
+        _check(self.L.rfx_net_read_loss(self.h, C.byref(v), _stream(stream)))
+        return v.value
+
+    # ------------------------------------------------------------ parameters
+    def params(self) -> List[ParamInfo]:
+        out = []
+        for i in range(self.L.rfx_net_num_params(self.h)):
+            name = C.create_string_buffer(256)
+            shp = (C.c_int32 * 4)()
+            nd, kind, cnt = C.c_int32(), C.c_int32(), C.c_int64()
+            _check(self.L.rfx_net_param_info(self.h, i, name, 256, shp, C.byref(nd), C.byref(kind), C.byref(cnt)))
+            out.append(ParamInfo(i, name.value.decode(), tuple(shp[: nd.value]), kind.value, cnt.value))
+        return out
+
+    def read_param(self, i: int, which: int = 0):
+        import numpy as np
+        p = self.params()[i]
+        a = np.empty(p.shape, dtype=np.float32)
+        _check(self.L.rfx_net_read_param(self.h, i, which, a.ctypes.data_as(C.c_void_p)))
+        return a
+
+    def write_param(self, i: int, value) -> None:
+        import numpy as np
+        a = np.ascontiguousarray(value, dtype=np.float32)
+        p = self.params()[i]
+        assert a.size == p.count, (p.name, a.shape, p.shape)
+        _check(self.L.rfx_net_write_param(self.h, i, a.ctypes.data_as(C.c_void_p)))
+
+    def read_tensor(self, t: int):
+        import numpy as np
+        info = self.tensors()[t]
+        a = np.empty(info.shape, dtype=np.float32)
+        _check(self.L.rfx_net_read_tensor(self.h, t, a.ctypes.data_as(C.c_void_p)))
+        return a
+
+    def read_bn_running(self, op: int):
+        import numpy as np
+        o = self.ops()[op]
+        c = self.tensors()[o.out].shape[3]
+        m, v = np.empty(c, np.float32), np.empty(c, np.float32)
+        _check(self.L.rfx_net_read_bn_running(self.h, op, m.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p)))
+        return m, v
+
+    def grad_buffer(self) -> Tuple[int, int]:
+        p, n = C.c_void_p(), C.c_int64()
+        _check(self.L.rfx_net_grad_buffer(self.h, C.byref(p), C.byref(n)))
+        return p.value, n.value

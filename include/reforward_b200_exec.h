@@ -76,6 +76,8 @@ int rfx_net_tensor_info(const rfx_net* net, int32_t t, char* name, size_t name_c
 int32_t rfx_net_num_ops(const rfx_net* net);
 int rfx_net_op_info(const rfx_net* net, int32_t op, char* name, size_t name_cap, int32_t* kind,
                     int32_t* inputs /* up to 2, -1 pads */, int32_t* out);
+/* attrs[8] = {R, S, stride, pad, k (pool window / bn relu flag), classes, cin_real, cout} */
+int rfx_net_op_attrs(const rfx_net* net, int32_t op, int32_t* attrs);
 int64_t rfx_net_flops_per_step(const rfx_net* net);
 
 /* planning: policy "reforward" | "store_all" | "lcg" | "sqrt" */
@@ -104,9 +106,10 @@ typedef struct rfx_memory_report {
 } rfx_memory_report;
 
 int rfx_net_plan_info(const rfx_net* net, uint8_t* stored_mask, int32_t* seg_of, rfx_memory_report* rep);
-/* schedule: kinds (0 forward, 1 backward, 2 release), op ids, segment ids, re-forward flags */
+/* schedule: kinds (0 forward, 1 backward, 2 release), op ids, segment ids, re-forward flags,
+ * phases (0 whole op; 1/2 = the two halves of a join whose inputs sit in two segments) */
 int rfx_net_schedule(const rfx_net* net, int32_t* kinds, int32_t* ops, int32_t* segs, int32_t* reforward,
-                     int32_t cap, int32_t* n_out);
+                     int32_t* phases, int32_t cap, int32_t* n_out);
 
 /* runtime */
 int rfx_net_setup(rfx_net* net, uint64_t seed);
@@ -117,7 +120,15 @@ int rfx_net_load_batch(rfx_net* net, const float* images, const int32_t* labels,
 int rfx_net_forward_backward(rfx_net* net, void* stream);
 int rfx_net_update(rfx_net* net, float lr, float momentum, float weight_decay, void* stream);
 int rfx_net_step(rfx_net* net, float lr, float momentum, float weight_decay, int32_t use_graph, void* stream);
+/* phase 0 forward+backward, 1 SGD update + weight prep, 2 both; with use_graph
+ * each phase is captured once into a CUDA graph and replayed */
+int rfx_net_run_phase(rfx_net* net, int32_t phase, float lr, float momentum, float weight_decay,
+                      int32_t use_graph, void* stream);
 int rfx_net_read_loss(rfx_net* net, float* loss, void* stream);
+/* live roofline probe: replay exactly the step's GEMM launches; ms and
+ * algorithmic flops per step, number of GEMM launches */
+int rfx_net_gemm_profile(rfx_net* net, int32_t iters, void* stream, double* ms_per_step,
+                         double* flops_per_step, int64_t* launches);
 
 int32_t rfx_net_num_params(const rfx_net* net);
 int rfx_net_param_info(const rfx_net* net, int32_t i, char* name, size_t name_cap, int32_t* shape,

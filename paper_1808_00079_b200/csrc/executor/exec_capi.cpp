@@ -129,6 +129,20 @@ int rfx_net_op_info(const rfx_net* n, int32_t o, char* name, size_t cap, int32_t
   });
 }
 
+int rfx_net_op_attrs(const rfx_net* n, int32_t o, int32_t* a) {
+  return guard([&] {
+    const auto& op = n->net->ops().at(o);
+    a[0] = op.R;
+    a[1] = op.S;
+    a[2] = op.stride;
+    a[3] = op.pad;
+    a[4] = op.k;
+    a[5] = op.classes;
+    a[6] = op.cin_real;
+    a[7] = op.cout;
+  });
+}
+
 int64_t rfx_net_flops_per_step(const rfx_net* n) { return n->net->flops_per_step(); }
 
 int rfx_net_plan(rfx_net* n, const char* policy) {
@@ -177,8 +191,8 @@ int rfx_net_plan_info(const rfx_net* n, uint8_t* mask, int32_t* seg_of, rfx_memo
   });
 }
 
-int rfx_net_schedule(const rfx_net* n, int32_t* kinds, int32_t* ops, int32_t* segs, int32_t* reforward, int32_t cap,
-                     int32_t* n_out) {
+int rfx_net_schedule(const rfx_net* n, int32_t* kinds, int32_t* ops, int32_t* segs, int32_t* reforward,
+                     int32_t* phases, int32_t cap, int32_t* n_out) {
   return guard([&] {
     const auto& s = n->net->schedule();
     *n_out = (int32_t)s.size();
@@ -189,6 +203,7 @@ int rfx_net_schedule(const rfx_net* n, int32_t* kinds, int32_t* ops, int32_t* se
       ops[i] = s[i].op;
       segs[i] = s[i].seg;
       reforward[i] = s[i].reforward ? 1 : 0;
+      if (phases) phases[i] = s[i].phase;
     }
   });
 }
@@ -215,6 +230,21 @@ int rfx_net_step(rfx_net* n, float lr, float momentum, float wd, int32_t use_gra
 
 int rfx_net_read_loss(rfx_net* n, float* loss, void* st) {
   return guard([&] { *loss = n->net->read_loss(S(st)); });
+}
+
+int rfx_net_run_phase(rfx_net* n, int32_t phase, float lr, float momentum, float wd, int32_t use_graph, void* st) {
+  return guard([&] {
+    if (phase < 0 || phase > 2) throw std::invalid_argument("phase must be 0, 1 or 2");
+    n->net->run_phase(phase, lr, momentum, wd, S(st), use_graph != 0);
+  });
+}
+
+int rfx_net_gemm_profile(rfx_net* n, int32_t iters, void* st, double* ms, double* flops, int64_t* launches) {
+  return guard([&] {
+    long l = 0;
+    n->net->gemm_profile(iters < 1 ? 1 : iters, S(st), ms, flops, &l);
+    *launches = l;
+  });
 }
 
 int32_t rfx_net_num_params(const rfx_net* n) { return n->net->num_params(); }

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -143,7 +144,15 @@ class Net {
   void forward_backward(cudaStream_t st);  // loss + gradients (no update)
   void update(float lr, float momentum, float wd, cudaStream_t st);  // SGD + weight prep
   void step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph);
+  // phase: 0 forward+backward, 1 update, 2 both (each cached as its own CUDA graph)
+  void run_phase(int phase, float lr, float momentum, float wd, cudaStream_t st, bool use_graph);
   float read_loss(cudaStream_t st);
+
+  // Live roofline probe of the dense-contraction kernels: replay exactly the
+  // GEMM launches of one step (same shapes, same buffers) as a CUDA graph and
+  // time it with events.  flops = algorithmic 2*M*N*K of the real (unpadded)
+  // problem summed over those launches.
+  void gemm_profile(int iters, cudaStream_t st, double* ms_per_step, double* flops_per_step, long* launches);
 
   // parameter access in canonical layout (host fp32)
   int num_params() const { return (int)params_.size(); }
@@ -222,6 +231,17 @@ class Net {
   float* d_hyper_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   float graph_lr_ = 0, graph_mom_ = 0, graph_wd_ = 0;
+  cudaGraphExec_t phase_exec_[3] = {nullptr, nullptr, nullptr};
+  float phase_hyper_[3][3] = {};
+
+  struct GemmRecord {
+    rfk::GemmDesc desc;
+    double flops;
+  };
+  bool tracing_ = false;
+  double trace_flops_ = 0;  // algorithmic flops to attach to the next traced GEMM
+  std::vector<GemmRecord> gemm_trace_;
+  cudaGraphExec_t capture(const std::function<void(cudaStream_t)>& body, long* kernel_nodes);
 
   friend class Scheduler;
 };

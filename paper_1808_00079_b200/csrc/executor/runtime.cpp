@@ -32,6 +32,11 @@ void Net::check(cudaError_t e, const char* what) const {
 void Net::free_device() {
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   graph_exec_ = nullptr;
+  for (auto& e : phase_exec_) {
+    if (e) cudaGraphExecDestroy(e);
+    e = nullptr;
+  }
+  gemm_trace_.clear();
   for (void* p : {(void*)d_arena_, (void*)d_grad_arena_, (void*)d_ws_, (void*)d_param_, (void*)d_grad_,
                   (void*)d_mom_, (void*)d_bf16_, (void*)d_state_, (void*)d_input_, (void*)d_images_,
                   (void*)d_labels_, (void*)d_loss_, (void*)d_rowloss_, (void*)d_lse_, (void*)d_hyper_})
@@ -203,7 +208,10 @@ __nv_bfloat16* Net::gptr(int t) const {
   return reinterpret_cast<__nv_bfloat16*>(d_grad_arena_ + grad_slot_[t]);
 }
 
-void Net::gemm(const rfk::GemmDesc& d, cudaStream_t st) { check(rfk::gemm_launch(d, st), "gemm"); }
+void Net::gemm(const rfk::GemmDesc& d, cudaStream_t st) {
+  if (tracing_) gemm_trace_.push_back({d, trace_flops_});
+  check(rfk::gemm_launch(d, st), "gemm");
+}
 
 // ============================================================ op dispatch
 void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
@@ -245,6 +253,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         d.b_ld = (long)op.R * op.S * op.cpad;
       }
       if (op.fuse_stats && !reforward) d.stats = ws_stats + op.stats_off;
+      trace_flops_ = 2.0 * y.rows() * op.cout * op.R * op.S * op.cin_real;
       gemm(d, st);
       break;
     }
@@ -312,6 +321,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       d.ldc = op.classes;
       d.out_f32 = true;
       d.bias = d_param_ + params_[op.b_param].offset;
+      trace_flops_ = 2.0 * batch_ * op.classes * op.cin;
       gemm(d, st);
       break;
     }
@@ -349,6 +359,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       const Tensor& y = tensors_[op.out];
       const Param& w = params_[op.w_param];
       const __nv_bfloat16* dy = gptr(op.out);
+      trace_flops_ = 2.0 * y.rows() * op.cout * op.R * op.S * op.cin_real;  // dgrad and wgrad each
       // ---- dgrad
       __nv_bfloat16* dx = gptr(op.in[0]);
       if (op.in[0] != input_t_ && dx) {
@@ -473,6 +484,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       const Param& w = params_[op.w_param];
       const float* dlog = reinterpret_cast<const float*>(gptr(op.out));
       const int ldd = round8(op.classes);
+      trace_flops_ = 2.0 * batch_ * op.classes * op.cin;
       // bf16 copy of dlogits with 16-byte aligned rows for TMA
       check(cudaMemsetAsync(ws_misc, 0, (long)batch_ * ldd * 2, st), "memset");
       check(rfk::cast_f32_bf16_2d(dlog, batch_, op.classes, ldd, ws_misc, st), "cast");
@@ -576,41 +588,101 @@ void Net::update(float lr, float momentum, float wd, cudaStream_t st) {
   prep_weights(st);
 }
 
-void Net::step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph) {
+cudaGraphExec_t Net::capture(const std::function<void(cudaStream_t)>& body, long* kernel_nodes) {
+  cudaStream_t cap;
+  check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream");
+  check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+  try {
+    body(cap);
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(cap, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    throw;
+  }
+  cudaGraph_t g;
+  check(cudaStreamEndCapture(cap, &g), "end capture");
+  size_t nn = 0;
+  check(cudaGraphGetNodes(g, nullptr, &nn), "graph nodes");
+  std::vector<cudaGraphNode_t> nodes(nn);
+  check(cudaGraphGetNodes(g, nodes.data(), &nn), "graph nodes");
+  long kernels = 0;
+  for (auto n : nodes) {
+    cudaGraphNodeType t;
+    cudaGraphNodeGetType(n, &t);
+    if (t == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  if (kernel_nodes) *kernel_nodes = kernels;
+  cudaGraphExec_t exec = nullptr;
+  check(cudaGraphInstantiate(&exec, g, 0), "instantiate");
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cap);
+  return exec;
+}
+
+void Net::run_phase(int phase, float lr, float momentum, float wd, cudaStream_t st, bool use_graph) {
+  auto body = [&](cudaStream_t s) {
+    if (phase == 0 || phase == 2) forward_backward(s);
+    if (phase == 1 || phase == 2) update(lr, momentum, wd, s);
+  };
   if (!use_graph) {
-    forward_backward(st);
-    update(lr, momentum, wd, st);
+    body(st);
     return;
   }
-  if (!graph_exec_ || lr != graph_lr_ || momentum != graph_mom_ || wd != graph_wd_) {
-    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-    graph_exec_ = nullptr;
-    cudaStream_t cap;
-    check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream");
-    check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
-    forward_backward(cap);
-    update(lr, momentum, wd, cap);
-    cudaGraph_t g;
-    check(cudaStreamEndCapture(cap, &g), "end capture");
-    size_t nn = 0;
-    check(cudaGraphGetNodes(g, nullptr, &nn), "graph nodes");
-    std::vector<cudaGraphNode_t> nodes(nn);
-    check(cudaGraphGetNodes(g, nodes.data(), &nn), "graph nodes");
-    long kernels = 0;
-    for (auto n : nodes) {
-      cudaGraphNodeType t;
-      cudaGraphNodeGetType(n, &t);
-      if (t == cudaGraphNodeTypeKernel) ++kernels;
-    }
-    rep_.launches_per_step = kernels;
-    check(cudaGraphInstantiate(&graph_exec_, g, 0), "instantiate");
-    cudaGraphDestroy(g);
-    cudaStreamDestroy(cap);
-    graph_lr_ = lr;
-    graph_mom_ = momentum;
-    graph_wd_ = wd;
+  float* hp = phase_hyper_[phase];
+  if (!phase_exec_[phase] || hp[0] != lr || hp[1] != momentum || hp[2] != wd) {
+    if (phase_exec_[phase]) cudaGraphExecDestroy(phase_exec_[phase]);
+    phase_exec_[phase] = nullptr;
+    long k = 0;
+    phase_exec_[phase] = capture(body, &k);
+    if (phase == 2) rep_.launches_per_step = k;
+    hp[0] = lr;
+    hp[1] = momentum;
+    hp[2] = wd;
   }
-  check(cudaGraphLaunch(graph_exec_, st), "graph launch");
+  check(cudaGraphLaunch(phase_exec_[phase], st), "graph launch");
+}
+
+void Net::step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph) {
+  run_phase(2, lr, momentum, wd, st, use_graph);
+}
+
+void Net::gemm_profile(int iters, cudaStream_t st, double* ms_per_step, double* flops_per_step, long* launches) {
+  if (gemm_trace_.empty()) {
+    tracing_ = true;
+    try {
+      cudaGraphExec_t e = capture([&](cudaStream_t s) { forward_backward(s); }, nullptr);
+      cudaGraphExecDestroy(e);  // only the trace was wanted
+    } catch (...) {
+      tracing_ = false;
+      throw;
+    }
+    tracing_ = false;
+  }
+  double flops = 0;
+  for (const auto& r : gemm_trace_) flops += r.flops;
+  cudaGraphExec_t g = capture(
+      [&](cudaStream_t s) {
+        for (const auto& r : gemm_trace_) check(rfk::gemm_launch(r.desc, s), "gemm");
+      },
+      nullptr);
+  cudaEvent_t e0, e1;
+  check(cudaEventCreate(&e0), "event");
+  check(cudaEventCreate(&e1), "event");
+  for (int i = 0; i < 2; ++i) check(cudaGraphLaunch(g, st), "warmup");
+  check(cudaEventRecord(e0, st), "event");
+  for (int i = 0; i < iters; ++i) check(cudaGraphLaunch(g, st), "gemm replay");
+  check(cudaEventRecord(e1, st), "event");
+  check(cudaEventSynchronize(e1), "event sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(g);
+  *ms_per_step = ms / iters;
+  *flops_per_step = flops;
+  *launches = (long)gemm_trace_.size();
 }
 
 float Net::read_loss(cudaStream_t st) {

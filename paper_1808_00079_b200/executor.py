@@ -57,18 +57,23 @@ _SIGS = {
     "rfx_net_op_info": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "rfx_net_flops_per_step": (C.c_int64, [C.c_void_p]),
+    "rfx_net_op_attrs": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
     "rfx_net_plan": (C.c_int, [C.c_void_p, C.c_char_p]),
     "rfx_net_plan_with_stored": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_char_p]),
     "rfx_net_plan_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_int32),
                                     C.POINTER(MemoryReport)]),
     "rfx_net_schedule": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
-                                   C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
     "rfx_net_setup": (C.c_int, [C.c_void_p, C.c_uint64]),
     "rfx_net_load_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "rfx_net_forward_backward": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rfx_net_update": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_void_p]),
     "rfx_net_step": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_int32, C.c_void_p]),
     "rfx_net_read_loss": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_void_p]),
+    "rfx_net_run_phase": (C.c_int, [C.c_void_p, C.c_int32, C.c_float, C.c_float, C.c_float, C.c_int32,
+                                    C.c_void_p]),
+    "rfx_net_gemm_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "rfx_net_num_params": (C.c_int32, [C.c_void_p]),
     "rfx_net_param_info": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_int32),
                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
@@ -222,6 +227,11 @@ class ReforwardNet:
             out.append(OpInfo(o, name.value.decode(), OP_KINDS[kind.value], [i for i in ins if i >= 0], ot.value))
         return out
 
+    def op_attrs(self, op: int) -> Dict[str, int]:
+        a = (C.c_int32 * 8)()
+        _check(self.L.rfx_net_op_attrs(self.h, op, a))
+        return dict(zip(("R", "S", "stride", "pad", "k", "classes", "cin_real", "cout"), list(a)))
+
     def graph(self) -> Tuple[List[Tuple[str, int]], List[Tuple[str, str]]]:
         """The tensor graph handed to the planner: (name, cost) vertices, named edges."""
         ts = self.tensors()
@@ -257,13 +267,14 @@ class ReforwardNet:
         _check(self.L.rfx_net_plan_info(self.h, m, s, None))
         return [i for i in range(n) if m[i]], list(s)
 
-    def schedule(self) -> List[Tuple[str, int, int, bool]]:
+    def schedule(self) -> List[Tuple[str, int, int, bool, int]]:
+        """(kind, op, segment, is_reforward, phase) per instruction of one step."""
         n = C.c_int32()
-        _check(self.L.rfx_net_schedule(self.h, None, None, None, None, 0, C.byref(n)))
-        k, o, s, r = [(C.c_int32 * max(n.value, 1))() for _ in range(4)]
-        _check(self.L.rfx_net_schedule(self.h, k, o, s, r, n.value, C.byref(n)))
+        _check(self.L.rfx_net_schedule(self.h, None, None, None, None, None, 0, C.byref(n)))
+        k, o, s, r, ph = [(C.c_int32 * max(n.value, 1))() for _ in range(5)]
+        _check(self.L.rfx_net_schedule(self.h, k, o, s, r, ph, n.value, C.byref(n)))
         names = ["forward", "backward", "release"]
-        return [(names[k[i]], o[i], s[i], bool(r[i])) for i in range(n.value)]
+        return [(names[k[i]], o[i], s[i], bool(r[i]), ph[i]) for i in range(n.value)]
 
     # ------------------------------------------------------------ runtime
     def setup(self, seed: int = 0) -> None:
@@ -296,6 +307,15 @@ class ReforwardNet:
 
     def step(self, lr=0.1, momentum=0.9, weight_decay=0.0, use_graph=True, stream=None) -> None:
         _check(self.L.rfx_net_step(self.h, lr, momentum, weight_decay, int(use_graph), _stream(stream)))
+
+    def run_phase(self, phase: int, lr=0.1, momentum=0.9, weight_decay=0.0, use_graph=True, stream=None) -> None:
+        _check(self.L.rfx_net_run_phase(self.h, phase, lr, momentum, weight_decay, int(use_graph), _stream(stream)))
+
+    def gemm_profile(self, iters: int = 10, stream=None) -> Tuple[float, float, int]:
+        """(ms per step, algorithmic flops per step, launches) of the step's GEMMs replayed alone."""
+        ms, fl, n = C.c_double(), C.c_double(), C.c_int64()
+        _check(self.L.rfx_net_gemm_profile(self.h, iters, _stream(stream), C.byref(ms), C.byref(fl), C.byref(n)))
+        return ms.value, fl.value, n.value
 
     def read_loss(self, stream=None) -> float:
         v = C.c_float()

@@ -132,16 +132,18 @@ def record(name, g):
 
 def network_graphs(P):
     """Tensor graphs of the executor's networks (byte costs), if available."""
-    try:
-        from paper_1808_00079_b200 import networks
-    except Exception:
-        return {}
+    from paper_1808_00079_b200.executor import ReforwardNet
     out = {}
-    for name, fn in networks.GOLDEN_NETWORKS.items():
-        spec = fn()
-        vs, es = spec.planner_graph()
-        out["net_" + name] = P.from_named_edges(vs, es)
+    for arch, batch, hw, classes in NETWORKS:
+        net = ReforwardNet.named(arch, batch, hw, hw, classes)
+        vs, es = net.graph()
+        out[f"net_{arch}_b{batch}_{hw}"] = P.from_named_edges(vs, es)
     return out
+
+
+# the executor's tensor graphs (vertex = tensor, cost = arena bytes)
+NETWORKS = [("chain8", 4, 32, 10), ("resnet18", 32, 224, 1000), ("resnet34", 32, 224, 1000),
+            ("resnet50", 32, 224, 1000), ("resnet101", 32, 224, 1000), ("resnet50", 2, 64, 16)]
 
 
 def main():

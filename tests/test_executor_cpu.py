@@ -1,0 +1,111 @@
+"""Host-side executor checks (no GPU): tensor-graph plans match the reference
+planner bit-exactly, the re-forward schedule's live-activation high-water mark
+equals the planner's Eq. 1 prediction, the CPU restatement of the schedule
+reproduces plain autograd, and the C-ABI library exports every declared symbol."""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+from oracle.train_oracle import OracleNet, random_batch, rel_err
+from paper_1808_00079_b200 import LIB_PATH
+from paper_1808_00079_b200.executor import ReforwardNet
+from paper_1808_00079_b200.planner import default_planner, reference_planner
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "oracle", "_ref", "libreforward_ref.so")
+
+SMALL = [("chain8", 4, 32, 10), ("resnet18", 2, 64, 16), ("resnet50", 2, 64, 16)]
+
+
+def test_abi_exports_every_declared_symbol():
+    lib = ctypes.CDLL(LIB_PATH)
+    names = set()
+    for h in ("reforward_b200.h", "reforward_b200_exec.h"):
+        text = open(os.path.join(ROOT, "include", h)).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names |= set(re.findall(r"\b(rfx?_[a-z0-9_]+)\s*\(", text))
+    assert len(names) > 60
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+@pytest.mark.parametrize("arch,batch,hw,classes", SMALL + [("resnet50", 32, 224, 1000)])
+def test_schedule_high_water_equals_planner_total(arch, batch, hw, classes):
+    net = ReforwardNet.named(arch, batch, hw, hw, classes)
+    r = net.plan("reforward")
+    assert r.tracked_peak == r.planned_total == r.stored_cost + r.max_segment
+    assert r.arena_bytes == r.planned_total
+    s = net.plan("store_all")
+    assert s.tracked_peak == s.planned_total == s.store_all_total
+    assert s.reforward_ops == 0
+    assert r.planned_total < s.planned_total
+
+
+def test_resnet50_memory_cut_and_single_reload_per_segment():
+    net = ReforwardNet.named("resnet50", 32, 224, 224, 1000)
+    r = net.plan("reforward")
+    assert 1 - r.planned_total / r.store_all_total >= 0.60  # north-star target: >= 60 % cut
+    # every segment is computed once in the first forward and re-forwarded at
+    # most once in the backward (the last one stays resident)
+    assert r.segment_loads <= 2 * r.n_segments - 1
+
+
+@pytest.mark.parametrize("arch,batch,hw,classes", SMALL)
+def test_plan_matches_reference_planner(arch, batch, hw, classes):
+    net = ReforwardNet.named(arch, batch, hw, hw, classes)
+    net.plan("reforward")
+    stored, _ = net.plan_sets()
+    verts, edges = net.graph()
+    g = default_planner().from_named_edges(verts, edges)
+    s = g.solve_acg()
+    assert s.stored == stored
+    assert s.total == net.report().planned_total
+    if os.path.exists(REF):
+        gr = reference_planner(REF).from_named_edges(verts, edges)
+        sr = gr.solve_acg()
+        assert sr.stored == stored and sr.total == s.total
+
+
+@pytest.mark.parametrize("arch,batch,hw,classes", SMALL)
+def test_cpu_schedule_reproduces_autograd(arch, batch, hw, classes):
+    net = ReforwardNet.named(arch, batch, hw, hw, classes)
+    r = net.plan("reforward")
+    o = OracleNet(net)
+    o.init_weights(3)
+    x, y = random_batch(net, 4)
+    l0, g0 = o.reference_step(x, y)
+    stored, seg = net.plan_sets()
+    l1, g1, peak = o.run_step(x, y, net.schedule(), stored, seg)
+    assert abs(l1 - l0) <= 1e-5 * abs(l0)
+    assert max(rel_err(g1[n], g0[n]) for n in g0) <= 1e-5
+    assert peak == r.planned_total
+
+
+def test_policies_on_the_linear_chain():
+    net = ReforwardNet.named("chain8", 4, 32, 32, 10)
+    totals = {p: net.plan(p).planned_total for p in ("reforward", "lcg", "sqrt", "store_all")}
+    assert totals["reforward"] == totals["lcg"]
+    assert totals["reforward"] <= totals["sqrt"] <= totals["store_all"]
+
+
+def test_custom_network_builder_and_errors():
+    net = ReforwardNet(4)
+    x = net.input(16, 16, 3)
+    a = net.conv(x, 32, 3, 1, 1, "c1")
+    a = net.bn(a, True, "b1")
+    b = net.conv(a, 32, 3, 1, 1, "c2")
+    b = net.bn_add_relu(b, a, "add")
+    p = net.avgpool(b)
+    lg = net.fc(p, 10)
+    net.loss(lg)
+    r = net.plan("reforward")
+    assert r.tracked_peak == r.planned_total
+    with pytest.raises(RuntimeError, match="frozen"):
+        net.relu(b)
+    bad = ReforwardNet(2)
+    xi = bad.input(8, 8, 3)
+    with pytest.raises(RuntimeError, match="multiple of 8"):
+        bad.conv(xi, 30, 3, 1, 1, "c")

@@ -138,6 +138,9 @@ int rfx_net_read_param(const rfx_net* net, int32_t i, int32_t which, float* host
 int rfx_net_write_param(rfx_net* net, int32_t i, const float* host);
 int rfx_net_read_tensor(const rfx_net* net, int32_t t, float* host); /* NHWC, valid if resident */
 int rfx_net_read_bn_running(const rfx_net* net, int32_t op, float* mean, float* var);
+/* debug: give every activation gradient its own slot (call before plan) and read it back */
+int rfx_net_set_keep_grads(rfx_net* net, int32_t on);
+int rfx_net_read_grad_tensor(const rfx_net* net, int32_t t, float* host);
 /* flat fp32 gradient buffer (data-parallel all-reduce target) */
 int rfx_net_grad_buffer(const rfx_net* net, void** dev_ptr, int64_t* count);
 

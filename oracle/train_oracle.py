@@ -146,6 +146,59 @@ class OracleNet:
         self.weights = saved
         return loss.item(), grads
 
+    def op_vjp(self, op, vals, dout, labels, src):
+        """Local vector-Jacobian product of one op from the tensors the executor
+        keeps for its backward.  Returns ([(input tensor, grad)], {param: grad})."""
+        wnames = [n for n in (op.name + ".weight", op.name + ".bias") if n in self.weights]
+        ws = [self.weights[n].clone().requires_grad_(True) for n in wnames]
+        saved = {n: self.weights[n] for n in wnames}
+        for n, w in zip(wnames, ws):
+            self.weights[n] = w
+        try:
+            if op.kind == "bn_add_relu":
+                y = vals[op.inputs[0]].detach().clone().requires_grad_(True)
+                z = self._bn_only(op, y)
+                g = dout * (vals[op.out] > 0).to(dout.dtype)
+                gs = torch.autograd.grad(z, [y] + ws, grad_outputs=g)
+                in_grads = [(op.inputs[0], gs[0]), (op.inputs[1], g)]
+                wgr = gs[1:]
+            elif op.kind == "relu":  # mask from the output (the input may be released)
+                in_grads = [(op.inputs[0], dout * (vals[op.out] > 0).to(dout.dtype))]
+                wgr = []
+            elif op.kind == "avgpool":  # shape only
+                _, h, w, _c = self.tensors[op.inputs[0]].shape
+                in_grads = [(op.inputs[0], (dout / (h * w)).expand(-1, -1, h, w).contiguous())]
+                wgr = []
+            elif op.kind == "concat":
+                ca = self.tensors[op.inputs[0]].shape[3]
+                in_grads = [(op.inputs[0], dout[:, :ca].contiguous()), (op.inputs[1], dout[:, ca:].contiguous())]
+                wgr = []
+            elif op.kind == "fc" and self.emulate_bf16:
+                # the GPU feeds bf16 dlogits to the dgrad / wgrad GEMMs, fp32 to the bias sum
+                x = vals[op.inputs[0]].flatten(1)
+                db16 = self.rb(dout)
+                wb = self.rb(saved[op.name + ".weight"])
+                dx = (db16 @ wb).view_as(vals[op.inputs[0]])
+                in_grads = [(op.inputs[0], dx)]
+                wgr = [db16.t() @ x, dout.sum(0)]
+            else:
+                ins = [vals[i].detach().clone().requires_grad_(i != src) for i in op.inputs]
+                out = self.op_forward(op, ins, labels)
+                targets = [x for x, i in zip(ins, op.inputs) if i != src] + ws
+                gs = torch.autograd.grad(out, targets, grad_outputs=dout, allow_unused=True)
+                in_grads = []
+                gi = 0
+                for x, i in zip(ins, op.inputs):
+                    if i == src:
+                        continue
+                    in_grads.append((i, gs[gi] if gs[gi] is not None else torch.zeros_like(x)))
+                    gi += 1
+                wgr = gs[gi:]
+        finally:
+            for n in wnames:
+                self.weights[n] = saved[n]
+        return in_grads, {n: (g if g is not None else torch.zeros_like(saved[n])) for n, g in zip(wnames, wgr)}
+
     # ------------------------------------------------------------ schedule-following re-forward step
     def run_step(self, images: torch.Tensor, labels: torch.Tensor, schedule, stored: List[int],
                  seg_of: List[int]):
@@ -195,53 +248,10 @@ class OracleNet:
             # backward: local VJP of this op, re-executed on the tensors the
             # executor keeps for it (the residual add uses its output's mask
             # instead of the skip input)
-            wnames = [n for n in (op.name + ".weight", op.name + ".bias") if n in self.weights]
-            ws = [self.weights[n].clone().requires_grad_(True) for n in wnames]
-            saved = {n: self.weights[n] for n in wnames}
-            for n, w in zip(wnames, ws):
-                self.weights[n] = w
             dout = None if op.out == sink else grads_t.pop(op.out)
-            if op.kind == "bn_add_relu":
-                y = vals[op.inputs[0]].detach().clone().requires_grad_(True)
-                z = self._bn_only(op, y)
-                g = dout * (vals[op.out] > 0).to(dout.dtype)
-                gs = torch.autograd.grad(z, [y] + ws, grad_outputs=g)
-                in_grads = [(op.inputs[0], gs[0]), (op.inputs[1], g)]
-                wgr = gs[1:]
-            elif op.kind == "relu":  # mask from the output (the input may be released)
-                in_grads = [(op.inputs[0], dout * (vals[op.out] > 0).to(dout.dtype))]
-                wgr = []
-            elif op.kind == "avgpool":  # shape only
-                _, h, w, _c = self.tensors[op.inputs[0]].shape
-                in_grads = [(op.inputs[0], (dout / (h * w)).expand(-1, -1, h, w).contiguous())]
-                wgr = []
-            elif op.kind == "concat":
-                ca = self.tensors[op.inputs[0]].shape[3]
-                in_grads = [(op.inputs[0], dout[:, :ca].contiguous()), (op.inputs[1], dout[:, ca:].contiguous())]
-                wgr = []
-            elif op.kind == "fc" and self.emulate_bf16:
-                # the GPU feeds bf16 dlogits to the dgrad / wgrad GEMMs, fp32 to the bias sum
-                x = vals[op.inputs[0]].flatten(1)
-                db16 = self.rb(dout)
-                wb = self.rb(self.weights[op.name + ".weight"])
-                dx = (db16 @ wb).view_as(vals[op.inputs[0]])
-                in_grads = [(op.inputs[0], dx)]
-                wgr = [db16.t() @ x, dout.sum(0)]
-            else:
-                ins = [vals[i].detach().clone().requires_grad_(i != src) for i in op.inputs]
-                out = self.op_forward(op, ins, labels)
-                targets = [x for x, i in zip(ins, op.inputs) if i != src] + ws
-                gs = torch.autograd.grad(out, targets, grad_outputs=dout, allow_unused=True)
-                in_grads = []
-                gi = 0
-                for x, i in zip(ins, op.inputs):
-                    if i == src:
-                        continue
-                    in_grads.append((i, gs[gi] if gs[gi] is not None else torch.zeros_like(x)))
-                    gi += 1
-                wgr = gs[gi:]
-            for n in wnames:
-                self.weights[n] = saved[n]
+            in_grads, wgr_named = self.op_vjp(op, vals, dout, labels, src)
+            wnames = list(wgr_named)
+            wgr = [wgr_named[n] for n in wnames]
             for i, g in in_grads:
                 if i == src:
                     continue

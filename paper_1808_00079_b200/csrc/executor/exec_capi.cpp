@@ -278,6 +278,14 @@ int rfx_net_read_tensor(const rfx_net* n, int32_t t, float* host) {
   return guard([&] { n->net->read_tensor(t, host); });
 }
 
+int rfx_net_set_keep_grads(rfx_net* n, int32_t on) {
+  return guard([&] { n->net->set_keep_grads(on != 0); });
+}
+
+int rfx_net_read_grad_tensor(const rfx_net* n, int32_t t, float* host) {
+  return guard([&] { n->net->read_grad_tensor(t, host); });
+}
+
 int rfx_net_read_bn_running(const rfx_net* n, int32_t op, float* mean, float* var) {
   return guard([&] { n->net->read_bn_running(op, mean, var); });
 }

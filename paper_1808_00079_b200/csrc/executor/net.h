@@ -160,6 +160,8 @@ class Net {
   void read_param(int i, int which, float* host) const;  // which: 0 value, 1 grad, 2 momentum
   void write_param(int i, const float* host);
   void read_tensor(int t, float* host) const;
+  void read_grad_tensor(int t, float* host) const;  // valid for every tensor with keep_grads
+  void set_keep_grads(bool on) { keep_grads_ = on; }
   void read_bn_running(int op, float* mean, float* var) const;
 
   float* grad_buffer() const { return d_grad_; }
@@ -201,6 +203,7 @@ class Net {
 
   Plan plan_;
   bool planned_ = false;
+  bool keep_grads_ = false;
   std::vector<Instr> sched_;
   std::vector<long> slot_;        // arena offset per tensor (stored or segment slot)
   std::vector<long> grad_slot_;   // grad arena offset per tensor, -1 if none

@@ -187,6 +187,19 @@ void Net::read_tensor(int t, float* host) const {
   for (long i = 0; i < tt.elems(); ++i) host[i] = bf16_to_float(buf[i]);
 }
 
+void Net::read_grad_tensor(int t, float* host) const {
+  const Tensor& tt = tensors_.at(t);
+  if (grad_slot_.empty() || grad_slot_[t] < 0) throw std::invalid_argument("tensor has no gradient slot");
+  const void* src = d_grad_arena_ + grad_slot_[t];
+  if (tt.dtype == DType::F32) {
+    check(cudaMemcpy(host, src, tt.bytes(), cudaMemcpyDeviceToHost), "read_grad_tensor");
+    return;
+  }
+  std::vector<uint16_t> buf(tt.elems());
+  check(cudaMemcpy(buf.data(), src, tt.bytes(), cudaMemcpyDeviceToHost), "read_grad_tensor");
+  for (long i = 0; i < tt.elems(); ++i) host[i] = bf16_to_float(buf[i]);
+}
+
 void Net::read_bn_running(int o, float* mean, float* var) const {
   const Op& op = ops_.at(o);
   if (op.bn < 0) throw std::invalid_argument("op has no batch norm");

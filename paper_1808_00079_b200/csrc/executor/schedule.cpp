@@ -596,8 +596,9 @@ void Net::layout() {
   std::vector<Iv> active;
   long gpeak = 0;
   for (const auto& iv : ivs) {
-    active.erase(std::remove_if(active.begin(), active.end(), [&](const Iv& a) { return a.end < iv.start; }),
-                 active.end());
+    if (!keep_grads_)  // debug mode keeps every gradient tensor in its own slot
+      active.erase(std::remove_if(active.begin(), active.end(), [&](const Iv& a) { return a.end < iv.start; }),
+                   active.end());
     std::vector<std::pair<long, long>> used;
     for (const auto& a : active) used.push_back({grad_slot_[a.t], grad_slot_[a.t] + a.size});
     std::sort(used.begin(), used.end());

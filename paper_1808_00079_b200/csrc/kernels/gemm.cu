@@ -14,6 +14,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 
 #include "kernels/kernels.h"
@@ -45,6 +46,7 @@ struct alignas(64) KParams {
   float* stats;
   long split_stride;
   int remap, rP, rQ, rH, rW, rsh, rsw;
+  int stages;  // smem ring depth (<= Cfg::kStages); fewer for short K so more CTAs share an SM
 };
 
 template <int BN>
@@ -71,9 +73,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
-  uint64_t* empty = full + C::kStages;
-  uint64_t* tmem_full = empty + C::kStages;
+  const int nst = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * C::kStage);
+  uint64_t* empty = full + nst;
+  uint64_t* tmem_full = empty + nst;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);  // unused scratch
 
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 0 && elect_one()) {
     tma_prefetch(&p.ta);
     tma_prefetch(&p.tb);
-    for (int s = 0; s < C::kStages; ++s) {
+    for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             }
           }
         }
-        if (++stage == C::kStages) {
+        if (++stage == nst) {
           stage = 0;
           phase ^= 1;
         }
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (kb + 1 == kb_end) umma_commit(tmem_full);
       }
       __syncwarp();
-      if (++stage == C::kStages) {
+      if (++stage == nst) {
         stage = 0;
         phase ^= 1;
       }
@@ -274,7 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         float s[32], q2[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          s[i] = row_ok ? v[i] : 0.f;
+          // statistics of the values actually stored (bf16-rounded), so the
+          // BatchNorm that reads them back normalises exactly what it sees
+          const float sv = p.out_f32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
+          s[i] = row_ok ? sv : 0.f;
           q2[i] = s[i] * s[i];
         }
         const uint32_t lane = lane_id();
@@ -374,7 +380,7 @@ bool encode_im2col(CUtensorMap* m, const void* ptr, const ConvGeom& g, uint32_t 
 }
 
 template <int BN>
-cudaError_t launch_bn(const KParams& kp, int m_tiles, int n_tiles, int splits, cudaStream_t st) {
+cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, cudaStream_t st) {
   using C = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
@@ -382,8 +388,12 @@ cudaError_t launch_bn(const KParams& kp, int m_tiles, int n_tiles, int splits, c
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  // ring depth: enough to cover this launch's K loop (a deeper ring only
+  // costs residency), at least 2 so loads overlap MMAs
+  kp.stages = std::max(2, std::min(C::kStages, kp.kb_per_split));
+  const int smem = kp.stages * C::kStage + 1024 + 256;
   dim3 grid(m_tiles, n_tiles, splits);
-  gemm_kernel<BN><<<grid, kThreads, C::kSmem, st>>>(kp);
+  gemm_kernel<BN><<<grid, kThreads, smem, st>>>(kp);
   return cudaGetLastError();
 }
 

@@ -82,6 +82,8 @@ _SIGS = {
     "rfx_net_read_tensor": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "rfx_net_read_bn_running": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "rfx_net_grad_buffer": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "rfx_net_set_keep_grads": (C.c_int, [C.c_void_p, C.c_int32]),
+    "rfx_net_read_grad_tensor": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "rf_last_error": (C.c_char_p, []),
 }
 
@@ -352,6 +354,16 @@ class ReforwardNet:
         info = self.tensors()[t]
         a = np.empty(info.shape, dtype=np.float32)
         _check(self.L.rfx_net_read_tensor(self.h, t, a.ctypes.data_as(C.c_void_p)))
+        return a
+
+    def set_keep_grads(self, on: bool = True) -> None:
+        _check(self.L.rfx_net_set_keep_grads(self.h, int(on)))
+
+    def read_grad_tensor(self, t: int):
+        import numpy as np
+        info = self.tensors()[t]
+        a = np.empty(info.shape, dtype=np.float32)
+        _check(self.L.rfx_net_read_grad_tensor(self.h, t, a.ctypes.data_as(C.c_void_p)))
         return a
 
     def read_bn_running(self, op: int):

@@ -53,15 +53,23 @@ class OracleNet:
         self.weights: Dict[str, torch.Tensor] = {}
         self.attrs = {op.id: net.op_attrs(op.id) for op in self.ops}
 
-    def init_weights(self, seed: int = 0) -> None:
-        """Deterministic fp32 init (Kaiming convs, unit BN, small classifier)."""
+    def init_weights(self, seed: int = 0, residual_gamma: float = 1.0) -> None:
+        """Deterministic fp32 init (Kaiming convs, unit BN, small classifier).
+
+        residual_gamma scales the BN gamma that feeds each residual add (the
+        usual small/zero init of a block's last BN); deep random ResNets are
+        otherwise so ill-conditioned that bf16 storage alone decorrelates
+        their gradients from an fp32 step."""
         g = torch.Generator().manual_seed(seed)
+        joins = {op.name for op in self.ops if op.kind == "bn_add_relu"}
         for p in self.params.values():
             if p.kind == 0:
                 fan = p.shape[1] * p.shape[2] * p.shape[3]
                 w = torch.randn(p.shape, generator=g) * (2.0 / fan) ** 0.5
             elif p.kind == 1:
                 w = 1.0 + 0.1 * torch.randn(p.shape, generator=g)
+                if p.name[: -len(".weight")] in joins:
+                    w = w * residual_gamma
             elif p.kind in (2, 4):
                 w = 0.1 * torch.randn(p.shape, generator=g)
             else:

@@ -235,6 +235,9 @@ class Net {
   cudaGraphExec_t graph_exec_ = nullptr;
   float graph_lr_ = 0, graph_mom_ = 0, graph_wd_ = 0;
   cudaGraphExec_t phase_exec_[3] = {nullptr, nullptr, nullptr};
+  void* d_prep_table_ = nullptr;
+  int prep_layers_ = 0;
+  long prep_total_ = 0;
   float phase_hyper_[3][3] = {};
 
   struct GemmRecord {

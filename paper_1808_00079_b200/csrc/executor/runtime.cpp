@@ -37,6 +37,8 @@ void Net::free_device() {
     e = nullptr;
   }
   gemm_trace_.clear();
+  if (d_prep_table_) cudaFree(d_prep_table_);
+  d_prep_table_ = nullptr;
   for (void* p : {(void*)d_arena_, (void*)d_grad_arena_, (void*)d_ws_, (void*)d_param_, (void*)d_grad_,
                   (void*)d_mom_, (void*)d_bf16_, (void*)d_state_, (void*)d_input_, (void*)d_images_,
                   (void*)d_labels_, (void*)d_loss_, (void*)d_rowloss_, (void*)d_lse_, (void*)d_hyper_})
@@ -485,7 +487,8 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       const Tensor& x = tensors_[op.in[0]];
       const Tensor& y = tensors_[op.out];
       rfk::PoolGeom g{x.N, x.H, x.W, x.C, y.H, y.W, op.k, op.stride, op.pad};
-      check(rfk::maxpool_bwd(tb(op.in[0]), tb(op.out), gptr(op.out), g, gptr(op.in[0]), acc(0), st), "maxpool_bwd");
+      check(rfk::maxpool_bwd(tb(op.in[0]), tb(op.out), gptr(op.out), g, gptr(op.in[0]), acc(0), ws_zero, st),
+            "maxpool_bwd");
       break;
     }
     case OpKind::AvgPool: {
@@ -559,21 +562,40 @@ void Net::run_instr(const Instr& ins, cudaStream_t st) {
 
 // ============================================================ step
 void Net::prep_weights(cudaStream_t st) {
-  for (const auto& p : params_) {
-    const Op& op = ops_[p.op];
-    if (p.kind == 0) {
-      if (op.explicit_im2col)
-        check(rfk::conv_weight_prep(d_param_ + p.offset, op.cout, 1, 1, op.kpad, op.kpad, op.coutpad,
-                                    d_bf16_ + p.bf16_off, nullptr, st),
-              "weight prep");
-      else
-        check(rfk::conv_weight_prep(d_param_ + p.offset, op.cout, op.R, op.S, op.cpad, op.cin, op.coutpad,
-                                    d_bf16_ + p.bf16_off, d_bf16_ + p.wt_off, st),
-              "weight prep");
-    } else if (p.kind == 3) {
-      check(rfk::cast_f32_bf16(d_param_ + p.offset, p.count, d_bf16_ + p.bf16_off, st), "fc weight cast");
+  // one batched launch over every conv / fc weight (table built once)
+  if (!d_prep_table_) {
+    std::vector<rfk::WeightPrepLayer> tab;
+    long start = 0;
+    for (const auto& p : params_) {
+      if (p.kind != 0 && p.kind != 3) continue;
+      const Op& op = ops_[p.op];
+      rfk::WeightPrepLayer L{};
+      L.w = d_param_ + p.offset;
+      L.wb = d_bf16_ + p.bf16_off;
+      L.n_copy = p.count;
+      if (p.kind == 0 && !op.explicit_im2col) {
+        L.wt = d_bf16_ + p.wt_off;
+        L.cout = op.cout;
+        L.R = op.R;
+        L.S = op.S;
+        L.cpad = op.cpad;
+        L.cin = op.cin;
+        L.coutpad = op.coutpad;
+        L.n_t = p.wt_count;
+      }
+      L.start = start;
+      start += L.n_copy + L.n_t;
+      tab.push_back(L);
     }
+    prep_layers_ = (int)tab.size();
+    prep_total_ = start;
+    check(cudaMalloc(&d_prep_table_, sizeof(rfk::WeightPrepLayer) * std::max<size_t>(1, tab.size())), "prep table");
+    check(cudaMemcpy(d_prep_table_, tab.data(), sizeof(rfk::WeightPrepLayer) * tab.size(), cudaMemcpyHostToDevice),
+          "prep table");
   }
+  check(rfk::weight_prep_batched(static_cast<const rfk::WeightPrepLayer*>(d_prep_table_), prep_layers_, prep_total_,
+                                 st),
+        "weight prep");
 }
 
 void Net::load_batch(const float* images, const int* labels, bool from_host, cudaStream_t st) {

@@ -529,10 +529,12 @@ void Net::build_schedule() {
 
 // ============================================================ layout
 namespace {
+// split-K of a weight-gradient GEMM: enough splits for about one persistent
+// wave (148 CTAs), each split keeping >= 8 K blocks, at most 32 partials
 int wgrad_splits(long tiles, long kblocks) {
-  long s = (2 * 148 + tiles - 1) / tiles;
-  s = std::min(s, std::max(1L, kblocks / 4));
-  return (int)std::max(1L, std::min(s, 64L));
+  long s = (148 + tiles - 1) / tiles;
+  s = std::min(s, std::max(1L, kblocks / 8));
+  return (int)std::max(1L, std::min(s, 32L));
 }
 }  // namespace
 
@@ -642,6 +644,8 @@ void Net::layout() {
       ws_partials_ = std::max(ws_partials_, align_up((long)rfk::colstats_blocks(y.rows()) * 2 * y.C * 4));
     }
     if (op.kind == OpKind::FC) ws_misc_ = std::max(ws_misc_, align_up((long)batch_ * round8(op.classes) * 2));
+    if (op.kind == OpKind::MaxPool)  // window argmax bytes for the backward (shares the zero-insert region)
+      ws_zero_ = std::max(ws_zero_, align_up(tensors_[op.out].elems()));
   }
   for (auto& op : ops_)
     if (op.kind == OpKind::Conv && op.fuse_stats) {

@@ -46,16 +46,17 @@ struct alignas(64) KParams {
   float* stats;
   long split_stride;
   int remap, rP, rQ, rH, rW, rsh, rsw;
-  int stages;  // smem ring depth (<= Cfg::kStages); fewer for short K so more CTAs share an SM
+  int stages;  // smem ring depth (<= Cfg::kStages)
+  int m_tiles, n_tiles, splits;  // persistent tile space
 };
 
 template <int BN>
 struct Cfg {
   static constexpr int kTileB = BN * kBlockK * 2;
   static constexpr int kStage = kTileA + kTileB;
-  static constexpr int kStages = (BN == 64) ? 8 : (BN == 128 ? 6 : 4);
+  static constexpr int kStages = (BN == 64) ? 8 : (BN == 128 ? 6 : 4);  // ~190 KB ring
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
-  static constexpr int kSmem = kStages * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kStages * kStage + 4 * 2048 /*epilogue staging*/ + 1024 /*align*/ + 256;
 };
 
 // Decode a flattened output-pixel index into im2col TMA base coordinates.
@@ -68,24 +69,41 @@ __device__ __forceinline__ void pixel_base(const KParams& p, int m, int& w, int&
   h = pp * p.g_sh - p.g_pad_h;
 }
 
+// Persistent tile loop: CTA b processes tiles b, b + grid, ...; tile t ->
+// (m tile fastest, then n tile, then split).  Two TMEM accumulators let the
+// epilogue of tile i drain while the MMA warp already accumulates tile i+1,
+// and the TMA warp streams K blocks across tile boundaries.
+struct TileCoord {
+  int m0, n0, z, kb_begin, kb_end;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(const KParams& p, int t, int BN) {
+  TileCoord c;
+  const int mt = t % p.m_tiles;
+  const int rest = t / p.m_tiles;
+  c.m0 = mt * kBlockM;
+  c.n0 = (rest % p.n_tiles) * BN;
+  c.z = rest / p.n_tiles;
+  c.kb_begin = c.z * p.kb_per_split;
+  c.kb_end = min(p.num_kb, c.kb_begin + p.kb_per_split);
+  return c;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nst = p.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + nst * C::kStage);
+  uint8_t* stage_buf = smem + nst * C::kStage;  // 4 warps x 32 rows x 64 B epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + 4 * 2048);
   uint64_t* empty = full + nst;
-  uint64_t* tmem_full = empty + nst;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // unused scratch
+  uint64_t* acc_full = empty + nst;   // [2] MMA -> epilogue
+  uint64_t* acc_empty = acc_full + 2; // [2] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const uint32_t warp = warp_id();
-  const int m0 = blockIdx.x * kBlockM;
-  const int n0 = blockIdx.y * BN;
-  const int kb_begin = blockIdx.z * p.kb_per_split;
-  const int kb_end = min(p.num_kb, kb_begin + p.kb_per_split);
-  (void)red;
+  const int total = p.m_tiles * p.n_tiles * p.splits;
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&p.ta);
@@ -94,10 +112,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);  // one arrive per epilogue warp
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 1) tmem_alloc<2 * C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -106,55 +127,56 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (elect_one()) {
-      int aw = 0, ah = 0, an = 0;
-      if (p.a_kind == (int)Operand::Im2colK) pixel_base(p, m0, aw, ah, an);
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = kb_begin; kb < kb_end; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * C::kStage;
-        uint8_t* sb = sa + kTileA;
-        mbar_arrive_expect_tx(&full[stage], C::kStage);
-        // A operand
-        switch (p.a_kind) {
-          case (int)Operand::KMajor2D:
-            tma_load_2d(sa, &p.ta, &full[stage], kb * kBlockK, m0);
-            break;
-          case (int)Operand::MNMajor2D:
-            tma_load_2d(sa, &p.ta, &full[stage], m0, kb * kBlockK);
-            tma_load_2d(sa + kTileA / 2, &p.ta, &full[stage], m0 + 64, kb * kBlockK);
-            break;
-          default: {  // Im2colK: K block -> (tap, channel block)
-            const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
-            const int r = tap / p.g_S, s = tap - r * p.g_S;
-            tma_load_im2col(sa, &p.ta, &full[stage], cb * 64, aw, ah, an, (uint16_t)s, (uint16_t)r);
-          }
-        }
-        // B operand
-        switch (p.b_kind) {
-          case (int)Operand::KMajor2D:
-            tma_load_2d(sb, &p.tb, &full[stage], kb * kBlockK, n0);
-            break;
-          case (int)Operand::MNMajor2D:
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sb + j * 8192, &p.tb, &full[stage], n0 + 64 * j, kb * kBlockK);
-            break;
-          default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
-            int bw, bh, bn;
-            pixel_base(p, kb * kBlockK, bw, bh, bn);
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
-              const int nb = n0 / 64 + j;
-              const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TileCoord tc = tile_coord(p, t, BN);
+        int aw = 0, ah = 0, an = 0;
+        if (p.a_kind == (int)Operand::Im2colK) pixel_base(p, tc.m0, aw, ah, an);
+        for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStage;
+          uint8_t* sb = sa + kTileA;
+          mbar_arrive_expect_tx(&full[stage], C::kStage);
+          switch (p.a_kind) {
+            case (int)Operand::KMajor2D:
+              tma_load_2d(sa, &p.ta, &full[stage], kb * kBlockK, tc.m0);
+              break;
+            case (int)Operand::MNMajor2D:
+              tma_load_2d(sa, &p.ta, &full[stage], tc.m0, kb * kBlockK);
+              tma_load_2d(sa + kTileA / 2, &p.ta, &full[stage], tc.m0 + 64, kb * kBlockK);
+              break;
+            default: {  // Im2colK: K block -> (tap, channel block)
+              const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
               const int r = tap / p.g_S, s = tap - r * p.g_S;
-              tma_load_im2col(sb + j * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+              tma_load_im2col(sa, &p.ta, &full[stage], cb * 64, aw, ah, an, (uint16_t)s, (uint16_t)r);
             }
           }
-        }
-        if (++stage == nst) {
-          stage = 0;
-          phase ^= 1;
+          switch (p.b_kind) {
+            case (int)Operand::KMajor2D:
+              tma_load_2d(sb, &p.tb, &full[stage], kb * kBlockK, tc.n0);
+              break;
+            case (int)Operand::MNMajor2D:
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(sb + j * 8192, &p.tb, &full[stage], tc.n0 + 64 * j, kb * kBlockK);
+              break;
+            default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
+              int bw, bh, bn;
+              pixel_base(p, kb * kBlockK, bw, bh, bn);
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) {
+                const int nb = tc.n0 / 64 + j;
+                const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
+                const int r = tap / p.g_S, s = tap - r * p.g_S;
+                tma_load_im2col(sb + j * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+              }
+            }
+          }
+          if (++stage == nst) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -165,67 +187,125 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const uint32_t idesc = umma_idesc_bf16(kBlockM, BN, a_mn, b_mn);
     int stage = 0;
     uint32_t phase = 0;
-    for (int kb = kb_begin; kb < kb_end; ++kb) {
-      mbar_wait(&full[stage], phase);
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const TileCoord tc = tile_coord(p, t, BN);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&acc_empty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
       tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sa = smem_u32(smem + stage * C::kStage);
-        const uint32_t sb = sa + kTileA;
-#pragma unroll
-        for (int kk = 0; kk < kBlockK / 16; ++kk) {
-          const uint64_t da = a_mn ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
-                                   : umma_desc_sw128(sa + kk * 32, 16, 1024);
-          const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
-                                   : umma_desc_sw128(sb + kk * 32, 16, 1024);
-          umma_bf16(tmem, da, db, idesc, (kb > kb_begin || kk > 0) ? 1u : 0u);
-        }
-        umma_commit(&empty[stage]);
-        if (kb + 1 == kb_end) umma_commit(tmem_full);
+      const uint32_t d_tmem = tmem + (uint32_t)(acc * C::kTmemCols);
+      if (tc.kb_end <= tc.kb_begin) {
+        if (elect_one()) mbar_arrive(&acc_full[acc]);  // empty split: nothing to accumulate
+        __syncwarp();
+        continue;
       }
-      __syncwarp();
-      if (++stage == nst) {
-        stage = 0;
-        phase ^= 1;
+      for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * C::kStage);
+          const uint32_t sb = sa + kTileA;
+#pragma unroll
+          for (int kk = 0; kk < kBlockK / 16; ++kk) {
+            const uint64_t da = a_mn ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
+                                     : umma_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
+                                     : umma_desc_sw128(sb + kk * 32, 16, 1024);
+            umma_bf16(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (kb + 1 == tc.kb_end) umma_commit(&acc_full[acc]);
+        }
+        __syncwarp();
+        if (++stage == nst) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
     }
   } else {
     // ------------------------------------------------ epilogue (warps 2..5)
     const uint32_t quarter = warp & 3;
-    const int row_local = quarter * 32 + lane_id();
-    const int m = m0 + row_local;
-    const bool row_ok = m < p.M;
-    const bool empty_k = kb_end <= kb_begin;
-    if (!empty_k) {
-      mbar_wait(tmem_full, 0);
+    const uint32_t lane = lane_id();
+    uint8_t* stg = stage_buf + quarter * 2048;  // this warp's 32 x 64 B staging tile
+    __shared__ float red_s[4][32], red_q[4][32];
+    int local = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+      const TileCoord tc = tile_coord(p, t, BN);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      const bool empty_k = tc.kb_end <= tc.kb_begin;
+      mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-    }
-    long out_row = m;
-    if (p.remap && row_ok) {
-      const int q = m % p.rQ, t = m / p.rQ, pp = t % p.rP, nn = t / p.rP;
-      out_row = (long)nn * p.rH * p.rW + (long)(pp * p.rsh) * p.rW + (long)q * p.rsw;
-    }
+      const int m = tc.m0 + (int)(quarter * 32 + lane);
+      const bool row_ok = m < p.M;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      if (!empty_k) {
-        tmem_ld32(tmem + ((quarter * 32u) << 16) + (uint32_t)c0, r);
-        tmem_ld_wait();
-      } else {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        if (!empty_k) {
+          tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
+          tmem_ld_wait();
+        } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) r[i] = 0u;
-      }
-      float v[32];
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (c0 + 32 >= BN) {
+          // every column of this accumulator is in registers: hand it back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[acc]);
+        }
+        float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-      const int col0 = n0 + c0;
-      if (p.bias) {
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        const int col0 = tc.n0 + c0;
+        if (col0 >= p.N) continue;  // warp-uniform
+        const bool full_cols = col0 + 32 <= p.N;
+        if (p.bias) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] += (col0 + i < p.N) ? p.bias[col0 + i] : 0.f;
-      }
-      if (row_ok) {
+          for (int i = 0; i < 32; ++i) v[i] += (col0 + i < p.N) ? __ldg(p.bias + col0 + i) : 0.f;
+        }
+        if (p.stats) {
+          // Column sums over this warp's 32 rows by a halving butterfly: after
+          // 5 rounds lane l holds column l's total (31 shuffles per 32 columns).
+          float s[32], q2[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            // statistics of the values actually stored (bf16-rounded), so the
+            // BatchNorm that reads them back normalises exactly what it sees
+            const float sv = p.out_f32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
+            s[i] = row_ok ? sv : 0.f;
+            q2[i] = s[i] * s[i];
+          }
+#pragma unroll
+          for (int half = 16; half >= 1; half >>= 1) {
+            const bool upper = (lane & half) != 0;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+              const float send_s = upper ? s[i] : s[i + half];
+              const float send_q = upper ? q2[i] : q2[i + half];
+              const float got_s = __shfl_xor_sync(0xffffffffu, send_s, half);
+              const float got_q = __shfl_xor_sync(0xffffffffu, send_q, half);
+              s[i] = (upper ? s[i + half] : s[i]) + got_s;
+              q2[i] = (upper ? q2[i + half] : q2[i]) + got_q;
+            }
+          }
+          const int col = col0 + (int)lane;
+          float* st = p.stats + (long)(tc.m0 / kBlockM) * 2 * p.N;
+          red_s[quarter][lane] = s[0];
+          red_q[quarter][lane] = q2[0];
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (quarter == 0 && col < p.N) {  // fixed order over the four row quarters
+            st[col] = ((red_s[0][lane] + red_s[1][lane]) + red_s[2][lane]) + red_s[3][lane];
+            st[p.N + col] = ((red_q[0][lane] + red_q[1][lane]) + red_q[2][lane]) + red_q[3][lane];
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         if (p.out_f32) {
-          float* dst = reinterpret_cast<float*>(p.out) + (long)blockIdx.z * p.split_stride + out_row * p.ldc + col0;
-          if (col0 + 32 <= p.N) {
+          float* dst = reinterpret_cast<float*>(p.out) + (long)tc.z * p.split_stride + (long)m * p.ldc + col0;
+          if (!row_ok) {
+          } else if (full_cols) {
             if (p.accumulate_out) {
 #pragma unroll
               for (int i = 0; i < 32; ++i) dst[i] += v[i];
@@ -234,97 +314,68 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
             }
           } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) dst[i] = p.accumulate_out ? dst[i] + v[i] : v[i];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.N) dst[i] = p.accumulate_out ? dst[i] + v[i] : v[i];
           }
-        } else {
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long)blockIdx.z * p.split_stride +
-                               out_row * p.ldc + col0;
-          if (p.accumulate_out) {
-            if (col0 + 32 <= p.N) {
+          continue;
+        }
+        // ---- bf16 output: stage the warp's 32 x 32 tile in smem (16-byte
+        // chunks XOR-swizzled by row), then write whole 64-byte row segments
+        // with 4 lanes per row: 8 rows per instruction instead of 32.
+        uint32_t w[16];
 #pragma unroll
-              for (int i = 0; i < 32; i += 8) {
-                const uint4 o = *reinterpret_cast<const uint4*>(dst + i);
-                const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&o);
+        for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const float2 f = __bfloat1622float2(ob[j]);
-                  v[i + 2 * j] += f.x;
-                  v[i + 2 * j + 1] += f.y;
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t sw = (uint32_t)j ^ ((lane >> 1) & 3u);
+          *reinterpret_cast<uint4*>(stg + lane * 64 + sw * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const uint32_t row = it * 8 + (lane >> 2), chunk = lane & 3;
+          const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 64 + ((chunk ^ ((row >> 1) & 3u)) * 16));
+          const int mr = tc.m0 + (int)(quarter * 32 + row);
+          if (mr < p.M && (full_cols || col0 + (int)chunk * 8 < p.N)) {
+            long orow = mr;
+            if (p.remap) {
+              const int q = mr % p.rQ, tt = mr / p.rQ, pp = tt % p.rP, nn = tt / p.rP;
+              orow = (long)nn * p.rH * p.rW + (long)(pp * p.rsh) * p.rW + (long)q * p.rsw;
+            }
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long)tc.z * p.split_stride +
+                                 orow * p.ldc + col0 + chunk * 8;
+            if (full_cols || col0 + (int)chunk * 8 + 8 <= p.N) {
+              uint4 o = val;
+              if (p.accumulate_out) {
+                const uint4 prev = *reinterpret_cast<const uint4*>(dst);
+                const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&val);
+                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&prev);
+                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 fa = __bfloat1622float2(a2[e]), fb = __bfloat1622float2(b2[e]);
+                  o2[e] = __floats2bfloat162_rn(fa.x + fb.x, fa.y + fb.y);
                 }
               }
+              *reinterpret_cast<uint4*>(dst) = o;
             } else {
-              for (int i = 0; i < 32 && col0 + i < p.N; ++i) v[i] += __bfloat162float(dst[i]);
+              const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&val);
+              for (int e = 0; e < 8 && col0 + (int)chunk * 8 + e < p.N; ++e)
+                dst[e] = p.accumulate_out ? __float2bfloat16_rn(__bfloat162float(dst[e]) + __bfloat162float(vb[e]))
+                                          : vb[e];
             }
           }
-          if (col0 + 32 <= p.N) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-              uint4 w;
-              w.x = pack_bf16(v[i], v[i + 1]);
-              w.y = pack_bf16(v[i + 2], v[i + 3]);
-              w.z = pack_bf16(v[i + 4], v[i + 5]);
-              w.w = pack_bf16(v[i + 6], v[i + 7]);
-              *reinterpret_cast<uint4*>(dst + i) = w;
-            }
-          } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) dst[i] = __float2bfloat16_rn(v[i]);
-          }
         }
-      }
-      if (p.stats) {
-        // Column sums over this warp's 32 rows by a halving butterfly: after
-        // 5 rounds lane l holds column l's total (31 shuffles per 32 columns).
-        float s[32], q2[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          // statistics of the values actually stored (bf16-rounded), so the
-          // BatchNorm that reads them back normalises exactly what it sees
-          const float sv = p.out_f32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
-          s[i] = row_ok ? sv : 0.f;
-          q2[i] = s[i] * s[i];
-        }
-        const uint32_t lane = lane_id();
-#pragma unroll
-        for (int half = 16; half >= 1; half >>= 1) {
-          const bool upper = (lane & half) != 0;
-#pragma unroll
-          for (int i = 0; i < half; ++i) {
-            // lanes with bit `half` set keep the upper half of the live window
-            const float send_s = upper ? s[i] : s[i + half];
-            const float send_q = upper ? q2[i] : q2[i + half];
-            const float got_s = __shfl_xor_sync(0xffffffffu, send_s, half);
-            const float got_q = __shfl_xor_sync(0xffffffffu, send_q, half);
-            const float keep_s = upper ? s[i + half] : s[i];
-            const float keep_q = upper ? q2[i + half] : q2[i];
-            s[i] = keep_s + got_s;
-            q2[i] = keep_q + got_q;
-          }
-        }
-        // lane l now owns column c0 + l of this warp's 32 rows
-        const int col = col0 + (int)lane;
-        float* st = p.stats + (long)blockIdx.x * 2 * p.N;
-        float* part = st;  // per-warp partials combined through shared memory below
-        (void)part;
-        __shared__ float red_s[4][32], red_q[4][32];
-        red_s[quarter][lane] = s[0];
-        red_q[quarter][lane] = q2[0];
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (quarter == 0 && col < p.N) {
-          // fixed order over the four row quarters: deterministic
-          const float ts = ((red_s[0][lane] + red_s[1][lane]) + red_s[2][lane]) + red_s[3][lane];
-          const float tq = ((red_q[0][lane] + red_q[1][lane]) + red_q[2][lane]) + red_q[3][lane];
-          st[col] = ts;
-          st[p.N + col] = tq;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        __syncwarp();
       }
     }
-    tc_fence_before();
   }
+  tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem);
+    tmem_dealloc<2 * C::kTmemCols>(tmem);
   }
 }
 
@@ -388,11 +439,22 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, cudaStr
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  // ring depth: enough to cover this launch's K loop (a deeper ring only
-  // costs residency), at least 2 so loads overlap MMAs
-  kp.stages = std::max(2, std::min(C::kStages, kp.kb_per_split));
-  const int smem = kp.stages * C::kStage + 1024 + 256;
-  dim3 grid(m_tiles, n_tiles, splits);
+  // persistent grid: one CTA per SM (two TMEM accumulators of BN columns)
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long total = (long)m_tiles * n_tiles * splits;
+  const int grid = (int)std::min<long>(total, sms);
+  kp.m_tiles = m_tiles;
+  kp.n_tiles = n_tiles;
+  kp.splits = splits;
+  const long kb_per_cta = (long)kp.kb_per_split * ((total + grid - 1) / grid);
+  kp.stages = (int)std::max<long>(2, std::min<long>(C::kStages, kb_per_cta));
+  const int smem = kp.stages * C::kStage + 4 * 2048 + 1024 + 256;
   gemm_kernel<BN><<<grid, kThreads, smem, st>>>(kp);
   return cudaGetLastError();
 }
@@ -406,7 +468,22 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   if (!g_encode_tiled || !g_encode_im2col) return cudaErrorNotSupported;
   if (d.M <= 0 || d.N <= 0) return cudaSuccess;
   int bn = d.block_n;
-  if (bn == 0) bn = d.N <= 64 ? 64 : (d.N <= 128 ? 128 : 256);
+  if (bn == 0) {
+    // pick the tile width that minimises (tiles per SM, rounded up) x width:
+    // wide tiles when there is plenty of parallelism, narrow ones when a
+    // wide grid would leave SMs idle
+    const long mt = (d.M + kBlockM - 1) / kBlockM;
+    long best = -1;
+    for (int cand : {256, 128, 64}) {
+      if (cand > 64 && d.N <= cand / 2) continue;
+      const long tiles = mt * ((d.N + cand - 1) / cand) * std::max(1, d.splits);
+      const long cost = ((tiles + 147) / 148) * (long)cand;
+      if (best < 0 || cost < best) {
+        best = cost;
+        bn = cand;
+      }
+    }
+  }
   if (d.b_kind == Operand::MNMajor2D || d.b_kind == Operand::Im2colMN) bn = bn < 64 ? 64 : bn;
   if (bn != 64 && bn != 128 && bn != 256) return cudaErrorInvalidValue;
 

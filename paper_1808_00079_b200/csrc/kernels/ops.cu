@@ -113,23 +113,38 @@ __global__ void __launch_bounds__(kThreads) colstats_kernel(const __nv_bfloat16*
 }
 
 // Sum `parts` partial rows [parts][2][C] in a fixed tree: channel per
-// threadIdx.x (32 wide), partial subsets per threadIdx.y (8 deep).
+// threadIdx.x (32 wide), partial subsets per threadIdx.y (32 deep, two
+// independent accumulators each), then a fixed-shape smem tree over y.
+constexpr int kFinY = 32;
 __device__ __forceinline__ void sum_partials(const float* __restrict__ partials, int parts, int C, int c, float& s0,
                                              float& s1) {
-  __shared__ float sh0[8][33], sh1[8][33];
-  float a = 0.f, b = 0.f;
-  if (c < C)
-    for (int p = threadIdx.y; p < parts; p += 8) {
-      a += partials[(long)p * 2 * C + c];
-      b += partials[(long)p * 2 * C + C + c];
+  __shared__ float sh0[kFinY][33], sh1[kFinY][33];
+  float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+  if (c < C) {
+    int p = threadIdx.y;
+    for (; p + kFinY < parts; p += 2 * kFinY) {
+      a0 += __ldg(partials + (long)p * 2 * C + c);
+      b0 += __ldg(partials + (long)p * 2 * C + C + c);
+      a1 += __ldg(partials + (long)(p + kFinY) * 2 * C + c);
+      b1 += __ldg(partials + (long)(p + kFinY) * 2 * C + C + c);
     }
-  sh0[threadIdx.y][threadIdx.x] = a;
-  sh1[threadIdx.y][threadIdx.x] = b;
+    if (p < parts) {
+      a0 += __ldg(partials + (long)p * 2 * C + c);
+      b0 += __ldg(partials + (long)p * 2 * C + C + c);
+    }
+  }
+  sh0[threadIdx.y][threadIdx.x] = a0 + a1;
+  sh1[threadIdx.y][threadIdx.x] = b0 + b1;
   __syncthreads();
-  s0 = ((sh0[0][threadIdx.x] + sh0[1][threadIdx.x]) + (sh0[2][threadIdx.x] + sh0[3][threadIdx.x])) +
-       ((sh0[4][threadIdx.x] + sh0[5][threadIdx.x]) + (sh0[6][threadIdx.x] + sh0[7][threadIdx.x]));
-  s1 = ((sh1[0][threadIdx.x] + sh1[1][threadIdx.x]) + (sh1[2][threadIdx.x] + sh1[3][threadIdx.x])) +
-       ((sh1[4][threadIdx.x] + sh1[5][threadIdx.x]) + (sh1[6][threadIdx.x] + sh1[7][threadIdx.x]));
+  for (int w = kFinY / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.y < w) {
+      sh0[threadIdx.y][threadIdx.x] += sh0[threadIdx.y + w][threadIdx.x];
+      sh1[threadIdx.y][threadIdx.x] += sh1[threadIdx.y + w][threadIdx.x];
+    }
+    __syncthreads();
+  }
+  s0 = sh0[0][threadIdx.x];
+  s1 = sh1[0][threadIdx.x];
 }
 
 __global__ void bn_finalize_kernel(const float* __restrict__ partials, int parts, int C, float count,
@@ -158,23 +173,50 @@ __global__ void bn_finalize_kernel(const float* __restrict__ partials, int parts
 
 // out = [relu](y * scale + shift [+ skip])
 // (skip may alias out: each element is read before it is written)
+__device__ __forceinline__ void ld8f(const float* p, float (&f)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+  f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w, f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+}
+
+// Each thread streams kVec 16-byte vectors per iteration, all loads issued
+// before any math, so every SM keeps enough bytes in flight for HBM.
+constexpr int kVec = 2;
+
 __global__ void __launch_bounds__(kThreads) bn_apply_kernel(const __nv_bfloat16* __restrict__ y,
                                                            const __nv_bfloat16* skip, const float* __restrict__ scale,
                                                            const float* __restrict__ shift, int relu, long nvec, int C,
                                                            __nv_bfloat16* out) {
-  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
-    const int c0 = (int)((v * 8) % C);
-    float f[8];
-    unpack8(ldg16(y + v * 8), f);
-    float k[8];
-    if (skip) unpack8(*reinterpret_cast<const uint4*>(skip + v * 8), k);
+  const int cv = C / 8;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long v0 = (long)blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * kVec) {
+    uint4 yv[kVec], kv[kVec];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float o = f[i] * __ldg(scale + c0 + i) + __ldg(shift + c0 + i);
-      if (skip) o += k[i];
-      f[i] = relu ? fmaxf(o, 0.f) : o;
+    for (int u = 0; u < kVec; ++u) {
+      const long v = v0 + u * stride;
+      if (v < nvec) {
+        yv[u] = ldg16(y + v * 8);
+        if (skip) kv[u] = *reinterpret_cast<const uint4*>(skip + v * 8);
+      }
     }
-    *reinterpret_cast<uint4*>(out + v * 8) = pack8(f);
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) {
+      const long v = v0 + u * stride;
+      if (v >= nvec) break;
+      const int c0 = (int)(v % cv) * 8;
+      float f[8], sc[8], sh[8], k[8];
+      unpack8(yv[u], f);
+      ld8f(scale + c0, sc);
+      ld8f(shift + c0, sh);
+      if (skip) unpack8(kv[u], k);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float o = fmaf(f[i], sc[i], sh[i]);
+        if (skip) o += k[i];
+        f[i] = relu ? fmaxf(o, 0.f) : o;
+      }
+      *reinterpret_cast<uint4*>(out + v * 8) = pack8(f);
+    }
   }
 }
 
@@ -208,13 +250,16 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(
     for (long r = r0 + rgrp; r < r1; r += s.rows_per_pass) {
       const long off = r * C + c0;
       float fy[8], fd[8], fo[8];
-      unpack8(ldg16(y + off), fy);
-      unpack8(ldg16(dout + off), fd);
-      if (mask_mode == 2) unpack8(ldg16(out + off), fo);
+      const uint4 uy = ldg16(y + off), ud = ldg16(dout + off);
+      uint4 uo = make_uint4(0, 0, 0, 0);
+      if (mask_mode == 2) uo = ldg16(out + off);
+      unpack8(uy, fy);
+      unpack8(ud, fd);
+      if (mask_mode == 2) unpack8(uo, fo);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float g = fd[i];
-        if (mask_mode == 1) g = (fy[i] * sc[i] + sf[i] > 0.f) ? g : 0.f;
+        if (mask_mode == 1) g = (fmaf(fy[i], sc[i], sf[i]) > 0.f) ? g : 0.f;  // same expression as the forward
         if (mask_mode == 2) g = (fo[i] > 0.f) ? g : 0.f;
         a[i] += g;
         b[i] += g * (fy[i] - mu[i]) * is[i];
@@ -267,20 +312,31 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(
     const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
     int mask_mode, const float* __restrict__ scale, const float* __restrict__ shift, const float* __restrict__ coef,
     long nvec, int C, __nv_bfloat16* __restrict__ dy, int acc_dy, __nv_bfloat16* __restrict__ dskip, int acc_dskip) {
+  const int cv = C / 8;
   for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
-    const int c0 = (int)((v * 8) % C);
+    const int c0 = (int)(v % cv) * 8;
     const long off = v * 8;
-    float fy[8], fd[8], fo[8], r[8], sk[8];
-    unpack8(ldg16(y + off), fy);
-    unpack8(ldg16(dout + off), fd);
-    if (mask_mode == 2) unpack8(ldg16(out + off), fo);
+    float fy[8], fd[8], fo[8], r[8], sk[8], k1[8], k2[8], k3[8], sc[8], sh[8];
+    const uint4 uy = ldg16(y + off), ud = ldg16(dout + off);
+    uint4 uo = make_uint4(0, 0, 0, 0);
+    if (mask_mode == 2) uo = ldg16(out + off);
+    unpack8(uy, fy);
+    unpack8(ud, fd);
+    if (mask_mode == 2) unpack8(uo, fo);
+    ld8f(coef + c0, k1);
+    ld8f(coef + C + c0, k2);
+    ld8f(coef + 2 * C + c0, k3);
+    if (mask_mode == 1) {
+      ld8f(scale + c0, sc);
+      ld8f(shift + c0, sh);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       float g = fd[i];
-      if (mask_mode == 1) g = (fy[i] * __ldg(scale + c0 + i) + __ldg(shift + c0 + i) > 0.f) ? g : 0.f;
+      if (mask_mode == 1) g = (fmaf(fy[i], sc[i], sh[i]) > 0.f) ? g : 0.f;  // same expression as the forward
       if (mask_mode == 2) g = (fo[i] > 0.f) ? g : 0.f;
       sk[i] = g;
-      r[i] = __ldg(coef + c0 + i) * g + __ldg(coef + C + c0 + i) * fy[i] + __ldg(coef + 2 * C + c0 + i);
+      r[i] = k1[i] * g + k2[i] * fy[i] + k3[i];
     }
     if (acc_dy) {
       float prev[8];
@@ -362,10 +418,52 @@ __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat
   }
 }
 
-// Gather form: each input element collects dy from every window whose first
-// maximum it is (windows scanned in row-major order, ties to the first hit).
-__global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x,
-                                                              const __nv_bfloat16* __restrict__ y,
+// Backward, pass 1: first argmax (row-major window position, ties to the
+// first hit) of every window and channel, one byte each.
+__global__ void __launch_bounds__(kThreads) maxpool_argmax_kernel(const __nv_bfloat16* __restrict__ x, PoolGeom g,
+                                                                 uint8_t* __restrict__ idx) {
+  const int cv = g.C / 8;
+  const long total = (long)g.N * g.P * g.Q * cv;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    long t = i / cv;
+    const int q = (int)(t % g.Q);
+    t /= g.Q;
+    const int p = (int)(t % g.P);
+    const int n = (int)(t / g.P);
+    float m[8];
+    uint32_t best[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      m[k] = -INFINITY;
+      best[k] = 0;
+    }
+    for (int r = 0; r < g.k; ++r) {
+      const int h = p * g.stride - g.pad + r;
+      if (h < 0 || h >= g.H) continue;
+      for (int s = 0; s < g.k; ++s) {
+        const int w = q * g.stride - g.pad + s;
+        if (w < 0 || w >= g.W) continue;
+        float f[8];
+        unpack8(ldg16(x + (((long)n * g.H + h) * g.W + w) * g.C + c8 * 8), f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (f[k] > m[k]) {
+            m[k] = f[k];
+            best[k] = (uint32_t)(r * g.k + s);
+          }
+      }
+    }
+    uint2 o;
+    o.x = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+    o.y = best[4] | (best[5] << 8) | (best[6] << 16) | (best[7] << 24);
+    *reinterpret_cast<uint2*>(idx + i * 8) = o;
+  }
+}
+
+// Backward, pass 2 (gather, no atomics): each input element sums, in fixed
+// window order, dy of every covering window whose argmax it is.
+__global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __restrict__ idx,
                                                               const __nv_bfloat16* __restrict__ dy, PoolGeom g,
                                                               __nv_bfloat16* __restrict__ dx, int acc) {
   const int cv = g.C / 8;
@@ -377,10 +475,9 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const __nv_bfloat
     t /= g.W;
     const int h = (int)(t % g.H);
     const int n = (int)(t / g.H);
-    float xv[8], acc_v[8];
-    unpack8(ldg16(x + i * 8), xv);
+    float sum[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) acc_v[k] = 0.f;
+    for (int k = 0; k < 8; ++k) sum[k] = 0.f;
     // windows p with p*stride - pad <= h <= p*stride - pad + k - 1
     const int p_lo = max(0, (h + g.pad - g.k + g.stride) / g.stride);
     const int p_hi = min(g.P - 1, (h + g.pad) / g.stride);
@@ -388,43 +485,24 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const __nv_bfloat
     const int q_hi = min(g.Q - 1, (w + g.pad) / g.stride);
     for (int p = p_lo; p <= p_hi; ++p)
       for (int q = q_lo; q <= q_hi; ++q) {
-        const long o = (((long)n * g.P + p) * g.Q + q) * g.C + c8 * 8;
-        float yv[8], dv[8];
-        unpack8(ldg16(y + o), yv);
-        unpack8(ldg16(dy + o), dv);
-        // is (h, w) the first position in this window holding the max?
-        bool first[8];
+        const long o = ((((long)n * g.P + p) * g.Q + q) * cv + c8);
+        const uint2 iv = __ldg(reinterpret_cast<const uint2*>(idx + o * 8));
+        const uint32_t self = (uint32_t)((h - (p * g.stride - g.pad)) * g.k + (w - (q * g.stride - g.pad)));
+        float dv[8];
+        unpack8(ldg16(dy + o * 8), dv);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) first[k] = xv[k] == yv[k];
-        const int h0 = p * g.stride - g.pad, w0 = q * g.stride - g.pad;
-        for (int r = 0; r < g.k; ++r) {
-          const int hh = h0 + r;
-          if (hh < 0 || hh >= g.H) continue;
-          for (int s = 0; s < g.k; ++s) {
-            const int ww = w0 + s;
-            if (ww < 0 || ww >= g.W) continue;
-            if (hh > h || (hh == h && ww >= w)) {
-              r = g.k;
-              break;
-            }
-            float e[8];
-            unpack8(ldg16(x + (((long)n * g.H + hh) * g.W + ww) * g.C + c8 * 8), e);
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (e[k] == yv[k]) first[k] = false;
-          }
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t b = ((k < 4 ? iv.x : iv.y) >> (8 * (k & 3))) & 0xffu;
+          if (b == self) sum[k] += dv[k];
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          if (first[k]) acc_v[k] += dv[k];
       }
     if (acc) {
       float pv[8];
       unpack8(*reinterpret_cast<const uint4*>(dx + i * 8), pv);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) acc_v[k] += pv[k];
+      for (int k = 0; k < 8; ++k) sum[k] += pv[k];
     }
-    *reinterpret_cast<uint4*>(dx + i * 8) = pack8(acc_v);
+    *reinterpret_cast<uint4*>(dx + i * 8) = pack8(sum);
   }
 }
 
@@ -594,6 +672,34 @@ __global__ void conv_weight_prep_kernel(const float* __restrict__ w, int Cout, i
   }
 }
 
+__global__ void __launch_bounds__(kThreads) weight_prep_batched_kernel(const WeightPrepLayer* __restrict__ tab,
+                                                                      int layers, long total) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = layers - 1;  // last layer with start <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tab[mid].start <= i) lo = mid;
+      else hi = mid - 1;
+    }
+    const WeightPrepLayer& L = tab[lo];
+    long e = i - L.start;
+    if (e < L.n_copy) {  // coalesced copy in GEMM layout
+      L.wb[e] = __float2bfloat16_rn(L.w[e]);
+      continue;
+    }
+    e -= L.n_copy;  // transpose, iterated in output order: wt[ci][r'][s'][co]
+    const int co = (int)(e % L.coutpad);
+    long t = e / L.coutpad;
+    const int s2 = (int)(t % L.S);
+    t /= L.S;
+    const int r2 = (int)(t % L.R);
+    const int ci = (int)(t / L.R);
+    float v = 0.f;
+    if (co < L.cout) v = L.w[(((long)co * L.R + (L.R - 1 - r2)) * L.S + (L.S - 1 - s2)) * L.cpad + ci];
+    L.wt[e] = __float2bfloat16_rn(v);
+  }
+}
+
 // NCHW fp32 -> NHWC bf16 with zero channel padding to Cpad
 __global__ void pack_input_kernel(const float* __restrict__ x, int N, int C, int H, int W, int Cpad,
                                   __nv_bfloat16* __restrict__ out) {
@@ -612,26 +718,45 @@ __global__ void pack_input_kernel(const float* __restrict__ x, int N, int C, int
 
 // explicit im2col for thin-channel convs: out[m][k], k = (r*S + s)*C + c, K
 // padded with zeros to Kpad.
-__global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x, ConvShape g, int Kpad,
-                              __nv_bfloat16* __restrict__ out) {
-  const long total = (long)g.N * g.P * g.Q * Kpad;
+// One thread per (output pixel, 8 consecutive k): a single 16-byte store;
+// the pixel decode is done once per thread.
+__global__ void __launch_bounds__(kThreads) im2col_kernel(const __nv_bfloat16* __restrict__ x, ConvShape g, int Kpad,
+                                                         __nv_bfloat16* __restrict__ out) {
+  const int kv = Kpad / 8;
+  const long total = (long)g.N * g.P * g.Q * kv;
   const int Kreal = g.R * g.S * g.C;
+  const unsigned short* xs = reinterpret_cast<const unsigned short*>(x);
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const int k = (int)(i % Kpad);
-    const long m = i / Kpad;
-    float v = 0.f;
-    if (k < Kreal) {
-      const int c = k % g.C;
-      const int rs = k / g.C;
-      const int s = rs % g.S, r = rs / g.S;
-      const int q = (int)(m % g.Q);
-      const long t = m / g.Q;
-      const int p = (int)(t % g.P);
-      const int n = (int)(t / g.P);
-      const int h = p * g.stride - g.pad + r, w = q * g.stride - g.pad + s;
-      if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = __bfloat162float(x[(((long)n * g.H + h) * g.W + w) * g.Cs + c]);
+    const int k0 = (int)(i % kv) * 8;
+    const long m = i / kv;
+    const int q = (int)(m % g.Q);
+    const long t = m / g.Q;
+    const int p = (int)(t % g.P);
+    const int n = (int)(t / g.P);
+    const int h0 = p * g.stride - g.pad, w0 = q * g.stride - g.pad;
+    const unsigned short* base = xs + (long)n * g.H * g.W * g.Cs;
+    unsigned short e[8];
+    int c = k0 % g.C, rs = k0 / g.C;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      unsigned short v = 0;
+      if (k0 + j < Kreal) {
+        const int s = rs % g.S, r = rs / g.S;
+        const int h = h0 + r, w = w0 + s;
+        if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = __ldg(base + ((long)h * g.W + w) * g.Cs + c);
+      }
+      e[j] = v;
+      if (++c == g.C) {
+        c = 0;
+        ++rs;
+      }
     }
-    out[i] = __float2bfloat16_rn(v);
+    uint4 o;
+    o.x = e[0] | ((uint32_t)e[1] << 16);
+    o.y = e[2] | ((uint32_t)e[3] << 16);
+    o.z = e[4] | ((uint32_t)e[5] << 16);
+    o.w = e[6] | ((uint32_t)e[7] << 16);
+    *reinterpret_cast<uint4*>(out + m * Kpad + k0) = o;
   }
 }
 
@@ -736,7 +861,7 @@ cudaError_t colstats(const __nv_bfloat16* x, long M, int C, float* partials, int
 cudaError_t bn_finalize(const float* partials, int parts, int C, long count, const float* gamma, const float* beta,
                         float eps, float* mean, float* invstd, float* scale, float* shift, float* run_mean,
                         float* run_var, float momentum, bool update_running, cudaStream_t st) {
-  bn_finalize_kernel<<<(C + 31) / 32, dim3(32, 8), 0, st>>>(partials, parts, C, (float)count, gamma, beta, eps, mean,
+  bn_finalize_kernel<<<(C + 31) / 32, dim3(32, kFinY), 0, st>>>(partials, parts, C, (float)count, gamma, beta, eps, mean,
                                                             invstd, scale, shift, run_mean, run_var, momentum,
                                                             update_running ? 1 : 0);
   return cudaGetLastError();
@@ -758,7 +883,7 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
   dim3 grid(blocks, (C + 2047) / 2048);
   bn_bwd_reduce_kernel<<<grid, kThreads, 0, st>>>(y, dout, out, mask_mode, mean, invstd, scale, shift, M, C,
                                                   rows_per_block_for(M, blocks), partials);
-  bn_bwd_finalize_kernel<<<(C + 31) / 32, dim3(32, 8), 0, st>>>(partials, blocks, C, (float)M, gamma, mean, invstd,
+  bn_bwd_finalize_kernel<<<(C + 31) / 32, dim3(32, kFinY), 0, st>>>(partials, blocks, C, (float)M, gamma, mean, invstd,
                                                                 dgamma, dbeta, coef);
   const long nvec = M * C / 8;
   bn_bwd_apply_kernel<<<grid_for(nvec, kThreads * 4), kThreads, 0, st>>>(y, dout, out, mask_mode, scale, shift, coef,
@@ -785,9 +910,14 @@ cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16
 }
 
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __nv_bfloat16* dy, const PoolGeom& g,
-                        __nv_bfloat16* dx, bool acc, cudaStream_t st) {
+                        __nv_bfloat16* dx, bool acc, void* idx_ws, cudaStream_t st) {
+  (void)y;
+  if (g.k * g.k > 256) return cudaErrorInvalidValue;
+  uint8_t* idx = static_cast<uint8_t*>(idx_ws);
+  const long wins = (long)g.N * g.P * g.Q * (g.C / 8);
+  maxpool_argmax_kernel<<<grid_for(wins, kThreads * 2), kThreads, 0, st>>>(x, g, idx);
   const long work = (long)g.N * g.H * g.W * (g.C / 8);
-  maxpool_bwd_kernel<<<grid_for(work, kThreads * 2), kThreads, 0, st>>>(x, y, dy, g, dx, acc ? 1 : 0);
+  maxpool_bwd_kernel<<<grid_for(work, kThreads * 2), kThreads, 0, st>>>(idx, dy, g, dx, acc ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -855,6 +985,12 @@ cudaError_t conv_weight_prep(const float* w, int Cout, int R, int S, int Cpad, i
   return cudaGetLastError();
 }
 
+cudaError_t weight_prep_batched(const WeightPrepLayer* table_dev, int layers, long total, cudaStream_t st) {
+  if (layers <= 0 || total <= 0) return cudaSuccess;
+  weight_prep_batched_kernel<<<grid_for(total, kThreads * 8, 148 * 16), kThreads, 0, st>>>(table_dev, layers, total);
+  return cudaGetLastError();
+}
+
 cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __nv_bfloat16* out, cudaStream_t st) {
   const long total = (long)N * H * W * Cpad;
   pack_input_kernel<<<grid_for(total, kThreads * 4), kThreads, 0, st>>>(x, N, C, H, W, Cpad, out);
@@ -862,8 +998,9 @@ cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __n
 }
 
 cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st) {
-  const long total = (long)g.N * g.P * g.Q * Kpad;
-  im2col_kernel<<<grid_for(total, kThreads * 4), kThreads, 0, st>>>(x, g, Kpad, out);
+  if (Kpad % 8) return cudaErrorInvalidValue;
+  const long total = (long)g.N * g.P * g.Q * (Kpad / 8);
+  im2col_kernel<<<grid_for(total, kThreads * 2, 148 * 32), kThreads, 0, st>>>(x, g, Kpad, out);
   return cudaGetLastError();
 }
 

@@ -30,8 +30,9 @@ cudaError_t relu_fwd(const __nv_bfloat16* x, long n, __nv_bfloat16* y, cudaStrea
 cudaError_t relu_bwd(const __nv_bfloat16* y, const __nv_bfloat16* dy, long n, __nv_bfloat16* dx, bool acc,
                      cudaStream_t st);
 cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st);
+// idx_ws: N*P*Q*C bytes of scratch (window argmax)
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __nv_bfloat16* dy, const PoolGeom& g,
-                        __nv_bfloat16* dx, bool acc, cudaStream_t st);
+                        __nv_bfloat16* dx, bool acc, void* idx_ws, cudaStream_t st);
 cudaError_t avgpool_fwd(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, cudaStream_t st);
 cudaError_t avgpool_bwd(const __nv_bfloat16* dout, int N, int HW, int C, __nv_bfloat16* dx, bool acc,
                         cudaStream_t st);
@@ -48,6 +49,19 @@ cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, flo
                        cudaStream_t st);
 cudaError_t conv_weight_prep(const float* w, int Cout, int R, int S, int Cpad, int Cin, int CoutPad,
                              __nv_bfloat16* wb, __nv_bfloat16* wt, cudaStream_t st);
+// One launch for every conv / fc layer after an SGD step: bf16 copy of the
+// GEMM-layout weights plus (convs) the flipped transpose used by dgrad.  The
+// table lives in device memory; `starts` are element offsets of each layer
+// in the virtual concatenation [copy elems | transpose elems].
+struct WeightPrepLayer {
+  const float* w;
+  __nv_bfloat16* wb;
+  __nv_bfloat16* wt;  // nullptr: no transpose
+  int cout, R, S, cpad, cin, coutpad;
+  long n_copy, n_t;   // elements of wb and of wt
+  long start;         // first virtual element of this layer
+};
+cudaError_t weight_prep_batched(const WeightPrepLayer* table_dev, int layers, long total, cudaStream_t st);
 cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __nv_bfloat16* out, cudaStream_t st);
 cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st);
 cudaError_t zero_insert(const __nv_bfloat16* dy, int N, int P, int Q, int C, int Hu, int Wu, int stride,

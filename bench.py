@@ -245,14 +245,17 @@ def main():
     x, y = random_batch(net, seed=rank)
     net.load_batch(x.cuda(), y.cuda(), stream=stream)
     allreduce = None
+    buckets = 0
+    uid = None
     if world > 1:
-        ptr, n = net.grad_buffer()
-        grads = torch.as_tensor(GradView(ptr, n), device="cuda")
-
-        def allreduce():
-            with torch.cuda.stream(stream):
-                dist.all_reduce(grads)
-                grads.div_(world)
+        # gradient averaging runs inside the step: NCCL all-reduce per bucket on
+        # a side stream as the backward finishes each range (torch.distributed
+        # only carries the NCCL unique id)
+        from paper_1808_00079_b200.executor import ReforwardNet
+        obj = [ReforwardNet.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+        buckets = net.set_comm(world, rank, uid)
 
     with ClockSampler(local) as clk:
         ms = time_steps(net, args.steps, args.warmup, stream, world, allreduce)
@@ -284,7 +287,9 @@ def main():
         torch.cuda.synchronize()
         net_sa, rep_sa, _ = build_net(args.batch, "store_all", seed=1234 + rank)
         net_sa.load_batch(x.cuda(), y.cuda(), stream=stream)
-        ms_sa = time_steps(net_sa, args.steps, args.warmup, stream, world, None if world == 1 else allreduce)
+        if world > 1:
+            net_sa.set_comm(world, rank, uid)
+        ms_sa = time_steps(net_sa, args.steps, args.warmup, stream, world)
         sa_value = args.batch * world / (ms_sa / 1000.0)
         overhead = ms / ms_sa
         del net_sa
@@ -324,6 +329,7 @@ def main():
                          "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)"},
             "cpu_baseline": cpu,
             "gpu_launches": launches * args.steps,
+            "allreduce_buckets": buckets,
             "clocks": clk.summary(),
         }
         print(json.dumps(line))

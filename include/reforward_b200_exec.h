@@ -144,6 +144,18 @@ int rfx_net_read_grad_tensor(const rfx_net* net, int32_t t, float* host);
 /* flat fp32 gradient buffer (data-parallel all-reduce target) */
 int rfx_net_grad_buffer(const rfx_net* net, void** dev_ptr, int64_t* count);
 
+/* data parallel over NCCL: rank 0 creates the 128-byte unique id, every rank
+ * passes it to rfx_net_set_comm (after setup); the step then averages the
+ * gradient buffer bucket by bucket on a side stream as the backward finishes
+ * each range (overlapped, captured in the step graph) */
+int rfx_comm_unique_id(char* id128);
+int rfx_net_set_comm(rfx_net* net, int32_t nranks, int32_t rank, const char* id128, int64_t bucket_bytes);
+int32_t rfx_net_comm_buckets(const rfx_net* net);
+/* dry run of the bucket plan (no GPU needed): per bucket, the schedule
+ * instruction after which it is reduced and its float range [lo, hi) */
+int rfx_net_bucket_plan(rfx_net* net, int64_t bucket_bytes, int32_t* after_instr, int64_t* lo, int64_t* hi,
+                        int32_t cap, int32_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -290,6 +290,37 @@ int rfx_net_read_bn_running(const rfx_net* n, int32_t op, float* mean, float* va
   return guard([&] { n->net->read_bn_running(op, mean, var); });
 }
 
+int rfx_comm_unique_id(char* id128) {
+  return guard([&] {
+    std::string err;
+    if (!rfx::NcclComm::get_unique_id(id128, &err)) throw std::runtime_error(err);
+  });
+}
+
+int rfx_net_set_comm(rfx_net* n, int32_t nranks, int32_t rank, const char* id128, int64_t bucket_bytes) {
+  return guard([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank / world size");
+    n->net->set_comm(nranks, rank, id128, bucket_bytes > 0 ? bucket_bytes : (25L << 20));
+  });
+}
+
+int32_t rfx_net_comm_buckets(const rfx_net* n) { return n->net->comm_buckets(); }
+
+int rfx_net_bucket_plan(rfx_net* n, int64_t bucket_bytes, int32_t* after, int64_t* lo, int64_t* hi, int32_t cap,
+                        int32_t* n_out) {
+  return guard([&] {
+    auto b = n->net->bucket_plan(bucket_bytes);
+    *n_out = (int32_t)b.size();
+    if (!after) return;
+    if (cap < (int32_t)b.size()) throw std::invalid_argument("bucket buffer too small");
+    for (size_t i = 0; i < b.size(); ++i) {
+      after[i] = (int32_t)b[i][0];
+      lo[i] = b[i][1];
+      hi[i] = b[i][2];
+    }
+  });
+}
+
 int rfx_net_grad_buffer(const rfx_net* n, void** p, int64_t* count) {
   return guard([&] {
     *p = n->net->grad_buffer();

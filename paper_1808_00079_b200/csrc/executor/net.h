@@ -15,12 +15,14 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
 #include <functional>
 #include <memory>
 #include <string>
 #include <vector>
 
+#include "executor/comm.h"
 #include "kernels/kernels.h"
 #include "kernels/ops.h"
 
@@ -167,6 +169,15 @@ class Net {
   float* grad_buffer() const { return d_grad_; }
   long grad_count() const { return n_params_; }
 
+  // Data parallel: average the flat gradient buffer across ranks with NCCL,
+  // bucket by bucket as the backward finalises parameter gradients (on a
+  // side stream, overlapped with the remaining backward; captured into the
+  // step's CUDA graph like everything else).
+  void set_comm(int nranks, int rank, const char id[128], long bucket_bytes);
+  int comm_buckets() const { return (int)buckets_.size(); }
+  // dry run of the bucket plan: (after instruction, lo, hi) per bucket
+  std::vector<std::array<long, 3>> bucket_plan(long bucket_bytes);
+
   const MemoryReport& report() const { return rep_; }
   const Plan& current_plan() const { return plan_; }
   const std::vector<Tensor>& tensors() const { return tensors_; }
@@ -235,6 +246,17 @@ class Net {
   cudaGraphExec_t graph_exec_ = nullptr;
   float graph_lr_ = 0, graph_mom_ = 0, graph_wd_ = 0;
   cudaGraphExec_t phase_exec_[3] = {nullptr, nullptr, nullptr};
+  std::unique_ptr<NcclComm> comm_;
+  cudaStream_t comm_stream_ = nullptr;
+  struct Bucket {
+    int after_instr;  // launch once this schedule instruction has been enqueued
+    long lo, hi;      // float range of the gradient buffer
+  };
+  std::vector<Bucket> buckets_;
+  std::vector<cudaEvent_t> bucket_events_;
+  cudaEvent_t comm_done_ = nullptr;
+  long bucket_floats_ = 0;
+  void plan_buckets();
   void* d_prep_table_ = nullptr;
   int prep_layers_ = 0;
   long prep_total_ = 0;

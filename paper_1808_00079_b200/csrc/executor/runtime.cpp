@@ -6,6 +6,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "executor/comm.h"
 #include "executor/net.h"
 
 namespace rfx {
@@ -23,7 +24,13 @@ float bf16_to_float(uint16_t b) {
 
 std::unique_ptr<Net> make_net(int batch) { return std::make_unique<Net>(batch); }
 
-Net::~Net() { free_device(); }
+Net::~Net() {
+  free_device();
+  comm_.reset();
+  for (auto e : bucket_events_) cudaEventDestroy(e);
+  if (comm_done_) cudaEventDestroy(comm_done_);
+  if (comm_stream_) cudaStreamDestroy(comm_stream_);
+}
 
 void Net::check(cudaError_t e, const char* what) const {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -613,9 +620,94 @@ void Net::load_batch(const float* images, const int* labels, bool from_host, cud
   check(rfk::pack_input(src, batch_, in_c_real_, in.H, in.W, in.C, d_input_, st), "pack_input");
 }
 
+void Net::set_comm(int nranks, int rank, const char id[128], long bucket_bytes) {
+  if (!setup_done_) throw std::invalid_argument("setup the network before set_comm");
+  auto c = std::make_unique<NcclComm>();
+  std::string err;
+  if (!c->init(nranks, rank, id, &err)) throw std::runtime_error(err);
+  comm_ = std::move(c);
+  if (!comm_stream_) check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
+  if (!comm_done_) check(cudaEventCreateWithFlags(&comm_done_, cudaEventDisableTiming), "event");
+  bucket_floats_ = std::max(1L, bucket_bytes / 4);
+  plan_buckets();
+  for (auto& p : phase_exec_)
+    if (p) {
+      cudaGraphExecDestroy(p);
+      p = nullptr;
+    }
+}
+
+// Which gradient ranges become final after which backward instruction.
+// Parameters sit in the flat buffer in op order, and the backward finishes
+// them roughly in reverse; a bucket is the longest finished suffix not yet
+// reduced, emitted once it holds bucket_floats_ or the backward is over.
+void Net::plan_buckets() {
+  buckets_.clear();
+  const int np = (int)params_.size();
+  std::vector<char> done(np, 0);
+  std::vector<std::vector<int>> of_op(ops_.size());
+  for (int i = 0; i < np; ++i) of_op[params_[i].op].push_back(i);
+  int frontier = np, reduced = np;  // params [frontier, np) finished; [reduced, np) already in a bucket
+  int last_bwd = -1;
+  for (int k = 0; k < (int)sched_.size(); ++k)
+    if (sched_[k].kind == InstrKind::Backward) last_bwd = k;
+  auto off = [&](int i) { return i >= np ? n_params_ : params_[i].offset; };
+  for (int k = 0; k < (int)sched_.size(); ++k) {
+    if (sched_[k].kind != InstrKind::Backward) continue;
+    for (int i : of_op[sched_[k].op]) done[i] = 1;
+    while (frontier > 0 && done[frontier - 1]) --frontier;
+    const bool last = k == last_bwd;
+    if (frontier < reduced && (off(reduced) - off(frontier) >= bucket_floats_ || last)) {
+      buckets_.push_back({k, off(frontier), off(reduced)});
+      reduced = frontier;
+    }
+  }
+  if (!comm_) return;  // dry run (bucket_plan): no device events needed
+  for (auto e : bucket_events_) cudaEventDestroy(e);
+  bucket_events_.assign(buckets_.size(), nullptr);
+  for (auto& e : bucket_events_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+}
+
+std::vector<std::array<long, 3>> Net::bucket_plan(long bucket_bytes) {
+  if (!planned_) throw std::invalid_argument("plan the network first");
+  const long saved = bucket_floats_;
+  auto saved_b = buckets_;
+  bucket_floats_ = std::max(1L, bucket_bytes / 4);
+  if (!comm_) plan_buckets();
+  else {
+    auto keep = std::move(comm_);
+    plan_buckets();
+    comm_ = std::move(keep);
+  }
+  std::vector<std::array<long, 3>> out;
+  for (const auto& b : buckets_) out.push_back({(long)b.after_instr, b.lo, b.hi});
+  bucket_floats_ = saved;
+  buckets_ = std::move(saved_b);
+  return out;
+}
+
 void Net::forward_backward(cudaStream_t st) {
   if (!setup_done_) throw std::invalid_argument("setup the network first");
-  for (const auto& ins : sched_) run_instr(ins, st);
+  const bool dp = comm_ && comm_->ready() && comm_->nranks() > 0;
+  size_t b = 0;
+  for (int k = 0; k < (int)sched_.size(); ++k) {
+    run_instr(sched_[k], st);
+    while (dp && b < buckets_.size() && buckets_[b].after_instr == k) {
+      // fork: the side stream waits for the gradients, then reduces them
+      // while this stream carries on with the backward
+      check(cudaEventRecord(bucket_events_[b], st), "event");
+      check(cudaStreamWaitEvent(comm_stream_, bucket_events_[b], 0), "wait");
+      std::string err;
+      if (!comm_->allreduce_avg(d_grad_ + buckets_[b].lo, (size_t)(buckets_[b].hi - buckets_[b].lo), comm_stream_,
+                                &err))
+        throw std::runtime_error(err);
+      ++b;
+    }
+  }
+  if (dp) {  // join
+    check(cudaEventRecord(comm_done_, comm_stream_), "event");
+    check(cudaStreamWaitEvent(st, comm_done_, 0), "wait");
+  }
 }
 
 void Net::update(float lr, float momentum, float wd, cudaStream_t st) {

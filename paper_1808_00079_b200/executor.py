@@ -83,6 +83,11 @@ _SIGS = {
     "rfx_net_read_bn_running": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "rfx_net_grad_buffer": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "rfx_net_set_keep_grads": (C.c_int, [C.c_void_p, C.c_int32]),
+    "rfx_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "rfx_net_set_comm": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_int64]),
+    "rfx_net_comm_buckets": (C.c_int32, [C.c_void_p]),
+    "rfx_net_bucket_plan": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32)]),
     "rfx_net_read_grad_tensor": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "rf_last_error": (C.c_char_p, []),
 }
@@ -373,6 +378,45 @@ class ReforwardNet:
         m, v = np.empty(c, np.float32), np.empty(c, np.float32)
         _check(self.L.rfx_net_read_bn_running(self.h, op, m.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p)))
         return m, v
+
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """NCCL unique id (rank 0); broadcast it with torch.distributed."""
+        buf = C.create_string_buffer(128)
+        _check(_lib().rfx_comm_unique_id(buf))
+        return buf.raw
+
+    def set_comm(self, world: int, rank: int, uid: bytes, bucket_bytes: int = 25 << 20) -> int:
+        """Average gradients across `world` ranks inside every step (NCCL,
+        bucketed, overlapped with the backward).  Returns the bucket count."""
+        assert len(uid) == 128
+        _check(self.L.rfx_net_set_comm(self.h, world, rank, uid, bucket_bytes))
+        return self.L.rfx_net_comm_buckets(self.h)
+
+    def bucket_plan(self, bucket_bytes: int = 25 << 20) -> List[Tuple[int, int, int]]:
+        """(after schedule instruction, lo, hi) float ranges of the all-reduce buckets."""
+        n = C.c_int32()
+        _check(self.L.rfx_net_bucket_plan(self.h, bucket_bytes, None, None, None, 0, C.byref(n)))
+        a, lo, hi = (C.c_int32 * max(n.value, 1))(), (C.c_int64 * max(n.value, 1))(), (C.c_int64 * max(n.value, 1))()
+        _check(self.L.rfx_net_bucket_plan(self.h, bucket_bytes, a, lo, hi, n.value, C.byref(n)))
+        return [(a[i], lo[i], hi[i]) for i in range(n.value)]
+
+    def param_offsets(self) -> List[Tuple[int, int]]:
+        """(offset, count) of every parameter in the flat gradient buffer (dry, from the layout rules)."""
+        out, off = [], 0
+        for p in self.params():
+            n = self._param_alloc_count(p)
+            out.append((off, n))
+            off += (n + 63) // 64 * 64
+        return out
+
+    def _param_alloc_count(self, p) -> int:
+        if p.kind != 0:
+            return p.count
+        co, ci, r, s = p.shape
+        if ci < 32:  # explicit-im2col layer: [Cout][Kpad]
+            return co * ((r * s * ci + 63) // 64 * 64)
+        return co * r * s * ((ci + 63) // 64 * 64)
 
     def grad_buffer(self) -> Tuple[int, int]:
         p, n = C.c_void_p(), C.c_int64()

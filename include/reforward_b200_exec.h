@@ -38,7 +38,10 @@ typedef struct rfx_gemm_args {
   int64_t split_stride;
   int32_t remap, rP, rQ, rH, rW, rsh, rsw;
   int32_t block_n;
+  int64_t b_extent;                  /* valid MN extent of an MN-major B (0 = N) */
+  int32_t b_taps, b_cpad, b_rows;    /* kind 4 (conv weights as dgrad B): R*S, Cpad, Cout */
 } rfx_gemm_args;
+/* kind 4 = conv weights [Cout][R][S][Cpad] read as the dgrad B operand (flipped taps) */
 
 int rfx_gemm(const rfx_gemm_args* args, void* stream);
 

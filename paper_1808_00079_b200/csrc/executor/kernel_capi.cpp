@@ -28,6 +28,10 @@ extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
   d.bias = a->bias; d.stats = a->stats; d.splits = a->splits; d.split_stride = a->split_stride;
   d.remap = a->remap != 0; d.rP = a->rP; d.rQ = a->rQ; d.rH = a->rH; d.rW = a->rW; d.rsh = a->rsh; d.rsw = a->rsw;
   d.block_n = a->block_n;
+  d.b_extent = a->b_extent;
+  d.b_taps = a->b_taps > 0 ? a->b_taps : 1;
+  d.b_cpad = a->b_cpad;
+  d.b_rows = a->b_rows;
   cudaError_t e = rfk::gemm_launch(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     rfexec::set_last_error(std::string("rfx_gemm: ") + cudaGetErrorString(e));

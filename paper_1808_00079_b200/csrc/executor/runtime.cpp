@@ -69,11 +69,7 @@ void Net::setup(uint64_t seed) {
       p.bf16_off = n_bf16_;
       p.bf16_count = p.count;
       n_bf16_ += (p.count + 63) / 64 * 64;
-      if (!op.explicit_im2col) {
-        p.wt_off = n_bf16_;
-        p.wt_count = (long)op.cin * op.R * op.S * op.coutpad;
-        n_bf16_ += (p.wt_count + 63) / 64 * 64;
-      }
+      (void)op;  // dgrad reads the same copy through a transposing TMA map
     } else if (p.kind == 3) {
       p.bf16_off = n_bf16_;
       p.bf16_count = p.count;
@@ -389,7 +385,8 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         rfk::GemmDesc d;
         d.N = op.cin;
         d.b_kind = rfk::Operand::KMajor2D;
-        d.b = d_bf16_ + w.wt_off;
+        d.b = d_bf16_ + w.bf16_off;  // the forward bf16 weights, read transposed by TMA
+        d.b_extent = op.cin;
         d.out = dx;
         d.ldc = op.cin;
         d.accumulate_out = acc(0);
@@ -399,7 +396,8 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           d.a_kind = rfk::Operand::KMajor2D;
           d.a = dy;
           d.a_ld = op.cout;
-          d.b_ld = op.coutpad;
+          d.b_kind = rfk::Operand::MNMajor2D;  // W[co][ci]: K = co rows, N = ci contiguous
+          d.b_ld = op.cpad;
           if (op.stride > 1) {
             if (!acc(0)) check(cudaMemsetAsync(dx, 0, x.bytes(), st), "memset");
             d.accumulate_out = acc(0);
@@ -413,7 +411,10 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         } else {
           d.M = (int)x.rows();
           d.K = op.R * op.S * op.coutpad;
-          d.b_ld = (long)op.R * op.S * op.coutpad;
+          d.b_kind = rfk::Operand::WeightTapsMN;  // W[co][tap][ci] with the tap flipped
+          d.b_taps = op.R * op.S;
+          d.b_cpad = op.cpad;
+          d.b_rows = op.cout;
           d.a_kind = rfk::Operand::Im2colK;
           const int pd = op.R - 1 - op.pad;
           if (op.stride == 1) {
@@ -580,16 +581,7 @@ void Net::prep_weights(cudaStream_t st) {
       L.w = d_param_ + p.offset;
       L.wb = d_bf16_ + p.bf16_off;
       L.n_copy = p.count;
-      if (p.kind == 0 && !op.explicit_im2col) {
-        L.wt = d_bf16_ + p.wt_off;
-        L.cout = op.cout;
-        L.R = op.R;
-        L.S = op.S;
-        L.cpad = op.cpad;
-        L.cin = op.cin;
-        L.coutpad = op.coutpad;
-        L.n_t = p.wt_count;
-      }
+      (void)op;
       L.start = start;
       start += L.n_copy + L.n_t;
       tab.push_back(L);

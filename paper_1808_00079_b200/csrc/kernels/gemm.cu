@@ -46,6 +46,7 @@ struct alignas(64) KParams {
   float* stats;
   long split_stride;
   int remap, rP, rQ, rH, rW, rsh, rsw;
+  int b_taps;  // WeightTapsMN: filter taps R*S
   int stages;  // smem ring depth (<= Cfg::kStages)
   int m_tiles, n_tiles, splits;  // persistent tile space
 };
@@ -161,6 +162,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               for (int j = 0; j < BN / 64; ++j)
                 tma_load_2d(sb + j * 8192, &p.tb, &full[stage], tc.n0 + 64 * j, kb * kBlockK);
               break;
+            case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
+              const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
+              const int ftap = p.b_taps - 1 - tap;
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_3d(sb + j * 8192, &p.tb, &full[stage], tc.n0 + 64 * j, ftap, cb * 64);
+              break;
+            }
             default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
               int bw, bh, bn;
               pixel_base(p, kb * kBlockK, bw, bh, bn);
@@ -183,7 +192,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     const bool a_mn = p.a_kind == (int)Operand::MNMajor2D;
-    const bool b_mn = p.b_kind == (int)Operand::MNMajor2D || p.b_kind == (int)Operand::Im2colMN;
+    const bool b_mn = p.b_kind == (int)Operand::MNMajor2D || p.b_kind == (int)Operand::Im2colMN ||
+                      p.b_kind == (int)Operand::WeightTapsMN;
     const uint32_t idesc = umma_idesc_bf16(kBlockM, BN, a_mn, b_mn);
     int stage = 0;
     uint32_t phase = 0;
@@ -484,7 +494,8 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
       }
     }
   }
-  if (d.b_kind == Operand::MNMajor2D || d.b_kind == Operand::Im2colMN) bn = bn < 64 ? 64 : bn;
+  if (d.b_kind == Operand::MNMajor2D || d.b_kind == Operand::Im2colMN || d.b_kind == Operand::WeightTapsMN)
+    bn = bn < 64 ? 64 : bn;
   if (bn != 64 && bn != 128 && bn != 256) return cudaErrorInvalidValue;
 
   KParams kp;
@@ -526,6 +537,21 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
       geo = &d.b_geom;
       ok = encode_im2col(&kp.tb, d.b, d.b_geom, 64);
       break;
+    case Operand::WeightTapsMN: {
+      // [Cout][taps][Cpad] viewed as {ci (valid extent), tap, co}; a box is a
+      // 64 (ci) x 64 (co) tile of one tap: MN-major with K = co rows
+      cuuint64_t dims[3] = {(cuuint64_t)(d.b_extent > 0 ? d.b_extent : d.N), (cuuint64_t)d.b_taps,
+                            (cuuint64_t)d.b_rows};
+      cuuint64_t strides[2] = {(cuuint64_t)d.b_cpad * 2, (cuuint64_t)d.b_taps * d.b_cpad * 2};
+      cuuint32_t box[3] = {64, 1, 64};
+      cuuint32_t es[3] = {1, 1, 1};
+      ok = g_encode_tiled(&kp.tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(d.b), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      kp.b_taps = d.b_taps;
+      if (d.a_kind != Operand::Im2colK) return cudaErrorInvalidValue;  // 1x1 dgrad uses MNMajor2D
+      break;
+    }
     default:
       return cudaErrorInvalidValue;
   }

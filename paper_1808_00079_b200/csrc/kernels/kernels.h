@@ -17,6 +17,9 @@ enum class Operand : int {
   MNMajor2D = 1,  // K rows x MN, MN contiguous (row stride `ld` elements)
   Im2colK = 2,    // NHWC activation, rows = output pixels, K = (r, s, c)
   Im2colMN = 3,   // NHWC activation, K = output pixels, MN = (r, s, c)
+  // conv weights [Cout][R][S][Cpad] read as the dgrad B operand: MN = input
+  // channel (contiguous), K = (flipped tap, Cout) — no transposed copy needed
+  WeightTapsMN = 4,
 };
 
 // Convolution geometry for an im2col operand: input tensor N x H x W x C,
@@ -39,6 +42,7 @@ struct GemmDesc {
   long b_ld = 0;
   ConvGeom b_geom;
   long b_extent = 0;  // valid MN extent of an MN-major B (0 = N)
+  int b_taps = 1, b_cpad = 0, b_rows = 0;  // WeightTapsMN: R*S, Cpad, Cout
   // epilogue
   void* out = nullptr;
   long ldc = 0;

@@ -137,3 +137,34 @@ def test_scatter_remap():
     K.gemm(args)
     torch.cuda.synchronize()
     _check(out, ref)
+
+
+DGRAD_CASES = [(2, 8, 8, 64, 128, 3, 1), (2, 10, 10, 96, 64, 3, 1), (1, 7, 7, 512, 512, 3, 1),
+               (2, 15, 15, 64, 64, 5, 2)]
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,R,pad", DGRAD_CASES)
+def test_conv_dgrad_weight_taps(N, H, W, Ci, Co, R, pad):
+    # stride-1 dgrad: im2col over dY (pad' = R-1-pad) x flipped weights read
+    # in place through a 3-D transposing TMA map
+    g = K.conv_geom(N, H, W, Ci, R, R, pad, 1)
+    dy = _bf(N, Co, g.P, g.Q, seed=11)
+    w = _bf(Co, Ci, R, R, scale=0.1, seed=12)
+    ref = torch.nn.grad.conv2d_input((N, Ci, H, W), w.float(), dy.float(), stride=1, padding=pad)
+    ref = ref.permute(0, 2, 3, 1).contiguous()
+    cpad = (Ci + 63) // 64 * 64
+    wp = _pad_w(w, cpad)  # [Co][R][S][Cpad]
+    dyn = dy.permute(0, 2, 3, 1).contiguous()
+    pd = R - 1 - pad
+    ga = K.ConvGeom(N, g.P, g.Q, Co, H, W, R, R, pd, pd, 1, 1)
+    copad = (Co + 63) // 64 * 64
+    out = torch.zeros(N, H, W, Ci, device=dev, dtype=torch.bfloat16)
+    args = K.GemmArgs(M=N * H * W, N=Ci, K=R * R * copad, a_kind=K.IM2COL_K, a=dyn.data_ptr(), a_geom=ga,
+                      b_kind=4, b=wp.data_ptr(), out=out.data_ptr(), ldc=Ci, splits=1)
+    args.b_extent = Ci
+    args.b_taps = R * R
+    args.b_cpad = cpad
+    args.b_rows = Co
+    K.gemm(args)
+    torch.cuda.synchronize()
+    _check(out, ref)

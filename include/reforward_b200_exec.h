@@ -132,6 +132,9 @@ int rfx_net_read_loss(rfx_net* net, float* loss, void* stream);
  * algorithmic flops per step, number of GEMM launches */
 int rfx_net_gemm_profile(rfx_net* net, int32_t iters, void* stream, double* ms_per_step,
                          double* flops_per_step, int64_t* launches);
+/* per GEMM launch of the step: 8 doubles {M, N, K, a_kind, b_kind, splits, ms, flops} */
+int rfx_net_gemm_profile_detail(rfx_net* net, int32_t iters, void* stream, double* rows, int32_t cap,
+                                int32_t* n_out);
 
 int32_t rfx_net_num_params(const rfx_net* net);
 int rfx_net_param_info(const rfx_net* net, int32_t i, char* name, size_t name_cap, int32_t* shape,

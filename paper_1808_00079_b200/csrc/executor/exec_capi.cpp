@@ -239,6 +239,17 @@ int rfx_net_run_phase(rfx_net* n, int32_t phase, float lr, float momentum, float
   });
 }
 
+int rfx_net_gemm_profile_detail(rfx_net* n, int32_t iters, void* st, double* rows, int32_t cap, int32_t* n_out) {
+  return guard([&] {
+    auto r = n->net->gemm_profile_detail(iters < 1 ? 1 : iters, S(st));
+    *n_out = (int32_t)r.size();
+    if (!rows) return;
+    if (cap < (int32_t)r.size()) throw std::invalid_argument("buffer too small");
+    for (size_t i = 0; i < r.size(); ++i)
+      for (int j = 0; j < 8; ++j) rows[i * 8 + j] = r[i][j];
+  });
+}
+
 int rfx_net_gemm_profile(rfx_net* n, int32_t iters, void* st, double* ms, double* flops, int64_t* launches) {
   return guard([&] {
     long l = 0;

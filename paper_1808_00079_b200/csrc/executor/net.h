@@ -155,6 +155,9 @@ class Net {
   // time it with events.  flops = algorithmic 2*M*N*K of the real (unpadded)
   // problem summed over those launches.
   void gemm_profile(int iters, cudaStream_t st, double* ms_per_step, double* flops_per_step, long* launches);
+  // per-launch timing of the step's GEMMs (events between eager launches):
+  // rows of {M, N, K, a_kind, b_kind, splits, ms, flops}
+  std::vector<std::array<double, 8>> gemm_profile_detail(int iters, cudaStream_t st);
 
   // parameter access in canonical layout (host fp32)
   int num_params() const { return (int)params_.size(); }
@@ -221,7 +224,8 @@ class Net {
   std::vector<char> grad_acc_;    // per (op, input) accumulate flags, flattened
   std::vector<int> grad_acc_base_;
   long arena_bytes_ = 0, grad_bytes_ = 0;
-  long ws_im2col_ = 0, ws_partials_ = 0, ws_zero_ = 0, ws_split_ = 0, ws_stats_ = 0, ws_misc_ = 0;
+  long ws_im2col_ = 0, ws_partials_ = 0, ws_zero_ = 0, ws_split_ = 0, ws_stats_ = 0, ws_misc_ = 0,
+       ws_counters_ = 0;
   MemoryReport rep_;
   long launches_ = 0;
   bool counting_ = false;

@@ -99,6 +99,7 @@ void Net::setup(uint64_t seed) {
   check(cudaMemset(d_mom_, 0, n_params_ * 4), "memset");
   check(cudaMemset(d_bf16_, 0, n_bf16_ * 2), "memset");
   check(cudaMemset(d_arena_, 0, arena_bytes_ > 0 ? arena_bytes_ : 256), "memset");
+  check(cudaMemset(d_ws_, 0, rep_.workspace_bytes > 0 ? rep_.workspace_bytes : 256), "memset");
   check(cudaMemset(d_labels_, 0, batch_ * 4), "memset");
   check(cudaMemset(d_input_, 0, in.bytes()), "memset");
 
@@ -459,11 +460,15 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         d.b_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad, op.stride, op.stride};
       }
       if (op.wg_splits > 1) {
+        // split-K partials in the workspace, summed in split order by the
+        // last CTA of each tile straight into the gradient buffer
         d.splits = op.wg_splits;
         d.out = ws_split;
         d.split_stride = (long)op.cout * kw;
+        d.final_out = dW;
+        d.counters = reinterpret_cast<int*>(ws + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ +
+                                            ws_misc_);
         gemm(d, st);
-        check(rfk::reduce_splits(ws_split, op.wg_splits, (long)op.cout * kw, dW, false, st), "reduce_splits");
       } else {
         d.out = dW;
         gemm(d, st);
@@ -765,6 +770,37 @@ void Net::run_phase(int phase, float lr, float momentum, float wd, cudaStream_t 
 
 void Net::step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph) {
   run_phase(2, lr, momentum, wd, st, use_graph);
+}
+
+std::vector<std::array<double, 8>> Net::gemm_profile_detail(int iters, cudaStream_t st) {
+  double a, b;
+  long c;
+  if (gemm_trace_.empty()) gemm_profile(1, st, &a, &b, &c);
+  std::vector<cudaEvent_t> ev(gemm_trace_.size() + 1);
+  for (auto& e : ev) check(cudaEventCreate(&e), "event");
+  std::vector<double> ms(gemm_trace_.size(), 0.0);
+  for (int it = 0; it < iters + 1; ++it) {
+    check(cudaEventRecord(ev[0], st), "event");
+    for (size_t i = 0; i < gemm_trace_.size(); ++i) {
+      check(rfk::gemm_launch(gemm_trace_[i].desc, st), "gemm");
+      check(cudaEventRecord(ev[i + 1], st), "event");
+    }
+    check(cudaEventSynchronize(ev.back()), "sync");
+    if (it == 0) continue;  // warm-up
+    for (size_t i = 0; i < gemm_trace_.size(); ++i) {
+      float t = 0;
+      cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+      ms[i] += t / iters;
+    }
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  std::vector<std::array<double, 8>> out;
+  for (size_t i = 0; i < gemm_trace_.size(); ++i) {
+    const auto& d = gemm_trace_[i].desc;
+    out.push_back({(double)d.M, (double)d.N, (double)d.K, (double)(int)d.a_kind, (double)(int)d.b_kind,
+                   (double)d.splits, ms[i], gemm_trace_[i].flops});
+  }
+  return out;
 }
 
 void Net::gemm_profile(int iters, cudaStream_t st, double* ms_per_step, double* flops_per_step, long* launches) {

@@ -653,7 +653,14 @@ void Net::layout() {
       op.stats_off = ws_stats_ / 4;
       ws_stats_ += align_up(mt * 2 * op.cout * 4);
     }
-  rep_.workspace_bytes = ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_;
+  // split-K tile counters (zeroed once at setup; kernels leave them zero)
+  ws_counters_ = 0;
+  for (const auto& op : ops_)
+    if (op.kind == OpKind::Conv) {
+      const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
+      ws_counters_ = std::max(ws_counters_, align_up(((op.cout + 127) / 128) * ((kw + op.wg_bn - 1) / op.wg_bn) * 4L));
+    }
+  rep_.workspace_bytes = ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_ + ws_counters_;
   rep_.param_bytes = n_params_ * 4 * 3;
   rep_.state_bytes = n_state_ * 4;
 }

@@ -47,6 +47,8 @@ struct alignas(64) KParams {
   long split_stride;
   int remap, rP, rQ, rH, rW, rsh, rsw;
   int b_taps;  // WeightTapsMN: filter taps R*S
+  float* final_out;  // split-K finished in-kernel into this fp32 matrix (null: keep partials)
+  int* counters;     // per output tile, zero between launches
   int stages;  // smem ring depth (<= Cfg::kStages)
   int m_tiles, n_tiles, splits;  // persistent tile space
 };
@@ -379,6 +381,41 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
         __syncwarp();
       }
+      if (p.final_out) {
+        // Split-K finish without a second kernel: every CTA publishes its
+        // fp32 partial and bumps the tile's counter; the CTA that completes
+        // the count sums all partials in split order 0..S-1 (so the result
+        // does not depend on which CTA came last) and resets the counter.
+        __shared__ int s_last;
+        const int tile_id = tc.m0 / kBlockM + p.m_tiles * (tc.n0 / BN);
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (quarter == 0 && lane == 0) s_last = atomicAdd(p.counters + tile_id, 1) == p.splits - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_last) {
+          __threadfence();
+          const float* part = reinterpret_cast<const float*>(p.out);
+          for (int i = 0; i < 32; ++i) {
+            const int row = tc.m0 + (int)quarter * 32 + i;
+            if (row >= p.M) break;
+            for (int c = (int)lane * 4; c < BN; c += 128) {
+              const int col = tc.n0 + c;
+              if (col >= p.N) break;
+              const long off = (long)row * p.ldc + col;
+              float4 a = __ldcg(reinterpret_cast<const float4*>(part + off));
+              for (int z = 1; z < p.splits; ++z) {
+                const float4 b = __ldcg(reinterpret_cast<const float4*>(part + (long)z * p.split_stride + off));
+                a.x += b.x;
+                a.y += b.y;
+                a.z += b.z;
+                a.w += b.w;
+              }
+              *reinterpret_cast<float4*>(p.final_out + off) = a;
+            }
+          }
+          if (quarter == 0 && lane == 0) p.counters[tile_id] = 0;
+        }
+      }
     }
   }
   tc_fence_before();
@@ -575,6 +612,12 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   kp.bias = d.bias;
   kp.stats = d.stats;
   kp.split_stride = d.split_stride;
+  if (d.final_out) {
+    if (!d.out_f32 || d.accumulate_out || !d.counters || d.remap || d.ldc % 4) return cudaErrorInvalidValue;
+    kp.final_out = d.splits > 1 ? d.final_out : nullptr;
+    kp.counters = d.counters;
+    if (d.splits <= 1) kp.out = d.final_out;  // nothing to reduce: write the result directly
+  }
   kp.remap = d.remap;
   kp.rP = d.rP;
   kp.rQ = d.rQ;

@@ -52,6 +52,10 @@ struct GemmDesc {
   float* stats = nullptr;       // [m_tiles][2][N] column sum / sum of squares
   int splits = 1;               // split-K; split z writes out + z * split_stride
   long split_stride = 0;
+  // fp32 split-K only: the last CTA of each output tile sums the partials (in
+  // split order) into final_out; counters = m_tiles * n_tiles zeroed ints
+  float* final_out = nullptr;
+  int* counters = nullptr;
   // row remap of the output (strided-conv dgrad scatter): row m = (n, p, q)
   // over P x Q goes to n * H * W + (p * sh) * W + q * sw.
   bool remap = false;

@@ -70,6 +70,8 @@ _SIGS = {
     "rfx_net_update": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_void_p]),
     "rfx_net_step": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_int32, C.c_void_p]),
     "rfx_net_read_loss": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_void_p]),
+    "rfx_net_gemm_profile_detail": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int32,
+                                              C.POINTER(C.c_int32)]),
     "rfx_net_run_phase": (C.c_int, [C.c_void_p, C.c_int32, C.c_float, C.c_float, C.c_float, C.c_int32,
                                     C.c_void_p]),
     "rfx_net_gemm_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double),
@@ -323,6 +325,15 @@ class ReforwardNet:
         ms, fl, n = C.c_double(), C.c_double(), C.c_int64()
         _check(self.L.rfx_net_gemm_profile(self.h, iters, _stream(stream), C.byref(ms), C.byref(fl), C.byref(n)))
         return ms.value, fl.value, n.value
+
+    def gemm_profile_detail(self, iters: int = 5, stream=None) -> List[Dict[str, float]]:
+        """Per-launch timing of the step's GEMMs (CUDA events between eager launches)."""
+        n = C.c_int32()
+        _check(self.L.rfx_net_gemm_profile_detail(self.h, iters, _stream(stream), None, 0, C.byref(n)))
+        buf = (C.c_double * (8 * max(n.value, 1)))()
+        _check(self.L.rfx_net_gemm_profile_detail(self.h, iters, _stream(stream), buf, n.value, C.byref(n)))
+        keys = ("M", "N", "K", "a_kind", "b_kind", "splits", "ms", "flops")
+        return [dict(zip(keys, buf[8 * i: 8 * i + 8])) for i in range(n.value)]
 
     def read_loss(self, stream=None) -> float:
         v = C.c_float()

@@ -33,6 +33,7 @@ enum class OpKind : int { Input = 0, Conv, BN, BNAddReLU, ReLU, MaxPool, AvgPool
 const char* op_kind_name(OpKind k);
 
 constexpr long kAlign = 1024;  // arena slot alignment (bytes); costs are rounded to it
+constexpr long kStatRows = 160;  // fused-BN partial rows: >= the persistent GEMM grid (SM count)
 inline long align_up(long x, long a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Tensor {
@@ -199,6 +200,7 @@ class Net {
   void op_forward(const Op& op, bool reforward, int phase, cudaStream_t st);
   void op_backward(const Op& op, cudaStream_t st);
   void prep_weights(cudaStream_t st);
+  void prep_weights_table(cudaStream_t st);  // per-layer table variant (unused by the step)
   void* tptr(int t) const;
   __nv_bfloat16* tb(int t) const { return static_cast<__nv_bfloat16*>(tptr(t)); }
   __nv_bfloat16* gptr(int t) const;

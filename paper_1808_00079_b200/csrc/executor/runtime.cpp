@@ -62,19 +62,13 @@ void Net::setup(uint64_t seed) {
   if (!planned_) throw std::invalid_argument("plan the network before setup");
   free_device();
   // bf16 weight copies
-  n_bf16_ = 0;
+  // the bf16 weight buffer mirrors the fp32 master buffer element for element
+  // (BN parameters ride along unused), so refreshing it after SGD is one flat
+  // vectorised cast; dgrad reads the same copy through a transposing TMA map
+  n_bf16_ = n_params_;
   for (auto& p : params_) {
-    const Op& op = ops_[p.op];
-    if (p.kind == 0) {
-      p.bf16_off = n_bf16_;
-      p.bf16_count = p.count;
-      n_bf16_ += (p.count + 63) / 64 * 64;
-      (void)op;  // dgrad reads the same copy through a transposing TMA map
-    } else if (p.kind == 3) {
-      p.bf16_off = n_bf16_;
-      p.bf16_count = p.count;
-      n_bf16_ += (p.count + 63) / 64 * 64;
-    }
+    p.bf16_off = p.offset;
+    p.bf16_count = p.count;
   }
   auto alloc = [&](void** p, long bytes, const char* what) {
     check(cudaMalloc(p, bytes > 0 ? bytes : 256), what);
@@ -291,7 +285,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         int parts;
         if (prod.kind == OpKind::Conv && prod.fuse_stats) {
           partials = ws_stats + prod.stats_off;
-          parts = (int)((y.rows() + 127) / 128);
+          parts = (int)kStatRows;  // rows past the GEMM's grid are zero
         } else {
           parts = rfk::colstats_blocks(y.rows());
           check(rfk::colstats(tb(op.in[0]), y.rows(), y.C, ws_part, parts, st), "colstats");
@@ -462,13 +456,13 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       if (op.wg_splits > 1) {
         // split-K partials in the workspace, summed in split order by the
         // last CTA of each tile straight into the gradient buffer
+        // (the GEMM can also finish split-K itself — final_out/counters — but a
+        // whole-GPU reduction kernel is faster when few tiles carry many splits)
         d.splits = op.wg_splits;
         d.out = ws_split;
         d.split_stride = (long)op.cout * kw;
-        d.final_out = dW;
-        d.counters = reinterpret_cast<int*>(ws + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ +
-                                            ws_misc_);
         gemm(d, st);
+        check(rfk::reduce_splits(ws_split, op.wg_splits, (long)op.cout * kw, dW, false, st), "reduce_splits");
       } else {
         d.out = dW;
         gemm(d, st);
@@ -575,6 +569,10 @@ void Net::run_instr(const Instr& ins, cudaStream_t st) {
 
 // ============================================================ step
 void Net::prep_weights(cudaStream_t st) {
+  check(rfk::cast_f32_bf16_vec(d_param_, n_params_, d_bf16_, st), "weight cast");
+}
+
+void Net::prep_weights_table(cudaStream_t st) {
   // one batched launch over every conv / fc weight (table built once)
   if (!d_prep_table_) {
     std::vector<rfk::WeightPrepLayer> tab;
@@ -708,8 +706,8 @@ void Net::forward_backward(cudaStream_t st) {
 }
 
 void Net::update(float lr, float momentum, float wd, cudaStream_t st) {
-  check(rfk::sgd_update(d_param_, d_grad_, d_mom_, n_params_, lr, momentum, wd, st), "sgd");
-  prep_weights(st);
+  // one pass: momentum SGD on the fp32 masters + refresh of their bf16 copy
+  check(rfk::sgd_update(d_param_, d_grad_, d_mom_, n_params_, lr, momentum, wd, d_bf16_, st), "sgd");
 }
 
 cudaGraphExec_t Net::capture(const std::function<void(cudaStream_t)>& body, long* kernel_nodes) {

@@ -649,9 +649,8 @@ void Net::layout() {
   }
   for (auto& op : ops_)
     if (op.kind == OpKind::Conv && op.fuse_stats) {
-      const long mt = (tensors_[op.out].rows() + 127) / 128;
-      op.stats_off = ws_stats_ / 4;
-      ws_stats_ += align_up(mt * 2 * op.cout * 4);
+      op.stats_off = ws_stats_ / 4;  // [kStatRows][2][cout]: one row per persistent GEMM CTA
+      ws_stats_ += align_up(kStatRows * 2 * op.cout * 4);
     }
   // split-K tile counters (zeroed once at setup; kernels leave them zero)
   ws_counters_ = 0;

@@ -242,12 +242,40 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const uint32_t lane = lane_id();
     uint8_t* stg = stage_buf + quarter * 2048;  // this warp's 32 x 64 B staging tile
     __shared__ float red_s[4][32], red_q[4][32];
+    // Fused BN statistics are accumulated per CTA over all its tiles of one
+    // column block (tiles come in order, so a column block never returns) and
+    // written once as this CTA's row of stats[gridDim][2][N]: the finalize
+    // sums ~148 rows instead of one per M tile.  Rows of column blocks a CTA
+    // never touches stay zero (workspace zeroed once; same mapping every launch).
+    __shared__ float col_s[BN], col_q[BN];
+    int cur_nt = -1;
+    auto flush_stats = [&](int nt) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      float* row = p.stats + (long)blockIdx.x * 2 * p.N;
+      for (int c = (int)(quarter * 32 + lane); c < BN; c += 128) {
+        const int col = nt * BN + c;
+        if (col < p.N) {
+          row[col] = col_s[c];
+          row[p.N + col] = col_q[c];
+        }
+        col_s[c] = 0.f;
+        col_q[c] = 0.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    };
+    if (p.stats) {
+      for (int c = (int)(quarter * 32 + lane); c < BN; c += 128) col_s[c] = col_q[c] = 0.f;
+    }
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const TileCoord tc = tile_coord(p, t, BN);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const bool empty_k = tc.kb_end <= tc.kb_begin;
+      if (p.stats && tc.n0 / BN != cur_nt) {
+        if (cur_nt >= 0) flush_stats(cur_nt);
+        cur_nt = tc.n0 / BN;
+      }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int m = tc.m0 + (int)(quarter * 32 + lane);
@@ -303,14 +331,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               q2[i] = (upper ? q2[i + half] : q2[i]) + got_q;
             }
           }
-          const int col = col0 + (int)lane;
-          float* st = p.stats + (long)(tc.m0 / kBlockM) * 2 * p.N;
           red_s[quarter][lane] = s[0];
           red_q[quarter][lane] = q2[0];
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (quarter == 0 && col < p.N) {  // fixed order over the four row quarters
-            st[col] = ((red_s[0][lane] + red_s[1][lane]) + red_s[2][lane]) + red_s[3][lane];
-            st[p.N + col] = ((red_q[0][lane] + red_q[1][lane]) + red_q[2][lane]) + red_q[3][lane];
+          if (quarter == 0) {  // fixed order over the four row quarters, then across tiles
+            col_s[c0 + lane] += ((red_s[0][lane] + red_s[1][lane]) + red_s[2][lane]) + red_s[3][lane];
+            col_q[c0 + lane] += ((red_q[0][lane] + red_q[1][lane]) + red_q[2][lane]) + red_q[3][lane];
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
         }
@@ -417,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
       }
     }
+    if (p.stats && cur_nt >= 0) flush_stats(cur_nt);
   }
   tc_fence_before();
   __syncthreads();

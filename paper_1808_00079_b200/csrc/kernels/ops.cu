@@ -38,6 +38,11 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 
 __device__ __forceinline__ uint4 ldg16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
+__device__ __forceinline__ uint32_t pack_bf16_pair(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 int grid_for(long work, int per_block, int cap = 148 * 16) {
   long g = (work + per_block - 1) / per_block;
   if (g < 1) g = 1;
@@ -606,6 +611,15 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ x, long n, __nv_b
     y[i] = __float2bfloat16_rn(x[i]);
 }
 
+__global__ void __launch_bounds__(kThreads) cast_f32_bf16_vec_kernel(const float* __restrict__ x, long nvec,
+                                                                    __nv_bfloat16* __restrict__ y) {
+  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    float f[8];
+    ld8f(x + v * 8, f);
+    *reinterpret_cast<uint4*>(y + v * 8) = pack8(f);
+  }
+}
+
 // fp32 [R, C] -> bf16 [R, ldo] (pad columns untouched)
 __global__ void cast_f32_bf16_2d_kernel(const float* __restrict__ x, int R, int C, int ldo,
                                         __nv_bfloat16* __restrict__ y) {
@@ -634,23 +648,70 @@ __global__ void colsum_f32_kernel(const float* __restrict__ x, int R, int C, flo
 }
 
 // sum of split-K partials [splits][n] -> out (fixed order)
-__global__ void reduce_splits_kernel(const float* __restrict__ parts, int splits, long n, float* __restrict__ out,
-                                     int acc) {
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += parts[(long)z * n + i];
-    out[i] = acc ? out[i] + s : s;
+// float4 per thread, split loop unrolled by 4 so several loads are in flight;
+// summation order z = 0, 1, ... is fixed (deterministic)
+__global__ void __launch_bounds__(kThreads) reduce_splits_kernel(const float* __restrict__ parts, int splits, long n4,
+                                                                float* __restrict__ out, int acc) {
+  const float4* p4 = reinterpret_cast<const float4*>(parts);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    int z = 0;
+    for (; z + 4 <= splits; z += 4) {
+      const float4 a = __ldg(p4 + (long)z * n4 + i), b = __ldg(p4 + (long)(z + 1) * n4 + i);
+      const float4 c = __ldg(p4 + (long)(z + 2) * n4 + i), d = __ldg(p4 + (long)(z + 3) * n4 + i);
+      s.x = (((s.x + a.x) + b.x) + c.x) + d.x;
+      s.y = (((s.y + a.y) + b.y) + c.y) + d.y;
+      s.z = (((s.z + a.z) + b.z) + c.z) + d.z;
+      s.w = (((s.w + a.w) + b.w) + c.w) + d.w;
+    }
+    for (; z < splits; ++z) {
+      const float4 a = __ldg(p4 + (long)z * n4 + i);
+      s.x += a.x;
+      s.y += a.y;
+      s.z += a.z;
+      s.w += a.w;
+    }
+    float4* o = reinterpret_cast<float4*>(out) + i;
+    if (acc) {
+      const float4 prev = *o;
+      s.x += prev.x;
+      s.y += prev.y;
+      s.z += prev.z;
+      s.w += prev.w;
+    }
+    *o = s;
   }
 }
 
 // ------------------------------------------------------------ optimizer + layouts
-__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m, long n, float lr,
-                           float momentum, float wd) {
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
-    const float d = g[i] + wd * w[i];
-    const float v = momentum * m[i] + d;
-    m[i] = v;
-    w[i] = w[i] - lr * v;
+// SGD with momentum and weight decay, 4 parameters per thread-iteration; when
+// wb is given it also refreshes the bf16 GEMM copy of the weights in the same
+// pass (n % 4 == 0, 16-byte aligned buffers).
+__global__ void __launch_bounds__(kThreads) sgd_kernel(float* __restrict__ w, const float* __restrict__ g,
+                                                      float* __restrict__ m, long n4, float lr, float momentum,
+                                                      float wd, __nv_bfloat16* __restrict__ wb) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
+    float4 wv = reinterpret_cast<float4*>(w)[i];
+    const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
+    float4 mv = reinterpret_cast<float4*>(m)[i];
+    float* wp = &wv.x;
+    const float* gp = &gv.x;
+    float* mp = &mv.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float d = gp[k] + wd * wp[k];
+      const float v = momentum * mp[k] + d;
+      mp[k] = v;
+      wp[k] = wp[k] - lr * v;
+    }
+    reinterpret_cast<float4*>(m)[i] = mv;
+    reinterpret_cast<float4*>(w)[i] = wv;
+    if (wb) {
+      uint2 o;
+      o.x = pack_bf16_pair(wv.x, wv.y);
+      o.y = pack_bf16_pair(wv.z, wv.w);
+      reinterpret_cast<uint2*>(wb)[i] = o;
+    }
   }
 }
 
@@ -951,6 +1012,12 @@ cudaError_t cast_f32_bf16(const float* x, long n, __nv_bfloat16* y, cudaStream_t
   return cudaGetLastError();
 }
 
+cudaError_t cast_f32_bf16_vec(const float* x, long n, __nv_bfloat16* y, cudaStream_t st) {
+  if (n % 8) return cudaErrorInvalidValue;
+  cast_f32_bf16_vec_kernel<<<grid_for(n / 8, kThreads * 4), kThreads, 0, st>>>(x, n / 8, y);
+  return cudaGetLastError();
+}
+
 cudaError_t cast_f32_bf16_2d(const float* x, int R, int C, int ldo, __nv_bfloat16* y, cudaStream_t st) {
   cast_f32_bf16_2d_kernel<<<grid_for((long)R * C, kThreads * 4), kThreads, 0, st>>>(x, R, C, ldo, y);
   return cudaGetLastError();
@@ -967,13 +1034,16 @@ cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaS
 }
 
 cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bool acc, cudaStream_t st) {
-  reduce_splits_kernel<<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(parts, splits, n, out, acc ? 1 : 0);
+  if (n % 4) return cudaErrorInvalidValue;
+  reduce_splits_kernel<<<grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st>>>(parts, splits, n / 4, out,
+                                                                               acc ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, float momentum, float wd,
-                       cudaStream_t st) {
-  sgd_kernel<<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(w, g, m, n, lr, momentum, wd);
+                       __nv_bfloat16* wb, cudaStream_t st) {
+  if (n % 4) return cudaErrorInvalidValue;
+  sgd_kernel<<<grid_for(n / 4, kThreads * 2), kThreads, 0, st>>>(w, g, m, n / 4, lr, momentum, wd, wb);
   return cudaGetLastError();
 }
 

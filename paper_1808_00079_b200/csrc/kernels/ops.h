@@ -41,12 +41,15 @@ cudaError_t softmax_ce_fwd(const float* logits, const int* labels, int N, int K,
 cudaError_t softmax_ce_bwd(const float* logits, const int* labels, const float* lse, int N, int K, float* dlogits,
                            cudaStream_t st);
 cudaError_t cast_f32_bf16(const float* x, long n, __nv_bfloat16* y, cudaStream_t st);
+// n % 8 == 0, 16-byte aligned buffers: 8 elements per thread-iteration
+cudaError_t cast_f32_bf16_vec(const float* x, long n, __nv_bfloat16* y, cudaStream_t st);
 cudaError_t cast_f32_bf16_2d(const float* x, int R, int C, int ldo, __nv_bfloat16* y, cudaStream_t st);
 cudaError_t colsum_bf16(const __nv_bfloat16* x, int R, int C, float* out, bool acc, cudaStream_t st);
 cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaStream_t st);
 cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bool acc, cudaStream_t st);
+// wb (optional): bf16 copy of w refreshed in the same pass
 cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, float momentum, float wd,
-                       cudaStream_t st);
+                       __nv_bfloat16* wb, cudaStream_t st);
 cudaError_t conv_weight_prep(const float* w, int Cout, int R, int S, int Cpad, int Cin, int CoutPad,
                              __nv_bfloat16* wb, __nv_bfloat16* wt, cudaStream_t st);
 // One launch for every conv / fc layer after an SGD step: bf16 copy of the

@@ -627,8 +627,12 @@ void Net::layout() {
         ws_zero_ = std::max(ws_zero_, align_up((long)x.N * (x.H - op.R + 1 + 2 * op.pad) *
                                                (x.W - op.S + 1 + 2 * op.pad) * op.cout * 2));
       const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
-      op.wg_bn = kw <= 64 ? 64 : (kw <= 128 ? 128 : 256);
-      const long tiles = ((op.cout + 127) / 128) * ((kw + op.wg_bn - 1) / op.wg_bn);
+      // weight-gradient orientation: the larger of (filter elements, Cout)
+      // goes on the 128-row M side of the MMA
+      op.wg_swap = kw > op.cout;
+      const long mside = op.wg_swap ? kw : op.cout, nside = op.wg_swap ? op.cout : kw;
+      op.wg_bn = nside <= 64 ? 64 : (nside <= 128 ? 128 : 256);
+      const long tiles = ((mside + 127) / 128) * ((nside + op.wg_bn - 1) / op.wg_bn);
       op.wg_splits = wgrad_splits(tiles, (y.rows() + 63) / 64);
       if (op.wg_splits > 1) ws_split_ = std::max(ws_split_, align_up((long)op.wg_splits * op.cout * kw * 4));
       // fused BN statistics slot for this conv

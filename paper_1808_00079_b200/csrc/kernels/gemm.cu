@@ -47,6 +47,8 @@ struct alignas(64) KParams {
   long split_stride;
   int remap, rP, rQ, rH, rW, rsh, rsw;
   int b_taps;  // WeightTapsMN: filter taps R*S
+  int g_taps;  // im2col operand: filter taps R*S
+  int store_t; // fp32 output stored transposed: out[col][m] with row length ldc
   float* final_out;  // split-K finished in-kernel into this fp32 matrix (null: keep partials)
   int* counters;     // per output tile, zero between launches
   int stages;  // smem ring depth (<= Cfg::kStages)
@@ -149,6 +151,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               tma_load_2d(sa, &p.ta, &full[stage], tc.m0, kb * kBlockK);
               tma_load_2d(sa + kTileA / 2, &p.ta, &full[stage], tc.m0 + 64, kb * kBlockK);
               break;
+            case (int)Operand::Im2colMN: {  // A = im2col(X)^T: K = 64 output pixels, M = (tap, channel)
+              int bw, bh, bn;
+              pixel_base(p, kb * kBlockK, bw, bh, bn);
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int mb = tc.m0 / 64 + j;
+                int tap = mb / p.g_cblocks;
+                const int cb = mb - tap * p.g_cblocks;
+                tap = min(tap, p.g_taps - 1);  // rows past M are masked in the epilogue
+                const int r = tap / p.g_S, s = tap - r * p.g_S;
+                tma_load_im2col(sa + j * 8192, &p.ta, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+              }
+              break;
+            }
             default: {  // Im2colK: K block -> (tap, channel block)
               const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
               const int r = tap / p.g_S, s = tap - r * p.g_S;
@@ -193,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    const bool a_mn = p.a_kind == (int)Operand::MNMajor2D;
+    const bool a_mn = p.a_kind == (int)Operand::MNMajor2D || p.a_kind == (int)Operand::Im2colMN;
     const bool b_mn = p.b_kind == (int)Operand::MNMajor2D || p.b_kind == (int)Operand::Im2colMN ||
                       p.b_kind == (int)Operand::WeightTapsMN;
     const uint32_t idesc = umma_idesc_bf16(kBlockM, BN, a_mn, b_mn);
@@ -340,7 +356,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
           asm volatile("bar.sync 1, 128;" ::: "memory");
         }
-        if (p.out_f32) {
+        if (p.out_f32 && p.store_t) {
+          // transposed store: element (m, col) -> out[col][m]; consecutive lanes
+          // hold consecutive m, so each of the 32 stores is one coalesced line
+          float* dst = reinterpret_cast<float*>(p.out) + (long)tc.z * p.split_stride + m;
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.N) dst[(long)(col0 + i) * p.ldc] = v[i];
+          }
+        } else if (p.out_f32) {
           float* dst = reinterpret_cast<float*>(p.out) + (long)tc.z * p.split_stride + (long)m * p.ldc + col0;
           if (!row_ok) {
           } else if (full_cols) {
@@ -577,13 +602,19 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
       kp.num_kb = (d.K + 63) / 64;
       break;
     case Operand::MNMajor2D:
-      ok = encode_2d(&kp.ta, d.a, d.M, d.K, d.a_ld, 64, 64);
+      ok = encode_2d(&kp.ta, d.a, d.a_extent > 0 ? d.a_extent : d.M, d.K, d.a_ld, 64, 64);
       kp.num_kb = (d.K + 63) / 64;
       break;
     case Operand::Im2colK:
       geo = &d.a_geom;
       ok = encode_im2col(&kp.ta, d.a, d.a_geom, kBlockM);
       kp.num_kb = d.a_geom.R * d.a_geom.S * ((d.a_geom.C + 63) / 64);
+      break;
+    case Operand::Im2colMN:  // weight-gradient GEMM computed transposed: M = (tap, channel)
+      if (d.b_kind == Operand::Im2colMN || d.b_kind == Operand::WeightTapsMN) return cudaErrorInvalidValue;
+      geo = &d.a_geom;
+      ok = encode_im2col(&kp.ta, d.a, d.a_geom, 64);
+      kp.num_kb = (d.K + 63) / 64;
       break;
     default:
       return cudaErrorInvalidValue;
@@ -629,6 +660,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
     kp.g_sw = geo->stride_w;
     kp.g_S = geo->S;
     kp.g_cblocks = (geo->C + 63) / 64;
+    kp.g_taps = geo->R * geo->S;
   }
   const int splits = d.splits < 1 ? 1 : d.splits;
   kp.kb_per_split = (kp.num_kb + splits - 1) / splits;
@@ -636,6 +668,9 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   kp.ldc = d.ldc;
   kp.out_f32 = d.out_f32;
   kp.accumulate_out = d.accumulate_out;
+  kp.store_t = d.store_t ? 1 : 0;
+  if (d.store_t && (!d.out_f32 || d.accumulate_out || d.bias || d.stats || d.remap || d.final_out))
+    return cudaErrorInvalidValue;
   kp.bias = d.bias;
   kp.stats = d.stats;
   kp.split_stride = d.split_stride;

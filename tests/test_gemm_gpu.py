@@ -169,3 +169,28 @@ def test_conv_dgrad_weight_taps(N, H, W, Ci, Co, R, pad):
     K.gemm(args)
     torch.cuda.synchronize()
     _check(out, ref)
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,R,pad,st", CONV_CASES)
+@pytest.mark.parametrize("splits", [1, 4])
+def test_conv_wgrad_transposed(N, H, W, Ci, Co, R, pad, st, splits):
+    # D^T[(tap, ci), co] = im2col(X)^T dY with A = im2col in MN-major form,
+    # stored transposed straight into the dW[co][(tap, ci)] layout
+    x = _bf(N, Ci, H, W, seed=13)
+    g = K.conv_geom(N, H, W, Ci, R, R, pad, st)
+    dy = _bf(N, Co, g.P, g.Q, seed=14)
+    ref = torch.nn.grad.conv2d_weight(x.float(), (Co, Ci, R, R), dy.float(), stride=st, padding=pad)
+    cpad = (Ci + 63) // 64 * 64
+    xn = x.permute(0, 2, 3, 1).contiguous()
+    dyn = dy.permute(0, 2, 3, 1).contiguous()
+    M = N * g.P * g.Q
+    ktot = R * R * cpad
+    out = torch.zeros(splits, Co, ktot, device=dev)
+    args = K.GemmArgs(M=ktot, N=Co, K=M, a_kind=K.IM2COL_MN, a=xn.data_ptr(), a_geom=g, b_kind=K.MNMAJOR,
+                      b=dyn.data_ptr(), b_ld=Co, out=out.data_ptr(), ldc=ktot, out_f32=1, splits=splits,
+                      split_stride=Co * ktot)
+    args.store_t = 1
+    K.gemm(args)
+    torch.cuda.synchronize()
+    got = out.sum(0).reshape(Co, R, R, cpad)[..., :Ci].permute(0, 3, 1, 2)
+    _check(got, ref)

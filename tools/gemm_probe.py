@@ -1,0 +1,95 @@
+"""Isolated timing of representative ResNet-50 GEMM launches (run on the GPU).
+
+python tools/gemm_probe.py            # time every case
+python tools/gemm_probe.py --only 3   # one case, a few launches (for ncu)
+"""
+import argparse
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1808_00079_b200 import kernels as K  # noqa: E402
+
+dev = "cuda"
+
+
+def bf(*shape):
+    return (torch.randn(*shape, device=dev) * 0.5).to(torch.bfloat16)
+
+
+def cases():
+    out = []
+    # 1x1 fprop, K=64 -> N=256 at 56x56 (stage-1 expand), with fused BN stats
+    M, Kd, N = 32 * 56 * 56, 64, 256
+    a, b, o = bf(M, Kd), bf(N, Kd), bf(M, N)
+    st = torch.zeros(160, 2, N, device=dev)
+    out.append(("1x1 fprop K64 N256 +stats", M, N, Kd,
+                dict(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, b_kind=K.KMAJOR, b=b.data_ptr(),
+                     b_ld=Kd, out=o.data_ptr(), ldc=N, stats=st.data_ptr(), splits=1), (a, b, o, st), {}))
+    out.append(("1x1 fprop K64 N256", M, N, Kd,
+                dict(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, b_kind=K.KMAJOR, b=b.data_ptr(),
+                     b_ld=Kd, out=o.data_ptr(), ldc=N, splits=1), (a, b, o), {}))
+    # 1x1 dgrad 64 -> 256 accumulating into the skip gradient
+    wt = bf(Kd, N)  # [Cout=64][Cin=256]: MN-major B
+    out.append(("1x1 dgrad K64 N256 accumulate", M, N, Kd,
+                dict(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, b_kind=K.MNMAJOR, b=wt.data_ptr(),
+                     b_ld=N, out=o.data_ptr(), ldc=N, accumulate_out=1, splits=1), (a, wt, o), {"b_extent": N}))
+    # 3x3 dgrad (stage 4 stride-2 via zero insert): M=6272 N=512 K=4608, weights in place
+    n, h, ci, co = 32, 14, 512, 512
+    dy = bf(n, h, h, co)
+    w = bf(co, 3, 3, ci)
+    o2 = bf(n, h, h, ci)
+    g = K.ConvGeom(n, h, h, co, h, h, 3, 3, 1, 1, 1, 1)
+    out.append(("3x3 dgrad Wtaps 14x14x512", n * h * h, ci, 9 * co,
+                dict(M=n * h * h, N=ci, K=9 * co, a_kind=K.IM2COL_K, a=dy.data_ptr(), a_geom=g, b_kind=4,
+                     b=w.data_ptr(), out=o2.data_ptr(), ldc=ci, splits=1), (dy, w, o2),
+                {"b_extent": ci, "b_taps": 9, "b_cpad": ci, "b_rows": co}))
+    # same contraction as a 3x3 fprop (K-major weights)
+    wk = bf(co, 9 * ci)
+    out.append(("3x3 fprop im2col 14x14x512", n * h * h, co, 9 * ci,
+                dict(M=n * h * h, N=co, K=9 * ci, a_kind=K.IM2COL_K, a=dy.data_ptr(), a_geom=g, b_kind=K.KMAJOR,
+                     b=wk.data_ptr(), b_ld=9 * ci, out=o2.data_ptr(), ldc=co, splits=1), (dy, wk, o2), {}))
+    # plain 2-D GEMM of the same size
+    a3 = bf(n * h * h, 9 * ci)
+    out.append(("2D K-major 6272x512x4608", n * h * h, co, 9 * ci,
+                dict(M=n * h * h, N=co, K=9 * ci, a_kind=K.KMAJOR, a=a3.data_ptr(), a_ld=9 * ci, b_kind=K.KMAJOR,
+                     b=wk.data_ptr(), b_ld=9 * ci, out=o2.data_ptr(), ldc=co, splits=1), (a3, wk, o2), {}))
+    # large square 2-D GEMM: the engine's best case
+    S = 8192
+    a4, b4, o4 = bf(S, S), bf(S, S), bf(S, S)
+    out.append(("2D K-major 8192^3", S, S, S,
+                dict(M=S, N=S, K=S, a_kind=K.KMAJOR, a=a4.data_ptr(), a_ld=S, b_kind=K.KMAJOR, b=b4.data_ptr(),
+                     b_ld=S, out=o4.data_ptr(), ldc=S, splits=1), (a4, b4, o4), {}))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", type=int, default=-1)
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    torch.manual_seed(0)
+    for i, (name, M, N, Kd, kw, keep, extra) in enumerate(cases()):
+        if args.only >= 0 and i != args.only:
+            continue
+        ga = K.GemmArgs(**kw)
+        for k, v in extra.items():
+            setattr(ga, k, v)
+        iters = 3 if args.only >= 0 else args.iters
+        for _ in range(2):
+            K.gemm(ga)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            K.gemm(ga)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / iters
+        fl = 2.0 * M * N * Kd
+        print(f"[{i}] {name:32s} {us:8.1f} us  {fl / us / 1e6:7.1f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    main()

@@ -40,8 +40,6 @@ typedef struct rfx_gemm_args {
   int32_t block_n;
   int64_t b_extent;                  /* valid MN extent of an MN-major B (0 = N) */
   int32_t b_taps, b_cpad, b_rows;    /* kind 4 (conv weights as dgrad B): R*S, Cpad, Cout */
-  int64_t a_extent;                  /* valid MN extent of an MN-major A (0 = M) */
-  int32_t store_t;                   /* fp32 output stored transposed: out[n][m], row length ldc */
 } rfx_gemm_args;
 /* kind 4 = conv weights [Cout][R][S][Cpad] read as the dgrad B operand (flipped taps) */
 

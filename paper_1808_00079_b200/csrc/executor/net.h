@@ -76,7 +76,6 @@ struct Op {
   bool fuse_stats = false;   // conv epilogue emits BN partial sums for its consumer
   long stats_off = -1;       // its slot in the statistics workspace (floats)
   int wg_splits = 1, wg_bn = 128;  // wgrad split-K and tile N
-  bool wg_swap = false;            // wgrad computed as D^T = X_col^T dY (stored transposed)
   // pool
   int k = 1;
   // classifier

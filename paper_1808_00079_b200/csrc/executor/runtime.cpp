@@ -428,61 +428,34 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
       float* dW = d_grad_ + w.offset;
       rfk::GemmDesc d;
+      d.M = op.cout;
+      d.N = (int)kw;
       d.K = (int)y.rows();
+      d.a_kind = rfk::Operand::MNMajor2D;
+      d.a = dy;
+      d.a_ld = op.cout;
       d.out_f32 = true;
       d.ldc = kw;
       d.block_n = op.wg_bn;
-      // the activation side: explicit im2col buffer, the raw tensor (1x1), or TMA im2col
-      rfk::Operand xk;
-      const void* xp;
-      long x_ld = 0, x_ext = 0;
-      rfk::ConvGeom xg{};
       if (op.explicit_im2col) {
         rfk::ConvShape cs{x.N, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
         check(rfk::im2col(tb(op.in[0]), cs, op.kpad, ws_im2col, st), "im2col");
-        xk = rfk::Operand::MNMajor2D;
-        xp = ws_im2col;
-        x_ld = x_ext = op.kpad;
-      } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0) {
-        xk = rfk::Operand::MNMajor2D;
-        xp = tptr(op.in[0]);
-        x_ld = x_ext = op.cin;
-      } else {
-        xk = rfk::Operand::Im2colMN;
-        xp = tptr(op.in[0]);
-        xg = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad, op.stride, op.stride};
-      }
-      if (op.wg_swap) {
-        // D^T[kw, cout] = X_col^T dY, stored transposed into dW[cout][kw]:
-        // the long filter side fills the 128-row MMA tiles
-        d.M = (int)kw;
-        d.N = op.cout;
-        d.a_kind = xk;
-        d.a = xp;
-        d.a_ld = x_ld;
-        d.a_extent = x_ext;
-        d.a_geom = xg;
         d.b_kind = rfk::Operand::MNMajor2D;
-        d.b = dy;
-        d.b_ld = op.cout;
-        d.store_t = true;
+        d.b = ws_im2col;
+        d.b_ld = op.kpad;
+      } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0) {
+        d.b_kind = rfk::Operand::MNMajor2D;
+        d.b = tptr(op.in[0]);
+        d.b_ld = op.cin;
+        d.b_extent = op.cin;
       } else {
-        d.M = op.cout;
-        d.N = (int)kw;
-        d.a_kind = rfk::Operand::MNMajor2D;
-        d.a = dy;
-        d.a_ld = op.cout;
-        d.b_kind = xk;
-        d.b = xp;
-        d.b_ld = x_ld;
-        d.b_extent = x_ext;
-        d.b_geom = xg;
+        d.b_kind = rfk::Operand::Im2colMN;
+        d.b = tptr(op.in[0]);
+        d.b_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad, op.stride, op.stride};
       }
       if (op.wg_splits > 1) {
-        // split-K partials in the workspace, summed in split order by the
-        // last CTA of each tile straight into the gradient buffer
-        // (the GEMM can also finish split-K itself — final_out/counters — but a
-        // whole-GPU reduction kernel is faster when few tiles carry many splits)
+        // split-K partials in the workspace, summed in split order by a
+        // whole-GPU reduction kernel into the gradient buffer
         d.splits = op.wg_splits;
         d.out = ws_split;
         d.split_stride = (long)op.cout * kw;

@@ -627,12 +627,8 @@ void Net::layout() {
         ws_zero_ = std::max(ws_zero_, align_up((long)x.N * (x.H - op.R + 1 + 2 * op.pad) *
                                                (x.W - op.S + 1 + 2 * op.pad) * op.cout * 2));
       const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
-      // weight-gradient orientation: the larger of (filter elements, Cout)
-      // goes on the 128-row M side of the MMA
-      op.wg_swap = kw > op.cout;
-      const long mside = op.wg_swap ? kw : op.cout, nside = op.wg_swap ? op.cout : kw;
-      op.wg_bn = nside <= 64 ? 64 : (nside <= 128 ? 128 : 256);
-      const long tiles = ((mside + 127) / 128) * ((nside + op.wg_bn - 1) / op.wg_bn);
+      op.wg_bn = kw <= 64 ? 64 : (kw <= 128 ? 128 : 256);
+      const long tiles = ((op.cout + 127) / 128) * ((kw + op.wg_bn - 1) / op.wg_bn);
       op.wg_splits = wgrad_splits(tiles, (y.rows() + 63) / 64);
       if (op.wg_splits > 1) ws_split_ = std::max(ws_split_, align_up((long)op.wg_splits * op.cout * kw * 4));
       // fused BN statistics slot for this conv
@@ -656,13 +652,7 @@ void Net::layout() {
       op.stats_off = ws_stats_ / 4;  // [kStatRows][2][cout]: one row per persistent GEMM CTA
       ws_stats_ += align_up(kStatRows * 2 * op.cout * 4);
     }
-  // split-K tile counters (zeroed once at setup; kernels leave them zero)
   ws_counters_ = 0;
-  for (const auto& op : ops_)
-    if (op.kind == OpKind::Conv) {
-      const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
-      ws_counters_ = std::max(ws_counters_, align_up(((op.cout + 127) / 128) * ((kw + op.wg_bn - 1) / op.wg_bn) * 4L));
-    }
   rep_.workspace_bytes = ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_ + ws_counters_;
   rep_.param_bytes = n_params_ * 4 * 3;
   rep_.state_bytes = n_state_ * 4;

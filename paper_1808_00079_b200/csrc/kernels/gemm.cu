@@ -28,10 +28,12 @@ constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;
 constexpr int kThreads = 192;
 constexpr int kTileA = kBlockM * kBlockK * 2;  // 16 KB
+constexpr int kStaging = 4 * 2 * 2048;          // epilogue: 4 warps x 2 buffers x (32 rows x 64 B)
 
 struct alignas(64) KParams {
   CUtensorMap ta;  // 64-byte aligned, must be first
   CUtensorMap tb;
+  CUtensorMap tc;  // output {N, M, splits}: 32x32 bf16 or 16x32 fp32 boxes, SWIZZLE_64B
   int M, N, K;
   int num_kb;          // total K blocks
   int kb_per_split;
@@ -47,10 +49,7 @@ struct alignas(64) KParams {
   long split_stride;
   int remap, rP, rQ, rH, rW, rsh, rsw;
   int b_taps;  // WeightTapsMN: filter taps R*S
-  int g_taps;  // im2col operand: filter taps R*S
-  int store_t; // fp32 output stored transposed: out[col][m] with row length ldc
-  float* final_out;  // split-K finished in-kernel into this fp32 matrix (null: keep partials)
-  int* counters;     // per output tile, zero between launches
+  int out_mode;  // 0 generic stores, 1 TMA store, 2 TMA reduce-add (accumulate_out)
   int stages;  // smem ring depth (<= Cfg::kStages)
   int m_tiles, n_tiles, splits;  // persistent tile space
 };
@@ -61,7 +60,8 @@ struct Cfg {
   static constexpr int kStage = kTileA + kTileB;
   static constexpr int kStages = (BN == 64) ? 8 : (BN == 128 ? 6 : 4);  // ~190 KB ring
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
-  static constexpr int kSmem = kStages * kStage + 4 * 2048 /*epilogue staging*/ + 1024 /*align*/ + 256;
+  static constexpr int kStats = 4 * 2 * BN * 4;  // per-warp column sums
+  static constexpr int kSmem = kStages * kStage + kStaging + kStats + 1024 /*align*/ + 256;
 };
 
 // Decode a flattened output-pixel index into im2col TMA base coordinates.
@@ -94,14 +94,36 @@ __device__ __forceinline__ TileCoord tile_coord(const KParams& p, int t, int BN)
   return c;
 }
 
+// Stage one 32-row x 64-byte box (lane = row) in 64B-swizzled smem and hand
+// it to the TMA unit; the buffer was last used two boxes ago.
+__device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const uint32_t (&w)[16], uint32_t lane,
+                                            int mode, int cx, int my, int z) {
+  if (lane == 0) bulk_wait_read<1>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t sw = (uint32_t)j ^ ((lane >> 1) & 3u);  // SWIZZLE_64B
+    *reinterpret_cast<uint4*>(b + lane * 64 + sw * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (mode == 2)
+      tma_reduce_add_3d(&p.tc, b, cx, my, z);
+    else
+      tma_store_3d(&p.tc, b, cx, my, z);
+    bulk_commit();
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nst = p.stages;
-  uint8_t* stage_buf = smem + nst * C::kStage;  // 4 warps x 32 rows x 64 B epilogue staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + 4 * 2048);
+  uint8_t* stage_buf = smem + nst * C::kStage;  // epilogue staging, then the column sums
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + kStaging + C::kStats);
   uint64_t* empty = full + nst;
   uint64_t* acc_full = empty + nst;   // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2; // [2] epilogue -> MMA
@@ -113,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   if (warp == 0 && elect_one()) {
     tma_prefetch(&p.ta);
     tma_prefetch(&p.tb);
+    if (p.out_mode) tma_prefetch(&p.tc);
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -151,20 +174,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               tma_load_2d(sa, &p.ta, &full[stage], tc.m0, kb * kBlockK);
               tma_load_2d(sa + kTileA / 2, &p.ta, &full[stage], tc.m0 + 64, kb * kBlockK);
               break;
-            case (int)Operand::Im2colMN: {  // A = im2col(X)^T: K = 64 output pixels, M = (tap, channel)
-              int bw, bh, bn;
-              pixel_base(p, kb * kBlockK, bw, bh, bn);
-#pragma unroll
-              for (int j = 0; j < 2; ++j) {
-                const int mb = tc.m0 / 64 + j;
-                int tap = mb / p.g_cblocks;
-                const int cb = mb - tap * p.g_cblocks;
-                tap = min(tap, p.g_taps - 1);  // rows past M are masked in the epilogue
-                const int r = tap / p.g_S, s = tap - r * p.g_S;
-                tma_load_im2col(sa + j * 8192, &p.ta, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
-              }
-              break;
-            }
             default: {  // Im2colK: K block -> (tap, channel block)
               const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
               const int r = tap / p.g_S, s = tap - r * p.g_S;
@@ -209,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    const bool a_mn = p.a_kind == (int)Operand::MNMajor2D || p.a_kind == (int)Operand::Im2colMN;
+    const bool a_mn = p.a_kind == (int)Operand::MNMajor2D;
     const bool b_mn = p.b_kind == (int)Operand::MNMajor2D || p.b_kind == (int)Operand::Im2colMN ||
                       p.b_kind == (int)Operand::WeightTapsMN;
     const uint32_t idesc = umma_idesc_bf16(kBlockM, BN, a_mn, b_mn);
@@ -254,33 +263,51 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
   } else {
     // ------------------------------------------------ epilogue (warps 2..5)
+    // TMEM -> registers (32 columns at a time) -> [bias] -> [column statistics]
+    // -> 64-byte-swizzled smem staging -> TMA store / TMA reduce-add of a
+    // 32-row box.  Two staging buffers per warp let the next chunk be staged
+    // while the previous box is still being read out by the TMA unit.
     const uint32_t quarter = warp & 3;
     const uint32_t lane = lane_id();
-    uint8_t* stg = stage_buf + quarter * 2048;  // this warp's 32 x 64 B staging tile
-    __shared__ float red_s[4][32], red_q[4][32];
-    // Fused BN statistics are accumulated per CTA over all its tiles of one
-    // column block (tiles come in order, so a column block never returns) and
-    // written once as this CTA's row of stats[gridDim][2][N]: the finalize
-    // sums ~148 rows instead of one per M tile.  Rows of column blocks a CTA
-    // never touches stay zero (workspace zeroed once; same mapping every launch).
-    __shared__ float col_s[BN], col_q[BN];
+    uint8_t* stg = stage_buf + quarter * 4096;
+    // Fused BN statistics: each warp keeps its own per-column sums in smem
+    // (lane l owns column c0 + l, so no synchronisation per chunk); when the
+    // CTA moves to another column block the four warps' sums are combined in
+    // a fixed order and written once as this CTA's row of stats[gridDim][2][N].
+    // The finalize then sums ~148 rows instead of one per M tile.  Rows of
+    // column blocks a CTA never touches stay zero (workspace zeroed once; the
+    // tile -> CTA mapping is the same every launch).
+    float* wsum = reinterpret_cast<float*>(stage_buf + kStaging);  // [4 warps][2][BN]
+    float* my_sum = wsum + quarter * 2 * BN;
+    const int mode = p.out_mode;
+    int buf = 0;
+    auto tma_out = [&](const uint32_t(&w)[16], int cx, int my, int z) {
+      epi_tma_out(p, stg + buf * 2048, w, lane, mode, cx, my, z);
+      buf ^= 1;
+    };
     int cur_nt = -1;
     auto flush_stats = [&](int nt) {
       asm volatile("bar.sync 1, 128;" ::: "memory");
       float* row = p.stats + (long)blockIdx.x * 2 * p.N;
       for (int c = (int)(quarter * 32 + lane); c < BN; c += 128) {
+        float s = 0.f, q = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          s += wsum[(2 * w) * BN + c];
+          q += wsum[(2 * w + 1) * BN + c];
+          wsum[(2 * w) * BN + c] = 0.f;
+          wsum[(2 * w + 1) * BN + c] = 0.f;
+        }
         const int col = nt * BN + c;
         if (col < p.N) {
-          row[col] = col_s[c];
-          row[p.N + col] = col_q[c];
+          row[col] = s;
+          row[p.N + col] = q;
         }
-        col_s[c] = 0.f;
-        col_q[c] = 0.f;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
     };
     if (p.stats) {
-      for (int c = (int)(quarter * 32 + lane); c < BN; c += 128) col_s[c] = col_q[c] = 0.f;
+      for (int c = (int)lane; c < BN; c += 32) my_sum[c] = my_sum[BN + c] = 0.f;
     }
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
@@ -294,7 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      const int m = tc.m0 + (int)(quarter * 32 + lane);
+      const int my = tc.m0 + (int)(quarter * 32);
+      const int m = my + (int)lane;
       const bool row_ok = m < p.M;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -347,45 +375,39 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               q2[i] = (upper ? q2[i + half] : q2[i]) + got_q;
             }
           }
-          red_s[quarter][lane] = s[0];
-          red_q[quarter][lane] = q2[0];
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (quarter == 0) {  // fixed order over the four row quarters, then across tiles
-            col_s[c0 + lane] += ((red_s[0][lane] + red_s[1][lane]) + red_s[2][lane]) + red_s[3][lane];
-            col_q[c0 + lane] += ((red_q[0][lane] + red_q[1][lane]) + red_q[2][lane]) + red_q[3][lane];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          my_sum[c0 + lane] += s[0];
+          my_sum[BN + c0 + lane] += q2[0];
         }
-        if (p.out_f32 && p.store_t) {
-          // transposed store: element (m, col) -> out[col][m]; consecutive lanes
-          // hold consecutive m, so each of the 32 stores is one coalesced line
-          float* dst = reinterpret_cast<float*>(p.out) + (long)tc.z * p.split_stride + m;
-          if (row_ok) {
+        if (mode != 0) {
+          uint32_t w[16];
+          if (p.out_f32) {  // two 16-column fp32 boxes
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (col0 + i < p.N) dst[(long)(col0 + i) * p.ldc] = v[i];
-          }
-        } else if (p.out_f32) {
-          float* dst = reinterpret_cast<float*>(p.out) + (long)tc.z * p.split_stride + (long)m * p.ldc + col0;
-          if (!row_ok) {
-          } else if (full_cols) {
-            if (p.accumulate_out) {
+            for (int i = 0; i < 16; ++i) w[i] = __float_as_uint(v[i]);
+            tma_out(w, col0, my, tc.z);
+            if (col0 + 16 < p.N) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) dst[i] += v[i];
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+              for (int i = 0; i < 16; ++i) w[i] = __float_as_uint(v[16 + i]);
+              tma_out(w, col0 + 16, my, tc.z);
             }
           } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+            tma_out(w, col0, my, tc.z);
+          }
+          continue;
+        }
+        // ---- generic stores (row remap scatter, or an output TMA cannot address)
+        if (p.out_f32) {
+          float* dst = reinterpret_cast<float*>(p.out) + (long)tc.z * p.split_stride + (long)m * p.ldc + col0;
+          if (row_ok) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (col0 + i < p.N) dst[i] = p.accumulate_out ? dst[i] + v[i] : v[i];
           }
           continue;
         }
-        // ---- bf16 output: stage the warp's 32 x 32 tile in smem (16-byte
-        // chunks XOR-swizzled by row), then write whole 64-byte row segments
-        // with 4 lanes per row: 8 rows per instruction instead of 32.
+        // bf16: stage the warp's 32 x 32 tile in smem, then write whole
+        // 64-byte row segments with 4 lanes per row (8 rows per instruction)
         uint32_t w[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
@@ -395,11 +417,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           *reinterpret_cast<uint4*>(stg + lane * 64 + sw * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
         }
         __syncwarp();
-#pragma unroll
+#pragma unroll 1
         for (int it = 0; it < 4; ++it) {
           const uint32_t row = it * 8 + (lane >> 2), chunk = lane & 3;
           const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 64 + ((chunk ^ ((row >> 1) & 3u)) * 16));
-          const int mr = tc.m0 + (int)(quarter * 32 + row);
+          const int mr = my + (int)row;
           if (mr < p.M && (full_cols || col0 + (int)chunk * 8 < p.N)) {
             long orow = mr;
             if (p.remap) {
@@ -408,22 +430,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             }
             __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long)tc.z * p.split_stride +
                                  orow * p.ldc + col0 + chunk * 8;
-            if (full_cols || col0 + (int)chunk * 8 + 8 <= p.N) {
-              uint4 o = val;
-              if (p.accumulate_out) {
-                const uint4 prev = *reinterpret_cast<const uint4*>(dst);
-                const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&val);
-                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&prev);
-                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 fa = __bfloat1622float2(a2[e]), fb = __bfloat1622float2(b2[e]);
-                  o2[e] = __floats2bfloat162_rn(fa.x + fb.x, fa.y + fb.y);
-                }
-              }
-              *reinterpret_cast<uint4*>(dst) = o;
+            const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&val);
+            if (!p.accumulate_out && (full_cols || col0 + (int)chunk * 8 + 8 <= p.N)) {
+              *reinterpret_cast<uint4*>(dst) = val;
             } else {
-              const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&val);
               for (int e = 0; e < 8 && col0 + (int)chunk * 8 + e < p.N; ++e)
                 dst[e] = p.accumulate_out ? __float2bfloat16_rn(__bfloat162float(dst[e]) + __bfloat162float(vb[e]))
                                           : vb[e];
@@ -432,43 +442,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
         __syncwarp();
       }
-      if (p.final_out) {
-        // Split-K finish without a second kernel: every CTA publishes its
-        // fp32 partial and bumps the tile's counter; the CTA that completes
-        // the count sums all partials in split order 0..S-1 (so the result
-        // does not depend on which CTA came last) and resets the counter.
-        __shared__ int s_last;
-        const int tile_id = tc.m0 / kBlockM + p.m_tiles * (tc.n0 / BN);
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (quarter == 0 && lane == 0) s_last = atomicAdd(p.counters + tile_id, 1) == p.splits - 1;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (s_last) {
-          __threadfence();
-          const float* part = reinterpret_cast<const float*>(p.out);
-          for (int i = 0; i < 32; ++i) {
-            const int row = tc.m0 + (int)quarter * 32 + i;
-            if (row >= p.M) break;
-            for (int c = (int)lane * 4; c < BN; c += 128) {
-              const int col = tc.n0 + c;
-              if (col >= p.N) break;
-              const long off = (long)row * p.ldc + col;
-              float4 a = __ldcg(reinterpret_cast<const float4*>(part + off));
-              for (int z = 1; z < p.splits; ++z) {
-                const float4 b = __ldcg(reinterpret_cast<const float4*>(part + (long)z * p.split_stride + off));
-                a.x += b.x;
-                a.y += b.y;
-                a.z += b.z;
-                a.w += b.w;
-              }
-              *reinterpret_cast<float4*>(p.final_out + off) = a;
-            }
-          }
-          if (quarter == 0 && lane == 0) p.counters[tile_id] = 0;
-        }
-      }
     }
     if (p.stats && cur_nt >= 0) flush_stats(cur_nt);
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -553,7 +529,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, cudaStr
   kp.splits = splits;
   const long kb_per_cta = (long)kp.kb_per_split * ((total + grid - 1) / grid);
   kp.stages = (int)std::max<long>(2, std::min<long>(C::kStages, kb_per_cta));
-  const int smem = kp.stages * C::kStage + 4 * 2048 + 1024 + 256;
+  const int smem = kp.stages * C::kStage + kStaging + C::kStats + 1024 + 256;
   gemm_kernel<BN><<<grid, kThreads, smem, st>>>(kp);
   return cudaGetLastError();
 }
@@ -602,19 +578,13 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
       kp.num_kb = (d.K + 63) / 64;
       break;
     case Operand::MNMajor2D:
-      ok = encode_2d(&kp.ta, d.a, d.a_extent > 0 ? d.a_extent : d.M, d.K, d.a_ld, 64, 64);
+      ok = encode_2d(&kp.ta, d.a, d.M, d.K, d.a_ld, 64, 64);
       kp.num_kb = (d.K + 63) / 64;
       break;
     case Operand::Im2colK:
       geo = &d.a_geom;
       ok = encode_im2col(&kp.ta, d.a, d.a_geom, kBlockM);
       kp.num_kb = d.a_geom.R * d.a_geom.S * ((d.a_geom.C + 63) / 64);
-      break;
-    case Operand::Im2colMN:  // weight-gradient GEMM computed transposed: M = (tap, channel)
-      if (d.b_kind == Operand::Im2colMN || d.b_kind == Operand::WeightTapsMN) return cudaErrorInvalidValue;
-      geo = &d.a_geom;
-      ok = encode_im2col(&kp.ta, d.a, d.a_geom, 64);
-      kp.num_kb = (d.K + 63) / 64;
       break;
     default:
       return cudaErrorInvalidValue;
@@ -660,7 +630,6 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
     kp.g_sw = geo->stride_w;
     kp.g_S = geo->S;
     kp.g_cblocks = (geo->C + 63) / 64;
-    kp.g_taps = geo->R * geo->S;
   }
   const int splits = d.splits < 1 ? 1 : d.splits;
   kp.kb_per_split = (kp.num_kb + splits - 1) / splits;
@@ -668,17 +637,25 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   kp.ldc = d.ldc;
   kp.out_f32 = d.out_f32;
   kp.accumulate_out = d.accumulate_out;
-  kp.store_t = d.store_t ? 1 : 0;
-  if (d.store_t && (!d.out_f32 || d.accumulate_out || d.bias || d.stats || d.remap || d.final_out))
-    return cudaErrorInvalidValue;
   kp.bias = d.bias;
   kp.stats = d.stats;
   kp.split_stride = d.split_stride;
-  if (d.final_out) {
-    if (!d.out_f32 || d.accumulate_out || !d.counters || d.remap || d.ldc % 4) return cudaErrorInvalidValue;
-    kp.final_out = d.splits > 1 ? d.final_out : nullptr;
-    kp.counters = d.counters;
-    if (d.splits <= 1) kp.out = d.final_out;  // nothing to reduce: write the result directly
+  // output through TMA (store, or reduce-add when accumulating) whenever the
+  // rows are not remapped and the strides are 16-byte multiples
+  {
+    const int es = d.out_f32 ? 4 : 2;
+    const long sstride = splits > 1 ? d.split_stride : (long)d.M * d.ldc;
+    if (!d.remap && d.out && ((long)d.ldc * es) % 16 == 0 && (sstride * es) % 16 == 0 &&
+        (reinterpret_cast<uintptr_t>(d.out) & 15) == 0) {
+      cuuint64_t dims[3] = {(cuuint64_t)d.N, (cuuint64_t)d.M, (cuuint64_t)splits};
+      cuuint64_t strides[2] = {(cuuint64_t)d.ldc * es, (cuuint64_t)sstride * es};
+      cuuint32_t box[3] = {d.out_f32 ? 16u : 32u, 32u, 1u};
+      cuuint32_t estr[3] = {1, 1, 1};
+      if (g_encode_tiled(&kp.tc, d.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                         d.out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        kp.out_mode = d.accumulate_out ? 2 : 1;
+    }
   }
   kp.remap = d.remap;
   kp.rP = d.rP;

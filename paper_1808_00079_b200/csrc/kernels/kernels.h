@@ -16,7 +16,7 @@ enum class Operand : int {
   KMajor2D = 0,   // rows x K, K contiguous (row stride `ld` elements)
   MNMajor2D = 1,  // K rows x MN, MN contiguous (row stride `ld` elements)
   Im2colK = 2,    // NHWC activation, rows = output pixels, K = (r, s, c)
-  Im2colMN = 3,   // NHWC activation, K = output pixels, MN = (r, s, c)  (A or B)
+  Im2colMN = 3,   // NHWC activation, K = output pixels, MN = (r, s, c)
   // conv weights [Cout][R][S][Cpad] read as the dgrad B operand: MN = input
   // channel (contiguous), K = (flipped tap, Cout) — no transposed copy needed
   WeightTapsMN = 4,
@@ -37,7 +37,6 @@ struct GemmDesc {
   const void* a = nullptr;
   long a_ld = 0;
   ConvGeom a_geom;
-  long a_extent = 0;  // valid MN extent of an MN-major 2-D A (0 = M)
   Operand b_kind = Operand::KMajor2D;
   const void* b = nullptr;
   long b_ld = 0;
@@ -53,13 +52,6 @@ struct GemmDesc {
   float* stats = nullptr;       // [m_tiles][2][N] column sum / sum of squares
   int splits = 1;               // split-K; split z writes out + z * split_stride
   long split_stride = 0;
-  // fp32 split-K only: the last CTA of each output tile sums the partials (in
-  // split order) into final_out; counters = m_tiles * n_tiles zeroed ints
-  float* final_out = nullptr;
-  int* counters = nullptr;
-  // fp32 only: store D transposed, out[n][m] with row length ldc (weight
-  // gradients computed as D^T = X_col^T dY when the filter side is larger)
-  bool store_t = false;
   // row remap of the output (strided-conv dgrad scatter): row m = (n, p, q)
   // over P x Q goes to n * H * W + (p * sh) * W + q * sw.
   bool remap = false;

@@ -777,6 +777,29 @@ __global__ void pack_input_kernel(const float* __restrict__ x, int N, int C, int
   }
 }
 
+// one thread per pixel and group of 8 channels: plane reads are coalesced
+// across the warp (consecutive w), the NHWC write is one 16-byte store
+__global__ void pack_input_vec_kernel(const float* __restrict__ x, int N, int C, int H, int W, int Cpad,
+                                      __nv_bfloat16* __restrict__ out) {
+  const long HW = (long)H * W;
+  const int groups = Cpad / 8;
+  const long total = (long)N * HW * groups;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long pix = i % ((long)N * HW);
+    const int grp = (int)(i / ((long)N * HW));
+    const long n = pix / HW, hw = pix % HW;
+    uint32_t w2[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c0 = grp * 8 + 2 * j;
+      const float a = c0 < C ? __ldg(x + (n * C + c0) * HW + hw) : 0.f;
+      const float b = c0 + 1 < C ? __ldg(x + (n * C + c0 + 1) * HW + hw) : 0.f;
+      w2[j] = pack_bf16_pair(a, b);
+    }
+    *reinterpret_cast<uint4*>(out + pix * Cpad + grp * 8) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+  }
+}
+
 // explicit im2col for thin-channel convs: out[m][k], k = (r*S + s)*C + c, K
 // padded with zeros to Kpad.
 // One thread per (output pixel, 8 consecutive k): a single 16-byte store;
@@ -818,6 +841,54 @@ __global__ void __launch_bounds__(kThreads) im2col_kernel(const __nv_bfloat16* _
     o.z = e[4] | ((uint32_t)e[5] << 16);
     o.w = e[6] | ((uint32_t)e[7] << 16);
     *reinterpret_cast<uint4*>(out + m * Kpad + k0) = o;
+  }
+}
+
+// Row-staged im2col (the stem's few-channel conv): one block per output row
+// (n, p) stages the R input rows it reads, zero-padded to W + 2*pad columns,
+// in shared memory with 16-byte loads, then writes the Q x Kpad slab with
+// coalesced 16-byte stores.  The gather happens in shared memory instead of
+// as 2-byte global loads, so the kernel runs at the output write rate.
+__global__ void __launch_bounds__(kThreads) im2col_rows_kernel(const __nv_bfloat16* __restrict__ x, ConvShape g,
+                                                              int Kpad, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned short rows_s[];  // [R][W + 2 pad][Cs]
+  const int Wp = g.W + 2 * g.pad;
+  const int cv = g.Cs / 8;  // 16-byte vectors per pixel
+  const int kv = Kpad / 8;
+  const int Kreal = g.R * g.S * g.C;
+  for (long rowid = blockIdx.x; rowid < (long)g.N * g.P; rowid += gridDim.x) {
+    const int p = (int)(rowid % g.P), n = (int)(rowid / g.P);
+    __syncthreads();
+    const uint4* xv = reinterpret_cast<const uint4*>(x) + (long)n * g.H * g.W * cv;
+    for (int i = threadIdx.x; i < g.R * Wp * cv; i += blockDim.x) {
+      const int c8 = i % cv, t = i / cv, wp = t % Wp, r = t / Wp;
+      const int h = p * g.stride - g.pad + r, w = wp - g.pad;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = __ldg(xv + ((long)h * g.W + w) * cv + c8);
+      reinterpret_cast<uint4*>(rows_s)[i] = v;
+    }
+    __syncthreads();
+    uint4* o = reinterpret_cast<uint4*>(out + rowid * g.Q * Kpad);
+    for (int i = threadIdx.x; i < g.Q * kv; i += blockDim.x) {
+      const int q = i / kv, k0 = (i % kv) * 8;
+      int c = k0 % g.C, rs = k0 / g.C;
+      unsigned short e[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        unsigned short v = 0;
+        if (k0 + j < Kreal) {
+          const int s = rs % g.S, r = rs / g.S;
+          v = rows_s[((long)r * Wp + q * g.stride + s) * g.Cs + c];
+        }
+        e[j] = v;
+        if (++c == g.C) {
+          c = 0;
+          ++rs;
+        }
+      }
+      o[i] = make_uint4(e[0] | ((uint32_t)e[1] << 16), e[2] | ((uint32_t)e[3] << 16), e[4] | ((uint32_t)e[5] << 16),
+                        e[6] | ((uint32_t)e[7] << 16));
+    }
   }
 }
 
@@ -1062,6 +1133,11 @@ cudaError_t weight_prep_batched(const WeightPrepLayer* table_dev, int layers, lo
 }
 
 cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __nv_bfloat16* out, cudaStream_t st) {
+  if (Cpad % 8 == 0) {
+    const long work = (long)N * H * W * (Cpad / 8);
+    pack_input_vec_kernel<<<grid_for(work, kThreads * 2), kThreads, 0, st>>>(x, N, C, H, W, Cpad, out);
+    return cudaGetLastError();
+  }
   const long total = (long)N * H * W * Cpad;
   pack_input_kernel<<<grid_for(total, kThreads * 4), kThreads, 0, st>>>(x, N, C, H, W, Cpad, out);
   return cudaGetLastError();
@@ -1069,6 +1145,17 @@ cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __n
 
 cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st) {
   if (Kpad % 8) return cudaErrorInvalidValue;
+  const long rows_smem = (long)g.R * (g.W + 2 * g.pad) * g.Cs * 2;
+  if (g.Cs % 8 == 0 && rows_smem <= 96 * 1024) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(im2col_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      attr_set = true;
+    }
+    const long rows = (long)g.N * g.P;
+    im2col_rows_kernel<<<(int)std::min<long>(rows, 148 * 8), kThreads, rows_smem, st>>>(x, g, Kpad, out);
+    return cudaGetLastError();
+  }
   const long total = (long)g.N * g.P * g.Q * (Kpad / 8);
   im2col_kernel<<<grid_for(total, kThreads * 2, 148 * 32), kThreads, 0, st>>>(x, g, Kpad, out);
   return cudaGetLastError();

@@ -171,26 +171,29 @@ def test_conv_dgrad_weight_taps(N, H, W, Ci, Co, R, pad):
     _check(out, ref)
 
 
-@pytest.mark.parametrize("N,H,W,Ci,Co,R,pad,st", CONV_CASES)
-@pytest.mark.parametrize("splits", [1, 4])
-def test_conv_wgrad_transposed(N, H, W, Ci, Co, R, pad, st, splits):
-    # D^T[(tap, ci), co] = im2col(X)^T dY with A = im2col in MN-major form,
-    # stored transposed straight into the dW[co][(tap, ci)] layout
-    x = _bf(N, Ci, H, W, seed=13)
-    g = K.conv_geom(N, H, W, Ci, R, R, pad, st)
-    dy = _bf(N, Co, g.P, g.Q, seed=14)
-    ref = torch.nn.grad.conv2d_weight(x.float(), (Co, Ci, R, R), dy.float(), stride=st, padding=pad)
-    cpad = (Ci + 63) // 64 * 64
-    xn = x.permute(0, 2, 3, 1).contiguous()
-    dyn = dy.permute(0, 2, 3, 1).contiguous()
-    M = N * g.P * g.Q
-    ktot = R * R * cpad
-    out = torch.zeros(splits, Co, ktot, device=dev)
-    args = K.GemmArgs(M=ktot, N=Co, K=M, a_kind=K.IM2COL_MN, a=xn.data_ptr(), a_geom=g, b_kind=K.MNMAJOR,
-                      b=dyn.data_ptr(), b_ld=Co, out=out.data_ptr(), ldc=ktot, out_f32=1, splits=splits,
-                      split_stride=Co * ktot)
-    args.store_t = 1
+@pytest.mark.parametrize("M,N,Kd,f32", [(256, 256, 64, False), (200, 72, 96, False), (130, 40, 128, True)])
+def test_gemm_accumulate_out(M, N, Kd, f32):
+    # out += A B^T (TMA reduce-add epilogue)
+    a = _bf(M, Kd, seed=15)
+    b = _bf(N, Kd, seed=16)
+    prev = _bf(M, N, seed=17)
+    out = prev.float().clone() if f32 else prev.clone()
+    ref = prev.float() + a.float() @ b.float().t()
+    args = K.GemmArgs(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, b_kind=K.KMAJOR, b=b.data_ptr(),
+                      b_ld=Kd, out=out.data_ptr(), ldc=N, out_f32=int(f32), accumulate_out=1, splits=1)
     K.gemm(args)
     torch.cuda.synchronize()
-    got = out.sum(0).reshape(Co, R, R, cpad)[..., :Ci].permute(0, 3, 1, 2)
-    _check(got, ref)
+    _check(out, ref)
+
+
+def test_gemm_split_partials_isolated():
+    # split-K partials: rows past M of one split must not spill into the next
+    M, N, Kd, S = 64, 192, 512, 4
+    a = _bf(M, Kd, seed=18)
+    b = _bf(N, Kd, seed=19)
+    out = torch.full((S, M, N), 7.0, device=dev)
+    args = K.GemmArgs(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, b_kind=K.KMAJOR, b=b.data_ptr(),
+                      b_ld=Kd, out=out.data_ptr(), ldc=N, out_f32=1, splits=S, split_stride=M * N)
+    K.gemm(args)
+    torch.cuda.synchronize()
+    _check(out.sum(0), a.float() @ b.float().t())

@@ -350,37 +350,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] += (col0 + i < p.N) ? __ldg(p.bias + col0 + i) : 0.f;
         }
-        if (p.stats) {
-          // Column sums over this warp's 32 rows by a halving butterfly: after
-          // 5 rounds lane l holds column l's total (31 shuffles per 32 columns).
-          float s[32], q2[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            // statistics of the values actually stored (bf16-rounded), so the
-            // BatchNorm that reads them back normalises exactly what it sees
-            const float sv = p.out_f32 ? v[i] : __bfloat162float(__float2bfloat16_rn(v[i]));
-            s[i] = row_ok ? sv : 0.f;
-            q2[i] = s[i] * s[i];
-          }
-#pragma unroll
-          for (int half = 16; half >= 1; half >>= 1) {
-            const bool upper = (lane & half) != 0;
-#pragma unroll
-            for (int i = 0; i < half; ++i) {
-              const float send_s = upper ? s[i] : s[i + half];
-              const float send_q = upper ? q2[i] : q2[i + half];
-              const float got_s = __shfl_xor_sync(0xffffffffu, send_s, half);
-              const float got_q = __shfl_xor_sync(0xffffffffu, send_q, half);
-              s[i] = (upper ? s[i + half] : s[i]) + got_s;
-              q2[i] = (upper ? q2[i + half] : q2[i]) + got_q;
-            }
-          }
-          my_sum[c0 + lane] += s[0];
-          my_sum[BN + c0 + lane] += q2[0];
-        }
-        if (mode != 0) {
-          uint32_t w[16];
-          if (p.out_f32) {  // two 16-column fp32 boxes
+        if (p.out_f32) {
+          if (mode != 0) {  // two 16-column fp32 boxes
+            uint32_t w[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) w[i] = __float_as_uint(v[i]);
             tma_out(w, col0, my, tc.z);
@@ -389,55 +361,97 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               for (int i = 0; i < 16; ++i) w[i] = __float_as_uint(v[16 + i]);
               tma_out(w, col0 + 16, my, tc.z);
             }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-            tma_out(w, col0, my, tc.z);
-          }
-          continue;
-        }
-        // ---- generic stores (row remap scatter, or an output TMA cannot address)
-        if (p.out_f32) {
-          float* dst = reinterpret_cast<float*>(p.out) + (long)tc.z * p.split_stride + (long)m * p.ldc + col0;
-          if (row_ok) {
+          } else if (row_ok) {
+            float* dst = reinterpret_cast<float*>(p.out) + (long)tc.z * p.split_stride + (long)m * p.ldc + col0;
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (col0 + i < p.N) dst[i] = p.accumulate_out ? dst[i] + v[i] : v[i];
           }
           continue;
         }
-        // bf16: stage the warp's 32 x 32 tile in smem, then write whole
-        // 64-byte row segments with 4 lanes per row (8 rows per instruction)
+        // bf16: rows past M are staged as zeros (TMA clips them on store; the
+        // statistics below then need no row mask)
         uint32_t w[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) w[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+        for (int i = 0; i < 16; ++i) w[i] = row_ok ? pack_bf16(v[2 * i], v[2 * i + 1]) : 0u;
+        const uint8_t* sbuf;
+        if (mode != 0) {
+          sbuf = stg + buf * 2048;
+          tma_out(w, col0, my, tc.z);
+        } else {
+          // generic: stage in the spare buffer, then write whole 64-byte row
+          // segments with 4 lanes per row (8 rows per instruction)
+          uint8_t* gb = stg + 2048;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t sw = (uint32_t)j ^ ((lane >> 1) & 3u);
-          *reinterpret_cast<uint4*>(stg + lane * 64 + sw * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-        }
-        __syncwarp();
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t sw = (uint32_t)j ^ ((lane >> 1) & 3u);
+            *reinterpret_cast<uint4*>(gb + lane * 64 + sw * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+          }
+          __syncwarp();
 #pragma unroll 1
-        for (int it = 0; it < 4; ++it) {
-          const uint32_t row = it * 8 + (lane >> 2), chunk = lane & 3;
-          const uint4 val = *reinterpret_cast<const uint4*>(stg + row * 64 + ((chunk ^ ((row >> 1) & 3u)) * 16));
-          const int mr = my + (int)row;
-          if (mr < p.M && (full_cols || col0 + (int)chunk * 8 < p.N)) {
-            long orow = mr;
-            if (p.remap) {
-              const int q = mr % p.rQ, tt = mr / p.rQ, pp = tt % p.rP, nn = tt / p.rP;
-              orow = (long)nn * p.rH * p.rW + (long)(pp * p.rsh) * p.rW + (long)q * p.rsw;
+          for (int it = 0; it < 4; ++it) {
+            const uint32_t row = it * 8 + (lane >> 2), chunk = lane & 3;
+            const uint4 val = *reinterpret_cast<const uint4*>(gb + row * 64 + ((chunk ^ ((row >> 1) & 3u)) * 16));
+            const int mr = my + (int)row;
+            if (mr < p.M && (full_cols || col0 + (int)chunk * 8 < p.N)) {
+              long orow = mr;
+              if (p.remap) {
+                const int q = mr % p.rQ, tt = mr / p.rQ, pp = tt % p.rP, nn = tt / p.rP;
+                orow = (long)nn * p.rH * p.rW + (long)(pp * p.rsh) * p.rW + (long)q * p.rsw;
+              }
+              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long)tc.z * p.split_stride +
+                                   orow * p.ldc + col0 + chunk * 8;
+              const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&val);
+              if (full_cols || col0 + (int)chunk * 8 + 8 <= p.N) {
+                uint4 o = val;
+                if (p.accumulate_out) {
+                  const uint4 prev = *reinterpret_cast<const uint4*>(dst);
+                  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&val);
+                  const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&prev);
+                  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 fa = __bfloat1622float2(a2[e]), fb = __bfloat1622float2(b2[e]);
+                    o2[e] = __floats2bfloat162_rn(fa.x + fb.x, fa.y + fb.y);
+                  }
+                }
+                *reinterpret_cast<uint4*>(dst) = o;
+              } else {
+                for (int e = 0; e < 8 && col0 + (int)chunk * 8 + e < p.N; ++e)
+                  dst[e] = p.accumulate_out ? __float2bfloat16_rn(__bfloat162float(dst[e]) + __bfloat162float(vb[e]))
+                                            : vb[e];
+              }
             }
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long)tc.z * p.split_stride +
-                                 orow * p.ldc + col0 + chunk * 8;
-            const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&val);
-            if (!p.accumulate_out && (full_cols || col0 + (int)chunk * 8 + 8 <= p.N)) {
-              *reinterpret_cast<uint4*>(dst) = val;
-            } else {
-              for (int e = 0; e < 8 && col0 + (int)chunk * 8 + e < p.N; ++e)
-                dst[e] = p.accumulate_out ? __float2bfloat16_rn(__bfloat162float(dst[e]) + __bfloat162float(vb[e]))
-                                          : vb[e];
-            }
+          }
+          sbuf = gb;
+        }
+        if (p.stats) {
+          // Column sums of the staged (bf16-rounded: exactly what the
+          // BatchNorm reads back) 32 x 32 tile: lane l sums the column pair
+          // 2 (l & 15) over the even (l < 16) or odd rows, then the two row
+          // halves combine with one shuffle.  Even/odd rows sit in opposite
+          // 64-byte halves of the bank space, so the reads are conflict-free.
+          const uint32_t cp = lane & 15, par = lane >> 4;
+          float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
+#pragma unroll
+          for (int rr = 0; rr < 16; ++rr) {
+            const uint32_t row = 2 * rr + par;
+            const uint32_t off = row * 64 + (((cp >> 2) ^ ((row >> 1) & 3u)) * 16) + (cp & 3) * 4;
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sbuf + off));
+            s0 += f.x;
+            s1 += f.y;
+            q0 = fmaf(f.x, f.x, q0);
+            q1 = fmaf(f.y, f.y, q1);
+          }
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+          q0 += __shfl_xor_sync(0xffffffffu, q0, 16);
+          q1 += __shfl_xor_sync(0xffffffffu, q1, 16);
+          if (lane < 16) {
+            my_sum[c0 + 2 * lane] += s0;
+            my_sum[c0 + 2 * lane + 1] += s1;
+            my_sum[BN + c0 + 2 * lane] += q0;
+            my_sum[BN + c0 + 2 * lane + 1] += q1;
           }
         }
         __syncwarp();
@@ -562,6 +576,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   if (d.b_kind == Operand::MNMajor2D || d.b_kind == Operand::Im2colMN || d.b_kind == Operand::WeightTapsMN)
     bn = bn < 64 ? 64 : bn;
   if (bn != 64 && bn != 128 && bn != 256) return cudaErrorInvalidValue;
+  if (d.stats && d.out_f32) return cudaErrorInvalidValue;  // statistics are of the stored bf16 values
 
   KParams kp;
   std::memset(&kp, 0, sizeof(kp));

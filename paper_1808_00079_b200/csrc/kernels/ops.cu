@@ -851,11 +851,18 @@ __global__ void __launch_bounds__(kThreads) im2col_kernel(const __nv_bfloat16* _
 // as 2-byte global loads, so the kernel runs at the output write rate.
 __global__ void __launch_bounds__(kThreads) im2col_rows_kernel(const __nv_bfloat16* __restrict__ x, ConvShape g,
                                                               int Kpad, __nv_bfloat16* __restrict__ out) {
-  extern __shared__ __align__(16) unsigned short rows_s[];  // [R][W + 2 pad][Cs]
+  extern __shared__ __align__(16) unsigned short rows_s[];  // [R][W + 2 pad][Cs], then the k table
   const int Wp = g.W + 2 * g.pad;
   const int cv = g.Cs / 8;  // 16-byte vectors per pixel
   const int kv = Kpad / 8;
   const int Kreal = g.R * g.S * g.C;
+  // k -> offset of (r, s, c) in the staged rows relative to the output
+  // pixel's first column (-1: K padding)
+  int* ktab = reinterpret_cast<int*>(rows_s + (long)g.R * Wp * g.Cs);
+  for (int k = threadIdx.x; k < Kpad; k += blockDim.x) {
+    const int c = k % g.C, rs = k / g.C, s = rs % g.S, r = rs / g.S;
+    ktab[k] = k < Kreal ? (r * Wp + s) * g.Cs + c : -1;
+  }
   for (long rowid = blockIdx.x; rowid < (long)g.N * g.P; rowid += gridDim.x) {
     const int p = (int)(rowid % g.P), n = (int)(rowid / g.P);
     __syncthreads();
@@ -871,23 +878,14 @@ __global__ void __launch_bounds__(kThreads) im2col_rows_kernel(const __nv_bfloat
     uint4* o = reinterpret_cast<uint4*>(out + rowid * g.Q * Kpad);
     for (int i = threadIdx.x; i < g.Q * kv; i += blockDim.x) {
       const int q = i / kv, k0 = (i % kv) * 8;
-      int c = k0 % g.C, rs = k0 / g.C;
-      unsigned short e[8];
+      const unsigned short* px = rows_s + q * g.stride * g.Cs;
+      uint32_t e[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        unsigned short v = 0;
-        if (k0 + j < Kreal) {
-          const int s = rs % g.S, r = rs / g.S;
-          v = rows_s[((long)r * Wp + q * g.stride + s) * g.Cs + c];
-        }
-        e[j] = v;
-        if (++c == g.C) {
-          c = 0;
-          ++rs;
-        }
+        const int off = ktab[k0 + j];
+        e[j] = off >= 0 ? px[off] : 0u;
       }
-      o[i] = make_uint4(e[0] | ((uint32_t)e[1] << 16), e[2] | ((uint32_t)e[3] << 16), e[4] | ((uint32_t)e[5] << 16),
-                        e[6] | ((uint32_t)e[7] << 16));
+      o[i] = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16), e[6] | (e[7] << 16));
     }
   }
 }
@@ -1145,7 +1143,7 @@ cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __n
 
 cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st) {
   if (Kpad % 8) return cudaErrorInvalidValue;
-  const long rows_smem = (long)g.R * (g.W + 2 * g.pad) * g.Cs * 2;
+  const long rows_smem = (long)g.R * (g.W + 2 * g.pad) * g.Cs * 2 + (long)Kpad * 4;
   if (g.Cs % 8 == 0 && rows_smem <= 96 * 1024) {
     static bool attr_set = false;
     if (!attr_set) {

@@ -44,32 +44,59 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region.
 
-    def __init__(self, index: int = 0):
+    NVML (nvidia-ml-py) is polled every few milliseconds from a thread, so
+    even a ~100 ms timed region gets tens of samples; nvidia-smi (one query
+    per ~0.2 s) is the fallback when NVML is unavailable.
+    """
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
+
+    def __init__(self, index: int = 0, period_s: float = 0.005):
         self.index = index
-        self.samples = []
+        self.period = period_s
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+    def _run_nvml(self, nv):
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
+                                 nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            self._stop.wait(self.period)
+
+    def _run_smi(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                f = [x.strip() for x in out.split(",")]
+                self.samples.append((float(f[0]), float(f[1]), int(f[2], 16)))
             except Exception:
                 pass
             self._stop.wait(0.2)
 
+    def _run(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+        except Exception:
+            return self._run_smi()
+        try:
+            self._run_nvml(nv)
+        finally:
+            nv.nvmlShutdown()
+
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.02)
         return self
 
     def __exit__(self, *a):
@@ -80,12 +107,12 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = sorted(s[0] for s in self.samples)
+        mask = 0
+        for s in self.samples:
+            mask |= int(s[2])
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": [n for n, bit in self.REASONS if mask & bit], "samples": len(self.samples)}
 
 
 def dist_setup(n):
@@ -272,10 +299,17 @@ def main():
     g_ms, g_flops, g_launch = net.gemm_profile(iters=5, stream=stream)
     achieved = g_flops / (g_ms / 1000.0) / 1e12
     peak = peaks.get("bf16_tflops", 1590.0)
+    # per-launch roofline: many ResNet-50 convs at batch 32 are HBM-bound, so
+    # the honest bound of the family is sum_i max(flops_i / tensor peak,
+    # bytes_i / HBM peak) over the step's GEMM launches
+    rows = net.gemm_profile_detail(iters=1, stream=stream)
+    roof_ms = sum(max(r["flops"] / (peak * 1e12), r["bytes"] / (peaks.get("hbm_gbs", 6650.0) * 1e9))
+                  for r in rows) * 1e3
+    alg_bytes = sum(r["bytes"] for r in rows)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            traffic = json.load(f).get("dram_bytes_per_step")
     except Exception:
         pass
 
@@ -326,6 +360,9 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "gemm_kernel (tcgen05 implicit-GEMM conv fprop/dgrad/wgrad + fc)",
                          "gemm_ms_per_step": g_ms, "gemm_share_of_step": g_ms / ms, "gemm_launches": g_launch,
+                         "algorithmic_bytes_per_step": alg_bytes,
+                         "traffic_note": "ncu dram read+write bytes of the step's GEMM launches (profiles/ncu_gemm_summary.json)",
+                         "roofline_ms_per_step": roof_ms, "frac_of_roofline_time": roof_ms / g_ms,
                          "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst)"},
             "cpu_baseline": cpu,
             "gpu_launches": launches * args.steps,

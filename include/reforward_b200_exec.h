@@ -132,9 +132,15 @@ int rfx_net_read_loss(rfx_net* net, float* loss, void* stream);
  * algorithmic flops per step, number of GEMM launches */
 int rfx_net_gemm_profile(rfx_net* net, int32_t iters, void* stream, double* ms_per_step,
                          double* flops_per_step, int64_t* launches);
-/* per GEMM launch of the step: 8 doubles {M, N, K, a_kind, b_kind, splits, ms, flops} */
+/* per GEMM launch of the step: 10 doubles {M, N, K, a_kind, b_kind, splits, ms, flops,
+ * algorithmic bytes, tile width BLOCK_N} */
 int rfx_net_gemm_profile_detail(rfx_net* net, int32_t iters, void* stream, double* rows, int32_t cap,
                                 int32_t* n_out);
+
+/* in-stream ms of every schedule instruction (eager launches, events between
+ * them, mean over iters) and of the SGD update last: |schedule| + 1 doubles.
+ * Runs forward/backward for real; the update uses lr 0. */
+int rfx_net_instr_profile(rfx_net* net, int32_t iters, void* stream, double* ms, int32_t cap, int32_t* n_out);
 
 int32_t rfx_net_num_params(const rfx_net* net);
 int rfx_net_param_info(const rfx_net* net, int32_t i, char* name, size_t name_cap, int32_t* shape,

@@ -246,7 +246,17 @@ int rfx_net_gemm_profile_detail(rfx_net* n, int32_t iters, void* st, double* row
     if (!rows) return;
     if (cap < (int32_t)r.size()) throw std::invalid_argument("buffer too small");
     for (size_t i = 0; i < r.size(); ++i)
-      for (int j = 0; j < 8; ++j) rows[i * 8 + j] = r[i][j];
+      for (int j = 0; j < 10; ++j) rows[i * 10 + j] = r[i][j];
+  });
+}
+
+int rfx_net_instr_profile(rfx_net* n, int32_t iters, void* st, double* ms, int32_t cap, int32_t* n_out) {
+  return guard([&] {
+    auto r = n->net->instr_profile(iters < 1 ? 1 : iters, S(st));
+    *n_out = (int32_t)r.size();
+    if (!ms) return;
+    if (cap < (int32_t)r.size()) throw std::invalid_argument("buffer too small");
+    for (size_t i = 0; i < r.size(); ++i) ms[i] = r[i];
   });
 }
 

@@ -158,7 +158,10 @@ class Net {
   void gemm_profile(int iters, cudaStream_t st, double* ms_per_step, double* flops_per_step, long* launches);
   // per-launch timing of the step's GEMMs (events between eager launches):
   // rows of {M, N, K, a_kind, b_kind, splits, ms, flops}
-  std::vector<std::array<double, 8>> gemm_profile_detail(int iters, cudaStream_t st);
+  std::vector<std::array<double, 10>> gemm_profile_detail(int iters, cudaStream_t st);
+  // in-stream time of every schedule instruction (events between eager
+  // launches, averaged over iters) followed by the SGD update: size = |schedule| + 1
+  std::vector<double> instr_profile(int iters, cudaStream_t st);
 
   // parameter access in canonical layout (host fp32)
   int num_params() const { return (int)params_.size(); }
@@ -271,6 +274,7 @@ class Net {
   struct GemmRecord {
     rfk::GemmDesc desc;
     double flops;
+    double bytes;  // algorithmic HBM bytes: operands read once + output written (read too when accumulating)
   };
   bool tracing_ = false;
   double trace_flops_ = 0;  // algorithmic flops to attach to the next traced GEMM

@@ -221,8 +221,28 @@ __nv_bfloat16* Net::gptr(int t) const {
   return reinterpret_cast<__nv_bfloat16*>(d_grad_arena_ + grad_slot_[t]);
 }
 
+// Algorithmic HBM bytes of one GEMM: each operand tensor read once (an im2col
+// operand is its activation tensor, not the expanded matrix), the output
+// written once (and read once more when accumulating).  Split-K partials are
+// implementation traffic and are not counted.
+static double gemm_algorithmic_bytes(const rfk::GemmDesc& d) {
+  auto tensor = [](const rfk::ConvGeom& g) { return 2.0 * g.N * g.H * g.W * g.C; };
+  double a = 0, b = 0;
+  switch (d.a_kind) {
+    case rfk::Operand::Im2colK: a = tensor(d.a_geom); break;
+    default: a = 2.0 * d.M * d.K;
+  }
+  switch (d.b_kind) {
+    case rfk::Operand::Im2colMN: b = tensor(d.b_geom); break;
+    case rfk::Operand::WeightTapsMN: b = 2.0 * d.b_rows * d.b_taps * (d.b_extent > 0 ? d.b_extent : d.N); break;
+    default: b = 2.0 * (double)d.N * d.K;
+  }
+  const double c = (d.out_f32 ? 4.0 : 2.0) * d.M * d.N * (d.accumulate_out ? 2 : 1);
+  return a + b + c;
+}
+
 void Net::gemm(const rfk::GemmDesc& d, cudaStream_t st) {
-  if (tracing_) gemm_trace_.push_back({d, trace_flops_});
+  if (tracing_) gemm_trace_.push_back({d, trace_flops_, gemm_algorithmic_bytes(d)});
   check(rfk::gemm_launch(d, st), "gemm");
 }
 
@@ -768,7 +788,7 @@ void Net::step(float lr, float momentum, float wd, cudaStream_t st, bool use_gra
   run_phase(2, lr, momentum, wd, st, use_graph);
 }
 
-std::vector<std::array<double, 8>> Net::gemm_profile_detail(int iters, cudaStream_t st) {
+std::vector<std::array<double, 10>> Net::gemm_profile_detail(int iters, cudaStream_t st) {
   double a, b;
   long c;
   if (gemm_trace_.empty()) gemm_profile(1, st, &a, &b, &c);
@@ -790,11 +810,12 @@ std::vector<std::array<double, 8>> Net::gemm_profile_detail(int iters, cudaStrea
     }
   }
   for (auto e : ev) cudaEventDestroy(e);
-  std::vector<std::array<double, 8>> out;
+  std::vector<std::array<double, 10>> out;
   for (size_t i = 0; i < gemm_trace_.size(); ++i) {
     const auto& d = gemm_trace_[i].desc;
     out.push_back({(double)d.M, (double)d.N, (double)d.K, (double)(int)d.a_kind, (double)(int)d.b_kind,
-                   (double)d.splits, ms[i], gemm_trace_[i].flops});
+                   (double)d.splits, ms[i], gemm_trace_[i].flops, gemm_trace_[i].bytes,
+                   (double)rfk::gemm_block_n(d)});
   }
   return out;
 }
@@ -834,6 +855,32 @@ void Net::gemm_profile(int iters, cudaStream_t st, double* ms_per_step, double* 
   *ms_per_step = ms / iters;
   *flops_per_step = flops;
   *launches = (long)gemm_trace_.size();
+}
+
+std::vector<double> Net::instr_profile(int iters, cudaStream_t st) {
+  if (!setup_done_) throw std::invalid_argument("setup the network first");
+  const size_t n = sched_.size();
+  std::vector<cudaEvent_t> ev(n + 2);
+  for (auto& e : ev) check(cudaEventCreate(&e), "event");
+  std::vector<double> ms(n + 1, 0.0);
+  for (int it = 0; it < iters + 1; ++it) {
+    check(cudaEventRecord(ev[0], st), "event");
+    for (size_t k = 0; k < n; ++k) {
+      run_instr(sched_[k], st);
+      check(cudaEventRecord(ev[k + 1], st), "event");
+    }
+    update(0.f, 0.f, 0.f, st);  // lr 0: parameters unchanged
+    check(cudaEventRecord(ev[n + 1], st), "event");
+    check(cudaEventSynchronize(ev[n + 1]), "sync");
+    if (it == 0) continue;  // warm-up
+    for (size_t k = 0; k <= n; ++k) {
+      float t = 0;
+      cudaEventElapsedTime(&t, ev[k], ev[k + 1]);
+      ms[k] += t / iters;
+    }
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  return ms;
 }
 
 float Net::read_loss(cudaStream_t st) {

@@ -552,10 +552,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, cudaStr
 
 int gemm_m_tiles(const GemmDesc& d) { return (d.M + kBlockM - 1) / kBlockM; }
 
-cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
-  load_driver_entry_points();
-  if (!g_encode_tiled || !g_encode_im2col) return cudaErrorNotSupported;
-  if (d.M <= 0 || d.N <= 0) return cudaSuccess;
+int gemm_block_n(const GemmDesc& d) {
   int bn = d.block_n;
   if (bn == 0) {
     // pick the tile width that minimises (tiles per SM, rounded up) x width:
@@ -575,6 +572,14 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   }
   if (d.b_kind == Operand::MNMajor2D || d.b_kind == Operand::Im2colMN || d.b_kind == Operand::WeightTapsMN)
     bn = bn < 64 ? 64 : bn;
+  return bn;
+}
+
+cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
+  load_driver_entry_points();
+  if (!g_encode_tiled || !g_encode_im2col) return cudaErrorNotSupported;
+  if (d.M <= 0 || d.N <= 0) return cudaSuccess;
+  const int bn = gemm_block_n(d);
   if (bn != 64 && bn != 128 && bn != 256) return cudaErrorInvalidValue;
   if (d.stats && d.out_f32) return cudaErrorInvalidValue;  // statistics are of the stored bf16 values
 

@@ -61,5 +61,6 @@ struct GemmDesc {
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream);
 int gemm_m_tiles(const GemmDesc& d);
+int gemm_block_n(const GemmDesc& d);  // tile width the launch will use
 
 }  // namespace rfk

@@ -225,12 +225,17 @@ __global__ void __launch_bounds__(kThreads) bn_apply_kernel(const __nv_bfloat16*
   }
 }
 
-// Backward reduction: g = dout * mask, accumulate sum(g) and sum(g * xhat).
-// mask mode: 0 none, 1 relu of (y*scale+shift), 2 relu of stored output (out>0)
-__global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(
+// Backward reduction: g = dout * mask, accumulate sum(g) and sum(g * (y - mean))
+// (the finalize scales the second sum by invstd, so the inner loop carries
+// only the mean).  MODE: 0 no mask, 1 relu recomputed from y*scale+shift
+// (same expression as the forward), 2 relu of the stored output (out > 0).
+// Two rows per thread in flight and <= 85 registers (3 blocks of 256 per SM)
+// keep enough loads outstanding for HBM.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 3) bn_bwd_reduce_kernel(
     const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
-    int mask_mode, const float* __restrict__ mean, const float* __restrict__ invstd, const float* __restrict__ scale,
-    const float* __restrict__ shift, long M, int C, long rows_per_block, float* __restrict__ partials) {
+    const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ shift, long M, int C,
+    long rows_per_block, float* __restrict__ partials) {
   __shared__ float sh[2][kThreads][8];
   const int cchunk = blockIdx.y;
   const int Cc = min(2048, C - cchunk * 2048);
@@ -238,36 +243,45 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(
   const int t = threadIdx.x;
   const int lane = t % s.tpr, rgrp = t / s.tpr;
   const int c0 = cchunk * 2048 + lane * 8;
-  float a[8], b[8], mu[8], is[8], sc[8], sf[8];
+  float a[8], b[8], mu[8], sc[8], sf[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    a[i] = b[i] = 0.f;
-    if (rgrp < s.rows_per_pass) {
-      mu[i] = mean[c0 + i];
-      is[i] = invstd[c0 + i];
-      sc[i] = scale[c0 + i];
-      sf[i] = shift[c0 + i];
-    }
-  }
+  for (int i = 0; i < 8; ++i) a[i] = b[i] = 0.f;
   const long r0 = (long)blockIdx.x * rows_per_block;
   const long r1 = min(M, r0 + rows_per_block);
   if (rgrp < s.rows_per_pass) {
-    for (long r = r0 + rgrp; r < r1; r += s.rows_per_pass) {
-      const long off = r * C + c0;
-      float fy[8], fd[8], fo[8];
-      const uint4 uy = ldg16(y + off), ud = ldg16(dout + off);
-      uint4 uo = make_uint4(0, 0, 0, 0);
-      if (mask_mode == 2) uo = ldg16(out + off);
-      unpack8(uy, fy);
-      unpack8(ud, fd);
-      if (mask_mode == 2) unpack8(uo, fo);
+    ld8f(mean + c0, mu);
+    if (MODE == 1) {
+      ld8f(scale + c0, sc);
+      ld8f(shift + c0, sf);
+    }
+    const long step = s.rows_per_pass;
+    for (long r = r0 + rgrp; r < r1; r += 2 * step) {
+      const bool two = r + step < r1;
+      const long off0 = r * C + c0, off1 = (r + step) * C + c0;
+      uint4 uy[2], ud[2], uo[2];
+      uy[0] = ldg16(y + off0);
+      ud[0] = ldg16(dout + off0);
+      if (MODE == 2) uo[0] = ldg16(out + off0);
+      if (two) {
+        uy[1] = ldg16(y + off1);
+        ud[1] = ldg16(dout + off1);
+        if (MODE == 2) uo[1] = ldg16(out + off1);
+      }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float g = fd[i];
-        if (mask_mode == 1) g = (fmaf(fy[i], sc[i], sf[i]) > 0.f) ? g : 0.f;  // same expression as the forward
-        if (mask_mode == 2) g = (fo[i] > 0.f) ? g : 0.f;
-        a[i] += g;
-        b[i] += g * (fy[i] - mu[i]) * is[i];
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && !two) break;
+        float fy[8], fd[8], fo[8];
+        unpack8(uy[u], fy);
+        unpack8(ud[u], fd);
+        if (MODE == 2) unpack8(uo[u], fo);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float g = fd[i];
+          if (MODE == 1) g = (fmaf(fy[i], sc[i], sf[i]) > 0.f) ? g : 0.f;
+          if (MODE == 2) g = (fo[i] > 0.f) ? g : 0.f;
+          a[i] += g;
+          b[i] = fmaf(g, fy[i] - mu[i], b[i]);
+        }
       }
     }
   }
@@ -293,18 +307,19 @@ __global__ void __launch_bounds__(kThreads) bn_bwd_reduce_kernel(
   }
 }
 
-// dbeta = sum g, dgamma = sum g*xhat; dy = k1*g + k2*y + k3
+// dbeta = sum g, dgamma = invstd * sum g*(y-mean); dy = k1*g + k2*y + k3
 __global__ void bn_bwd_finalize_kernel(const float* __restrict__ partials, int parts, int C, float count,
                                        const float* __restrict__ gamma, const float* __restrict__ mean,
                                        const float* __restrict__ invstd, float* __restrict__ dgamma,
                                        float* __restrict__ dbeta, float* __restrict__ coef) {
   const int c = blockIdx.x * 32 + threadIdx.x;
-  float sg, sgx;
-  sum_partials(partials, parts, C, c, sg, sgx);
+  float sg, sgy;
+  sum_partials(partials, parts, C, c, sg, sgy);
   if (threadIdx.y != 0 || c >= C) return;
+  const float is = invstd[c];
+  const float sgx = sgy * is;
   dbeta[c] = sg;
   dgamma[c] = sgx;
-  const float is = invstd[c];
   const float k1 = gamma[c] * is;
   const float k2 = -k1 * is * sgx / count;
   const float k3 = -k1 * sg / count - k2 * mean[c];
@@ -313,51 +328,76 @@ __global__ void bn_bwd_finalize_kernel(const float* __restrict__ partials, int p
   coef[2 * C + c] = k3;
 }
 
-__global__ void __launch_bounds__(kThreads) bn_bwd_apply_kernel(
+// dy (+)= k1*g + k2*y + k3 with g = dout * mask; dskip (+)= g (residual add).
+// Two vectors per thread in flight; <= 64 registers.
+template <int MODE, bool SKIP>
+__global__ void __launch_bounds__(kThreads, 4) bn_bwd_apply_kernel(
     const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
-    int mask_mode, const float* __restrict__ scale, const float* __restrict__ shift, const float* __restrict__ coef,
-    long nvec, int C, __nv_bfloat16* __restrict__ dy, int acc_dy, __nv_bfloat16* __restrict__ dskip, int acc_dskip) {
-  const int cv = C / 8;
-  for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
-    const int c0 = (int)(v % cv) * 8;
-    const long off = v * 8;
-    float fy[8], fd[8], fo[8], r[8], sk[8], k1[8], k2[8], k3[8], sc[8], sh[8];
-    const uint4 uy = ldg16(y + off), ud = ldg16(dout + off);
-    uint4 uo = make_uint4(0, 0, 0, 0);
-    if (mask_mode == 2) uo = ldg16(out + off);
-    unpack8(uy, fy);
-    unpack8(ud, fd);
-    if (mask_mode == 2) unpack8(uo, fo);
-    ld8f(coef + c0, k1);
-    ld8f(coef + C + c0, k2);
-    ld8f(coef + 2 * C + c0, k3);
-    if (mask_mode == 1) {
-      ld8f(scale + c0, sc);
-      ld8f(shift + c0, sh);
-    }
+    const float* __restrict__ scale, const float* __restrict__ shift, const float* __restrict__ coef, unsigned nvec,
+    int C, __nv_bfloat16* __restrict__ dy, int acc_dy, __nv_bfloat16* __restrict__ dskip, int acc_dskip) {
+  const unsigned cv = (unsigned)C / 8;
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += 2 * stride) {
+    uint4 uy[2], ud[2], uo[2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float g = fd[i];
-      if (mask_mode == 1) g = (fmaf(fy[i], sc[i], sh[i]) > 0.f) ? g : 0.f;  // same expression as the forward
-      if (mask_mode == 2) g = (fo[i] > 0.f) ? g : 0.f;
-      sk[i] = g;
-      r[i] = k1[i] * g + k2[i] * fy[i] + k3[i];
-    }
-    if (acc_dy) {
-      float prev[8];
-      unpack8(*reinterpret_cast<const uint4*>(dy + off), prev);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) r[i] += prev[i];
-    }
-    *reinterpret_cast<uint4*>(dy + off) = pack8(r);
-    if (dskip) {
-      if (acc_dskip) {
-        float prev[8];
-        unpack8(*reinterpret_cast<const uint4*>(dskip + off), prev);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sk[i] += prev[i];
+    for (int u = 0; u < 2; ++u) {
+      const unsigned v = v0 + u * stride;
+      if (v < nvec) {
+        uy[u] = ldg16(y + (size_t)v * 8);
+        ud[u] = ldg16(dout + (size_t)v * 8);
+        if (MODE == 2) uo[u] = ldg16(out + (size_t)v * 8);
       }
-      *reinterpret_cast<uint4*>(dskip + off) = pack8(sk);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const unsigned v = v0 + u * stride;
+      if (v >= nvec) break;
+      const int c0 = (int)(v % cv) * 8;
+      const size_t off = (size_t)v * 8;
+      float fy[8], fd[8], r[8];
+      unpack8(uy[u], fy);
+      unpack8(ud[u], fd);
+      if (MODE == 2) {
+        float fo[8];
+        unpack8(uo[u], fo);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) fd[i] = fo[i] > 0.f ? fd[i] : 0.f;
+      }
+      if (MODE == 1) {
+        float sc[8], sh[8];
+        ld8f(scale + c0, sc);
+        ld8f(shift + c0, sh);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) fd[i] = (fmaf(fy[i], sc[i], sh[i]) > 0.f) ? fd[i] : 0.f;
+      }
+      {
+        float k[8];
+        ld8f(coef + c0, k);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = k[i] * fd[i];
+        ld8f(coef + C + c0, k);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] += k[i] * fy[i];
+        ld8f(coef + 2 * C + c0, k);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] += k[i];
+      }
+      if (acc_dy) {
+        float prev[8];
+        unpack8(*reinterpret_cast<const uint4*>(dy + off), prev);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] += prev[i];
+      }
+      *reinterpret_cast<uint4*>(dy + off) = pack8(r);
+      if (SKIP) {
+        if (acc_dskip) {
+          float prev[8];
+          unpack8(*reinterpret_cast<const uint4*>(dskip + off), prev);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) fd[i] += prev[i];
+        }
+        *reinterpret_cast<uint4*>(dskip + off) = pack8(fd);
+      }
     }
   }
 }
@@ -975,9 +1015,9 @@ long rows_per_block_for(long M, int blocks) { return (M + blocks - 1) / blocks; 
 
 // ============================================================ launchers
 int colstats_blocks(long M) {
-  // enough blocks to fill the chip, each with >= 64 rows
+  // one full wave (3 resident blocks per SM), each with >= 64 rows
   long b = (M + 63) / 64;
-  if (b > 148 * 4) b = 148 * 4;
+  if (b > 148 * 3) b = 148 * 3;
   return (int)(b < 1 ? 1 : b);
 }
 
@@ -1009,16 +1049,37 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
                         const float* shift, long M, int C, float* partials, int blocks, float* coef, float* dgamma,
                         float* dbeta, __nv_bfloat16* dy, bool acc_dy, __nv_bfloat16* dskip, bool acc_dskip,
                         cudaStream_t st) {
-  if (C % 8 || (C > 2048 && C % 2048)) return cudaErrorInvalidValue;
+  if (C % 8 || (C > 2048 && C % 2048) || mask_mode < 0 || mask_mode > 2) return cudaErrorInvalidValue;
+  const long nvec = M * C / 8;
+  if (nvec >= (1L << 31)) return cudaErrorInvalidValue;
   dim3 grid(blocks, (C + 2047) / 2048);
-  bn_bwd_reduce_kernel<<<grid, kThreads, 0, st>>>(y, dout, out, mask_mode, mean, invstd, scale, shift, M, C,
-                                                  rows_per_block_for(M, blocks), partials);
+  const long rpb = rows_per_block_for(M, blocks);
+  switch (mask_mode) {
+    case 0: bn_bwd_reduce_kernel<0><<<grid, kThreads, 0, st>>>(y, dout, out, mean, scale, shift, M, C, rpb, partials); break;
+    case 1: bn_bwd_reduce_kernel<1><<<grid, kThreads, 0, st>>>(y, dout, out, mean, scale, shift, M, C, rpb, partials); break;
+    default: bn_bwd_reduce_kernel<2><<<grid, kThreads, 0, st>>>(y, dout, out, mean, scale, shift, M, C, rpb, partials);
+  }
   bn_bwd_finalize_kernel<<<(C + 31) / 32, dim3(32, kFinY), 0, st>>>(partials, blocks, C, (float)M, gamma, mean, invstd,
                                                                 dgamma, dbeta, coef);
-  const long nvec = M * C / 8;
-  bn_bwd_apply_kernel<<<grid_for(nvec, kThreads * 4), kThreads, 0, st>>>(y, dout, out, mask_mode, scale, shift, coef,
-                                                                         nvec, C, dy, acc_dy ? 1 : 0, dskip,
-                                                                         acc_dskip ? 1 : 0);
+  const int g = grid_for(nvec, kThreads * 2, 148 * 4);  // one wave at 4 blocks per SM
+  const unsigned nv = (unsigned)nvec;
+  const int ad = acc_dy ? 1 : 0, as = acc_dskip ? 1 : 0;
+#define RF_BWD_APPLY(MODE, SKIP) \
+  bn_bwd_apply_kernel<MODE, SKIP><<<g, kThreads, 0, st>>>(y, dout, out, scale, shift, coef, nv, C, dy, ad, dskip, as)
+  if (dskip) {
+    switch (mask_mode) {
+      case 0: RF_BWD_APPLY(0, true); break;
+      case 1: RF_BWD_APPLY(1, true); break;
+      default: RF_BWD_APPLY(2, true);
+    }
+  } else {
+    switch (mask_mode) {
+      case 0: RF_BWD_APPLY(0, false); break;
+      case 1: RF_BWD_APPLY(1, false); break;
+      default: RF_BWD_APPLY(2, false);
+    }
+  }
+#undef RF_BWD_APPLY
   return cudaGetLastError();
 }
 

@@ -70,6 +70,8 @@ _SIGS = {
     "rfx_net_update": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_void_p]),
     "rfx_net_step": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_int32, C.c_void_p]),
     "rfx_net_read_loss": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_void_p]),
+    "rfx_net_instr_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int32,
+                                        C.POINTER(C.c_int32)]),
     "rfx_net_gemm_profile_detail": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int32,
                                               C.POINTER(C.c_int32)]),
     "rfx_net_run_phase": (C.c_int, [C.c_void_p, C.c_int32, C.c_float, C.c_float, C.c_float, C.c_int32,
@@ -330,10 +332,18 @@ class ReforwardNet:
         """Per-launch timing of the step's GEMMs (CUDA events between eager launches)."""
         n = C.c_int32()
         _check(self.L.rfx_net_gemm_profile_detail(self.h, iters, _stream(stream), None, 0, C.byref(n)))
-        buf = (C.c_double * (8 * max(n.value, 1)))()
+        buf = (C.c_double * (10 * max(n.value, 1)))()
         _check(self.L.rfx_net_gemm_profile_detail(self.h, iters, _stream(stream), buf, n.value, C.byref(n)))
-        keys = ("M", "N", "K", "a_kind", "b_kind", "splits", "ms", "flops")
-        return [dict(zip(keys, buf[8 * i: 8 * i + 8])) for i in range(n.value)]
+        keys = ("M", "N", "K", "a_kind", "b_kind", "splits", "ms", "flops", "bytes", "block_n")
+        return [dict(zip(keys, buf[10 * i: 10 * i + 10])) for i in range(n.value)]
+
+    def instr_profile(self, iters: int = 3, stream=None) -> List[float]:
+        """In-stream ms of each schedule instruction, then of the SGD update (last entry)."""
+        n = C.c_int32()
+        _check(self.L.rfx_net_instr_profile(self.h, iters, _stream(stream), None, 0, C.byref(n)))
+        buf = (C.c_double * max(n.value, 1))()
+        _check(self.L.rfx_net_instr_profile(self.h, iters, _stream(stream), buf, n.value, C.byref(n)))
+        return list(buf[:n.value])
 
     def read_loss(self, stream=None) -> float:
         v = C.c_float()

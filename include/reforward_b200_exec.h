@@ -142,6 +142,11 @@ int rfx_net_gemm_profile_detail(rfx_net* net, int32_t iters, void* stream, doubl
  * Runs forward/backward for real; the update uses lr 0. */
 int rfx_net_instr_profile(rfx_net* net, int32_t iters, void* stream, double* ms, int32_t cap, int32_t* n_out);
 
+/* tuning probe: ms of traced GEMM `idx` re-launched with a forced tile width
+ * (64/128/256) and split-K count, writing fp32 partials to a scratch buffer */
+int rfx_net_gemm_try(rfx_net* net, int32_t idx, int32_t block_n, int32_t splits, int32_t iters, void* stream,
+                     double* ms);
+
 int32_t rfx_net_num_params(const rfx_net* net);
 int rfx_net_param_info(const rfx_net* net, int32_t i, char* name, size_t name_cap, int32_t* shape,
                        int32_t* ndim, int32_t* kind, int64_t* count);

@@ -260,6 +260,10 @@ int rfx_net_instr_profile(rfx_net* n, int32_t iters, void* st, double* ms, int32
   });
 }
 
+int rfx_net_gemm_try(rfx_net* n, int32_t idx, int32_t block_n, int32_t splits, int32_t iters, void* st, double* ms) {
+  return guard([&] { *ms = n->net->gemm_try(idx, block_n, splits, iters < 1 ? 1 : iters, S(st)); });
+}
+
 int rfx_net_gemm_profile(rfx_net* n, int32_t iters, void* st, double* ms, double* flops, int64_t* launches) {
   return guard([&] {
     long l = 0;

@@ -162,6 +162,10 @@ class Net {
   // in-stream time of every schedule instruction (events between eager
   // launches, averaged over iters) followed by the SGD update: size = |schedule| + 1
   std::vector<double> instr_profile(int iters, cudaStream_t st);
+  // tuning probe: re-time traced GEMM `idx` with a forced tile width and
+  // split count (fp32 partials into a scratch buffer; the step's buffers are
+  // not written)
+  double gemm_try(int idx, int block_n, int splits, int iters, cudaStream_t st);
 
   // parameter access in canonical layout (host fp32)
   int num_params() const { return (int)params_.size(); }

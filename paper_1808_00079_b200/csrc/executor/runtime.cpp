@@ -857,6 +857,42 @@ void Net::gemm_profile(int iters, cudaStream_t st, double* ms_per_step, double* 
   *launches = (long)gemm_trace_.size();
 }
 
+double Net::gemm_try(int idx, int block_n, int splits, int iters, cudaStream_t st) {
+  if (gemm_trace_.empty()) {
+    double a, b;
+    long c;
+    gemm_profile(1, st, &a, &b, &c);
+  }
+  if (idx < 0 || idx >= (int)gemm_trace_.size()) throw std::invalid_argument("gemm index out of range");
+  rfk::GemmDesc d = gemm_trace_[idx].desc;
+  d.block_n = block_n;
+  d.splits = splits < 1 ? 1 : splits;
+  d.stats = nullptr;
+  d.bias = nullptr;
+  d.remap = false;
+  d.accumulate_out = false;
+  d.out_f32 = true;
+  d.ldc = d.N;
+  d.split_stride = (long)d.M * d.N;
+  void* scratch = nullptr;
+  check(cudaMalloc(&scratch, (size_t)d.splits * d.M * d.N * 4), "scratch");
+  d.out = scratch;
+  cudaEvent_t e0, e1;
+  check(cudaEventCreate(&e0), "event");
+  check(cudaEventCreate(&e1), "event");
+  for (int i = 0; i < 2; ++i) check(rfk::gemm_launch(d, st), "gemm");
+  check(cudaEventRecord(e0, st), "event");
+  for (int i = 0; i < iters; ++i) check(rfk::gemm_launch(d, st), "gemm");
+  check(cudaEventRecord(e1, st), "event");
+  check(cudaEventSynchronize(e1), "sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(scratch);
+  return ms / iters;
+}
+
 std::vector<double> Net::instr_profile(int iters, cudaStream_t st) {
   if (!setup_done_) throw std::invalid_argument("setup the network first");
   const size_t n = sched_.size();

@@ -2,8 +2,9 @@
 //
 //   warp 0      TMA producer (one elected lane): A and B tiles -> smem ring
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  epilogue: TMEM -> registers -> global, optional fused
-//               per-column statistics (BatchNorm sum / sum of squares)
+//   warps 2..9  epilogue: TMEM -> registers -> global, optional fused
+//               per-column statistics (BatchNorm sum / sum of squares);
+//               two warps per TMEM lane quarter, alternating 32-column chunks
 //
 // Tiles: BLOCK_M = 128 output rows, BLOCK_N in {64, 128, 256}, BLOCK_K = 64
 // (one 128-byte swizzle row of bf16).  Operands are staged with TMA in
@@ -26,9 +27,9 @@ namespace {
 
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kTileA = kBlockM * kBlockK * 2;  // 16 KB
-constexpr int kStaging = 4 * 2 * 2048;          // epilogue: 4 warps x 2 buffers x (32 rows x 64 B)
 
 struct alignas(64) KParams {
   CUtensorMap ta;  // 64-byte aligned, must be first
@@ -58,9 +59,15 @@ template <int BN>
 struct Cfg {
   static constexpr int kTileB = BN * kBlockK * 2;
   static constexpr int kStage = kTileA + kTileB;
-  static constexpr int kStages = (BN == 64) ? 8 : (BN == 128 ? 6 : 4);  // ~190 KB ring
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
-  static constexpr int kStats = 4 * 2 * BN * 4;  // per-warp column sums
+  // epilogue staging: per warp, 1 or 2 buffers of one 32-row x 64-byte box
+  static constexpr int kStgBufs = BN == 256 ? 1 : 2;
+  static constexpr int kStaging = kEpiWarps * kStgBufs * 2048;
+  static constexpr int kStats = kEpiWarps * 2 * (BN / 2) * 4;  // per-warp sums of the warp's own columns
+  // as deep a TMA ring as the 227 KB of dynamic shared memory allows
+  static constexpr int kSmemMax = 232448;
+  static constexpr int kStages = (kSmemMax - kStaging - kStats - 1024 - 256) / kStage;
+  static_assert(kStages >= 3, "ring too shallow");
   static constexpr int kSmem = kStages * kStage + kStaging + kStats + 1024 /*align*/ + 256;
 };
 
@@ -96,9 +103,10 @@ __device__ __forceinline__ TileCoord tile_coord(const KParams& p, int t, int BN)
 
 // Stage one 32-row x 64-byte box (lane = row) in 64B-swizzled smem and hand
 // it to the TMA unit; the buffer was last used two boxes ago.
+template <int NBUF>
 __device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const uint32_t (&w)[16], uint32_t lane,
                                             int mode, int cx, int my, int z) {
-  if (lane == 0) bulk_wait_read<1>();
+  if (lane == 0) bulk_wait_read<NBUF - 1>();
   __syncwarp();
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -120,10 +128,13 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the shared array itself, so
+  // every derived pointer keeps the shared address space (LDS/STS, not
+  // generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nst = p.stages;
   uint8_t* stage_buf = smem + nst * C::kStage;  // epilogue staging, then the column sums
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + kStaging + C::kStats);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + C::kStaging + C::kStats);
   uint64_t* empty = full + nst;
   uint64_t* acc_full = empty + nst;   // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2; // [2] epilogue -> MMA
@@ -142,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&acc_empty[a], kEpiWarps);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -262,41 +273,48 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------ epilogue (warps 2..9)
     // TMEM -> registers (32 columns at a time) -> [bias] -> [column statistics]
     // -> 64-byte-swizzled smem staging -> TMA store / TMA reduce-add of a
-    // 32-row box.  Two staging buffers per warp let the next chunk be staged
-    // while the previous box is still being read out by the TMA unit.
+    // 32-row box.  Warp w reads TMEM lanes 32 * (w % 4) (the hardware's lane
+    // quarter rule); the two warps of a quarter take alternating 32-column
+    // chunks, so eight warps drain an accumulator in parallel.
     const uint32_t quarter = warp & 3;
+    const uint32_t half = (warp - 2) >> 2;
+    const uint32_t ew = warp - 2;  // epilogue warp index 0..7
     const uint32_t lane = lane_id();
-    uint8_t* stg = stage_buf + quarter * 4096;
+    constexpr int NB = C::kStgBufs;
+    uint8_t* stg = stage_buf + ew * (NB * 2048);
     // Fused BN statistics: each warp keeps its own per-column sums in smem
-    // (lane l owns column c0 + l, so no synchronisation per chunk); when the
-    // CTA moves to another column block the four warps' sums are combined in
-    // a fixed order and written once as this CTA's row of stats[gridDim][2][N].
-    // The finalize then sums ~148 rows instead of one per M tile.  Rows of
-    // column blocks a CTA never touches stay zero (workspace zeroed once; the
-    // tile -> CTA mapping is the same every launch).
-    float* wsum = reinterpret_cast<float*>(stage_buf + kStaging);  // [4 warps][2][BN]
-    float* my_sum = wsum + quarter * 2 * BN;
+    // for the columns it owns (lane l owns column pair 2 (l & 15) of a chunk,
+    // so no synchronisation per chunk); when the CTA moves to another column
+    // block the eight warps' sums are combined in a fixed order and written
+    // once as this CTA's row of stats[gridDim][2][N].  The finalize then sums
+    // ~148 rows instead of one per M tile.  Rows of column blocks a CTA never
+    // touches stay zero (workspace zeroed once; the tile -> CTA mapping is the
+    // same every launch).
+    constexpr int HB = BN / 2;  // columns owned by one warp
+    float* wsum = reinterpret_cast<float*>(stage_buf + C::kStaging);  // [8 warps][2][HB]
+    float* my_sum = wsum + ew * 2 * HB;
     const int mode = p.out_mode;
     int buf = 0;
     auto tma_out = [&](const uint32_t(&w)[16], int cx, int my, int z) {
-      epi_tma_out(p, stg + buf * 2048, w, lane, mode, cx, my, z);
-      buf ^= 1;
+      epi_tma_out<NB>(p, stg + buf * 2048, w, lane, mode, cx, my, z);
+      if (NB == 2) buf ^= 1;
     };
     int cur_nt = -1;
     auto flush_stats = [&](int nt) {
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       float* row = p.stats + (long)blockIdx.x * 2 * p.N;
-      for (int c = (int)(quarter * 32 + lane); c < BN; c += 128) {
+      for (int c = (int)(ew * 32 + lane); c < BN; c += 256) {
+        const int j = c >> 5, h = j & 1, lc = ((j >> 1) << 5) + (c & 31);
         float s = 0.f, q = 0.f;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          s += wsum[(2 * w) * BN + c];
-          q += wsum[(2 * w + 1) * BN + c];
-          wsum[(2 * w) * BN + c] = 0.f;
-          wsum[(2 * w + 1) * BN + c] = 0.f;
+        for (int qq = 0; qq < 4; ++qq) {
+          // warp of (half h, quarter qq): ew = 4 h + ((qq + 2) & 3)
+          float* ws = wsum + (4 * h + ((qq + 2) & 3)) * 2 * HB;
+          s += ws[lc];
+          q += ws[HB + lc];
         }
         const int col = nt * BN + c;
         if (col < p.N) {
@@ -304,10 +322,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           row[p.N + col] = q;
         }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      for (int c = (int)lane; c < 2 * HB; c += 32) my_sum[c] = 0.f;
+      __syncwarp();
     };
     if (p.stats) {
-      for (int c = (int)lane; c < BN; c += 32) my_sum[c] = my_sum[BN + c] = 0.f;
+      for (int c = (int)lane; c < 2 * HB; c += 32) my_sum[c] = 0.f;
+      __syncwarp();
     }
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const int m = my + (int)lane;
       const bool row_ok = m < p.M;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = (int)half * 32; c0 < BN; c0 += 64) {
         uint32_t r[32];
         if (!empty_k) {
           tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
@@ -334,8 +355,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
-        if (c0 + 32 >= BN) {
-          // every column of this accumulator is in registers: hand it back
+        if (c0 + 64 >= BN) {
+          // this warp's last chunk of the accumulator is in registers: hand it back
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[acc]);
@@ -379,9 +400,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           sbuf = stg + buf * 2048;
           tma_out(w, col0, my, tc.z);
         } else {
-          // generic: stage in the spare buffer, then write whole 64-byte row
-          // segments with 4 lanes per row (8 rows per instruction)
-          uint8_t* gb = stg + 2048;
+          // generic: stage, then write whole 64-byte row segments with 4
+          // lanes per row (8 rows per instruction)
+          uint8_t* gb = stg;
+          __syncwarp();
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t sw = (uint32_t)j ^ ((lane >> 1) & 3u);
@@ -448,10 +470,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           q0 += __shfl_xor_sync(0xffffffffu, q0, 16);
           q1 += __shfl_xor_sync(0xffffffffu, q1, 16);
           if (lane < 16) {
-            my_sum[c0 + 2 * lane] += s0;
-            my_sum[c0 + 2 * lane + 1] += s1;
-            my_sum[BN + c0 + 2 * lane] += q0;
-            my_sum[BN + c0 + 2 * lane + 1] += q1;
+            const int lc = ((c0 >> 6) << 5) + 2 * (int)lane;  // this warp's local column
+            my_sum[lc] += s0;
+            my_sum[lc + 1] += s1;
+            my_sum[HB + lc] += q0;
+            my_sum[HB + lc + 1] += q1;
           }
         }
         __syncwarp();
@@ -543,7 +566,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, cudaStr
   kp.splits = splits;
   const long kb_per_cta = (long)kp.kb_per_split * ((total + grid - 1) / grid);
   kp.stages = (int)std::max<long>(2, std::min<long>(C::kStages, kb_per_cta));
-  const int smem = kp.stages * C::kStage + kStaging + C::kStats + 1024 + 256;
+  const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
   gemm_kernel<BN><<<grid, kThreads, smem, st>>>(kp);
   return cudaGetLastError();
 }
@@ -555,15 +578,30 @@ int gemm_m_tiles(const GemmDesc& d) { return (d.M + kBlockM - 1) / kBlockM; }
 int gemm_block_n(const GemmDesc& d) {
   int bn = d.block_n;
   if (bn == 0) {
-    // pick the tile width that minimises (tiles per SM, rounded up) x width:
-    // wide tiles when there is plenty of parallelism, narrow ones when a
-    // wide grid would leave SMs idle
+    // Empirical cost model, fitted to a B200 sweep of every ResNet-50 GEMM
+    // shape over tile widths and split counts (tools/gemm_sweep.py):
+    //   t(bn) = waves * (k_blocks * a + b)   [us]
+    // a = cost of one 64-deep K block of a 128 x bn tile: ~0.5 us whenever A
+    // comes through TMA im2col (the im2col load, not the MMA, is the limit,
+    // so wider tiles are free work), 0.20 / 0.25 / 0.30 us for plain 2-D
+    // tiles; b = per-tile prologue + epilogue, 2.5 / 3.5 / 7 us.
     const long mt = (d.M + kBlockM - 1) / kBlockM;
-    long best = -1;
+    const int splits = std::max(1, d.splits);
+    long kb;
+    if (d.a_kind == Operand::Im2colK)
+      kb = (long)d.a_geom.R * d.a_geom.S * ((d.a_geom.C + 63) / 64);
+    else
+      kb = (d.K + 63) / 64;
+    kb = (kb + splits - 1) / splits;
+    const bool im2col = d.a_kind == Operand::Im2colK;
+    double best = -1;
     for (int cand : {256, 128, 64}) {
       if (cand > 64 && d.N <= cand / 2) continue;
-      const long tiles = mt * ((d.N + cand - 1) / cand) * std::max(1, d.splits);
-      const long cost = ((tiles + 147) / 148) * (long)cand;
+      const long tiles = mt * ((d.N + cand - 1) / cand) * splits;
+      const long waves = (tiles + 147) / 148;
+      const double a = im2col ? 0.5 : (cand == 64 ? 0.20 : (cand == 128 ? 0.25 : 0.30));
+      const double b = cand == 64 ? 2.5 : (cand == 128 ? 3.5 : 7.0);
+      const double cost = (double)waves * ((double)kb * a + b);
       if (best < 0 || cost < best) {
         best = cost;
         bn = cand;

@@ -256,7 +256,12 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-store-all", action="store_true")
+    ap.add_argument("--arch", default="resnet50",
+                    help="resnet50 (headline) | resnet18/34/101/152 | densenet121/169/201/161 | vgg11-19 | alexnet")
+    ap.add_argument("--hw", type=int, default=224)
     args = ap.parse_args()
+    global ARCH, HW
+    ARCH, HW = args.arch, args.hw
     if args.impl == "reference":
         return run_reference(args)
 
@@ -342,8 +347,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (N,3,224,224) random images + random labels; random-init weights",
-            "config": {"workload": f"resnet50 re-forward training, batch {args.batch}/GPU, 3x224x224, SGD",
-                       "model": "resnet50", "global_batch": args.batch * world, "seq_len": None,
+            "config": {"workload": f"{ARCH} re-forward training, batch {args.batch}/GPU, 3x{HW}x{HW}, SGD",
+                       "model": ARCH, "global_batch": args.batch * world, "seq_len": None,
                        "parallelism": f"dp{world}", "policy": "reforward (Algorithm 5 plan)",
                        "l2": "working set (activations + weights) far exceeds the 126 MB L2; no flush"},
             "memory": {"activation_peak_bytes": rep.tracked_peak, "planned_eq1_bytes": rep.planned_total,

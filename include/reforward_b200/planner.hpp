@@ -26,6 +26,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <optional>
@@ -53,11 +54,21 @@ class VertexSet {
  public:
   VertexSet() = default;
   explicit VertexSet(std::size_t n);
+  VertexSet(const VertexSet& o) { copy_from(o); }
+  VertexSet(VertexSet&& o) noexcept { move_from(std::move(o)); }
+  VertexSet& operator=(const VertexSet& o) {
+    if (this != &o) copy_from(o);
+    return *this;
+  }
+  VertexSet& operator=(VertexSet&& o) noexcept {
+    if (this != &o) move_from(std::move(o));
+    return *this;
+  }
 
   std::size_t capacity() const { return bits_; }
-  bool test(std::size_t i) const { return (w_[i >> 6] >> (i & 63)) & 1u; }
-  void set(std::size_t i) { w_[i >> 6] |= std::uint64_t{1} << (i & 63); }
-  void reset(std::size_t i) { w_[i >> 6] &= ~(std::uint64_t{1} << (i & 63)); }
+  bool test(std::size_t i) const { return (data()[i >> 6] >> (i & 63)) & 1u; }
+  void set(std::size_t i) { data()[i >> 6] |= std::uint64_t{1} << (i & 63); }
+  void reset(std::size_t i) { data()[i >> 6] &= ~(std::uint64_t{1} << (i & 63)); }
   void clear();
 
   std::size_t count() const;
@@ -66,8 +77,8 @@ class VertexSet {
 
   VertexSet& operator|=(const VertexSet& o);
   VertexSet& operator&=(const VertexSet& o);
-  bool operator==(const VertexSet& o) const { return w_ == o.w_; }
-  bool operator!=(const VertexSet& o) const { return w_ != o.w_; }
+  bool operator==(const VertexSet& o) const;
+  bool operator!=(const VertexSet& o) const { return !(*this == o); }
   bool is_subset_of(const VertexSet& o) const;
   bool intersects(const VertexSet& o) const;
   std::vector<std::uint32_t> to_indices() const;
@@ -76,13 +87,38 @@ class VertexSet {
   // sorts first.  Returns -1 / 0 / +1.
   static int compare_lex(const VertexSet& a, const VertexSet& b);
 
-  // raw word access for the planner internals
-  const std::vector<std::uint64_t>& words() const { return w_; }
-  std::vector<std::uint64_t>& words() { return w_; }
-
  private:
+  // Sets of up to 512 vertices live inline: the planner's frontier scans copy
+  // millions of them, and a heap allocation per copy dominated their cost.
+  static constexpr std::size_t kInline = 8;
   std::size_t bits_ = 0;
-  std::vector<std::uint64_t> w_;
+  std::size_t nw_ = 0;
+  std::uint64_t inl_[kInline] = {};
+  std::unique_ptr<std::uint64_t[]> heap_;
+  std::uint64_t* data() { return heap_ ? heap_.get() : inl_; }
+  const std::uint64_t* data() const { return heap_ ? heap_.get() : inl_; }
+  void copy_from(const VertexSet& o) {
+    bits_ = o.bits_;
+    nw_ = o.nw_;
+    if (nw_ <= kInline) {
+      heap_.reset();
+      std::memcpy(inl_, o.data(), nw_ * sizeof(std::uint64_t));
+    } else {
+      heap_.reset(new std::uint64_t[nw_]);
+      std::memcpy(heap_.get(), o.data(), nw_ * sizeof(std::uint64_t));
+    }
+  }
+  void move_from(VertexSet&& o) {
+    bits_ = o.bits_;
+    nw_ = o.nw_;
+    if (o.heap_) {
+      heap_ = std::move(o.heap_);
+    } else {
+      heap_.reset();
+      std::memcpy(inl_, o.inl_, nw_ * sizeof(std::uint64_t));
+    }
+    o.bits_ = o.nw_ = 0;
+  }
 };
 
 // ---------------------------------------------------------------- CompGraph

@@ -68,6 +68,11 @@ int rfx_net_relu(rfx_net* net, int32_t x, const char* name, int32_t* out);
 int rfx_net_maxpool(rfx_net* net, int32_t x, int32_t k, int32_t stride, int32_t pad, const char* name,
                     int32_t* out);
 int rfx_net_avgpool(rfx_net* net, int32_t x, const char* name, int32_t* out);
+/* windowed average pooling (torch AvgPool2d, count_include_pad) */
+int rfx_net_avgpool2d(rfx_net* net, int32_t x, int32_t k, int32_t stride, int32_t pad, const char* name,
+                      int32_t* out);
+/* hidden fully connected layer: NHWC input flattened, bf16 output [N, out_features] + bias */
+int rfx_net_linear(rfx_net* net, int32_t x, int32_t out_features, const char* name, int32_t* out);
 int rfx_net_fc(rfx_net* net, int32_t x, int32_t classes, const char* name, int32_t* out);
 int rfx_net_concat(rfx_net* net, int32_t a, int32_t b, const char* name, int32_t* out);
 int rfx_net_loss(rfx_net* net, int32_t logits, const char* name, int32_t* out);

@@ -25,8 +25,9 @@ executes exactly that on the CPU:
 * ``live_peak`` reports the activation high-water mark (tensor bytes at the
   executor's cost granularity) observed while doing so.
 
-Layout note: tensors are NCHW here; the executor's NHWC flattening only
-matters for FC inputs, which are always pooled [N, C, 1, 1].
+Layout note: tensors are NCHW here.  The executor flattens a hidden linear
+layer's input in NHWC order and stores its weight accordingly; read_param /
+write_param convert to the canonical NCHW-flatten layout used here.
 """
 from __future__ import annotations
 
@@ -72,6 +73,8 @@ class OracleNet:
                     w = w * residual_gamma
             elif p.kind in (2, 4):
                 w = 0.1 * torch.randn(p.shape, generator=g)
+            elif p.kind == 5:  # hidden linear layer (Kaiming over the fan-in)
+                w = torch.randn(p.shape, generator=g) * (2.0 / p.shape[1]) ** 0.5
             else:
                 w = torch.randn(p.shape, generator=g) * 0.05
             self.weights[p.name] = w.to(self.dtype)
@@ -120,9 +123,15 @@ class OracleNet:
             return F.max_pool2d(ins[0], a["k"], a["stride"], a["pad"])
         if k == "avgpool":
             return ins[0].mean(dim=(2, 3), keepdim=True)
+        if k == "avgpool2d":
+            return F.avg_pool2d(ins[0], a["k"], a["stride"], a["pad"], count_include_pad=True)
         if k == "fc":
             x = ins[0].flatten(1)
             return F.linear(x, self.rb(self.weights[op.name + ".weight"]), self.weights[op.name + ".bias"])
+        if k == "linear":  # hidden layer: NCHW flatten (the canonical weight layout), [N, out, 1, 1]
+            x = ins[0].flatten(1)
+            y = F.linear(x, self.rb(self.weights[op.name + ".weight"]), self.weights[op.name + ".bias"])
+            return y.view(y.shape[0], -1, 1, 1)
         if k == "concat":
             return torch.cat(ins, dim=1)
         if k == "loss":
@@ -176,6 +185,13 @@ class OracleNet:
             elif op.kind == "avgpool":  # shape only
                 _, h, w, _c = self.tensors[op.inputs[0]].shape
                 in_grads = [(op.inputs[0], (dout / (h * w)).expand(-1, -1, h, w).contiguous())]
+                wgr = []
+            elif op.kind == "avgpool2d":  # linear and shape only: the input itself is not kept
+                n, h, w, c = self.tensors[op.inputs[0]].shape
+                x = torch.zeros(n, c, h, w, dtype=dout.dtype, requires_grad=True)
+                a = self.attrs[op.id]
+                z = F.avg_pool2d(x, a["k"], a["stride"], a["pad"], count_include_pad=True)
+                in_grads = [(op.inputs[0], torch.autograd.grad(z, x, grad_outputs=dout)[0])]
                 wgr = []
             elif op.kind == "concat":
                 ca = self.tensors[op.inputs[0]].shape[3]

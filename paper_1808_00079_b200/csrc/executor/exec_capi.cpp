@@ -84,6 +84,13 @@ int rfx_net_maxpool(rfx_net* n, int32_t x, int32_t k, int32_t stride, int32_t pa
 int rfx_net_avgpool(rfx_net* n, int32_t x, const char* name, int32_t* out) {
   return guard([&] { *out = n->net->avgpool(x, nm(name)); });
 }
+int rfx_net_avgpool2d(rfx_net* n, int32_t x, int32_t k, int32_t stride, int32_t pad, const char* name,
+                      int32_t* out) {
+  return guard([&] { *out = n->net->avgpool2d(x, k, stride, pad, nm(name)); });
+}
+int rfx_net_linear(rfx_net* n, int32_t x, int32_t out_features, const char* name, int32_t* out) {
+  return guard([&] { *out = n->net->linear(x, out_features, nm(name)); });
+}
 int rfx_net_fc(rfx_net* n, int32_t x, int32_t classes, const char* name, int32_t* out) {
   return guard([&] { *out = n->net->fc(x, classes, nm(name)); });
 }

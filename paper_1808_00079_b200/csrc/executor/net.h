@@ -29,7 +29,7 @@
 namespace rfx {
 
 enum class DType : int { BF16 = 0, F32 = 1 };
-enum class OpKind : int { Input = 0, Conv, BN, BNAddReLU, ReLU, MaxPool, AvgPool, FC, Concat, Loss };
+enum class OpKind : int { Input = 0, Conv, BN, BNAddReLU, ReLU, MaxPool, AvgPool, FC, Concat, Loss, AvgPool2d, Linear };
 const char* op_kind_name(OpKind k);
 
 constexpr long kAlign = 1024;  // arena slot alignment (bytes); costs are rounded to it
@@ -55,7 +55,7 @@ struct BNState {  // per-BN-layer device state (persistent, fp32 [C] each)
 
 struct Param {
   std::string name;
-  int kind = 0;  // 0 conv weight, 1 bn gamma, 2 bn beta, 3 fc weight, 4 fc bias
+  int kind = 0;  // 0 conv weight, 1 bn gamma, 2 bn beta, 3 fc weight, 4 fc / linear bias, 5 linear weight
   int op = -1;
   long offset = 0, count = 0;          // slice of the flat fp32 master / grad / momentum buffers
   long bf16_off = -1, bf16_count = 0;  // bf16 GEMM-layout copy (conv / fc weights)
@@ -78,8 +78,9 @@ struct Op {
   int wg_splits = 1, wg_bn = 128;  // wgrad split-K and tile N
   // pool
   int k = 1;
-  // classifier
-  int classes = 0;
+  // classifier / linear
+  int classes = 0;  // output features
+  int lin_h = 1, lin_w = 1, lin_c = 0;  // linear: input spatial shape (flattened NHWC)
   // parameters / state
   int w_param = -1, b_param = -1;  // conv/fc weight + fc bias; bn gamma (w) + beta (b)
   int bn = -1;                     // BNState index
@@ -128,8 +129,10 @@ class Net {
   int bn_add_relu(int y, int skip, const std::string& name);
   int relu(int x, const std::string& name);
   int maxpool(int x, int k, int stride, int pad, const std::string& name);
-  int avgpool(int x, const std::string& name);
-  int fc(int x, int classes, const std::string& name);
+  int avgpool(int x, const std::string& name);                                     // global
+  int avgpool2d(int x, int k, int stride, int pad, const std::string& name);       // windowed
+  int fc(int x, int classes, const std::string& name);                             // fp32 logits
+  int linear(int x, int out_features, const std::string& name);                    // bf16 hidden layer
   int concat(int a, int b, const std::string& name);
   int loss(int logits, const std::string& name);
 

@@ -116,6 +116,10 @@ void Net::setup(uint64_t seed) {
       std::normal_distribution<float> nd(0.f, 0.01f);
       for (long i = 0; i < p.count; ++i) dst[i] = nd(rng);
     }
+    if (p.kind == 5) {  // hidden linear layer: Kaiming normal over its fan-in
+      std::normal_distribution<float> nd(0.f, std::sqrt(2.f / (float)op.cin));
+      for (long i = 0; i < p.count; ++i) dst[i] = nd(rng);
+    }
     check(cudaMemcpy(d_param_ + p.offset, dst, p.count * 4, cudaMemcpyHostToDevice), "param upload");
   }
   std::vector<float> st(n_state_, 0.f);
@@ -143,6 +147,13 @@ void Net::write_param(int i, const float* host) {
             else idx = (((long)a * R + r) * S + s) * op.cpad + c;
             buf[idx] = v;
           }
+  } else if (p.kind == 5 && op.lin_h * op.lin_w > 1) {
+    // canonical [out][c][h][w] (NCHW flatten) -> GEMM [out][h][w][c]
+    const int HW = op.lin_h * op.lin_w, Cc = op.lin_c;
+    for (int o = 0; o < op.classes; ++o)
+      for (int c = 0; c < Cc; ++c)
+        for (int hw = 0; hw < HW; ++hw)
+          buf[(long)o * op.cin + (long)hw * Cc + c] = host[(long)o * op.cin + (long)c * HW + hw];
   } else {
     std::memcpy(buf.data(), host, p.count * 4);
   }
@@ -170,6 +181,12 @@ void Net::read_param(int i, int which, float* host) const {
             else idx = (((long)a * R + r) * S + s) * op.cpad + c;
             host[(((long)a * ci + c) * R + r) * S + s] = buf[idx];
           }
+  } else if (p.kind == 5 && op.lin_h * op.lin_w > 1) {
+    const int HW = op.lin_h * op.lin_w, Cc = op.lin_c;
+    for (int o = 0; o < op.classes; ++o)
+      for (int c = 0; c < Cc; ++c)
+        for (int hw = 0; hw < HW; ++hw)
+          host[(long)o * op.cin + (long)c * HW + hw] = buf[(long)o * op.cin + (long)hw * Cc + c];
   } else {
     std::memcpy(host, buf.data(), p.count * 4);
   }
@@ -353,6 +370,32 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       d.out = tptr(op.out);
       d.ldc = op.classes;
       d.out_f32 = true;
+      d.bias = d_param_ + params_[op.b_param].offset;
+      trace_flops_ = 2.0 * batch_ * op.classes * op.cin;
+      gemm(d, st);
+      break;
+    }
+    case OpKind::AvgPool2d: {
+      const Tensor& x = tensors_[op.in[0]];
+      const Tensor& y = tensors_[op.out];
+      rfk::PoolGeom g{x.N, x.H, x.W, x.C, y.H, y.W, op.k, op.stride, op.pad};
+      check(rfk::avgpool2d_fwd(tb(op.in[0]), g, tb(op.out), st), "avgpool2d");
+      break;
+    }
+    case OpKind::Linear: {
+      const Param& w = params_[op.w_param];
+      rfk::GemmDesc d;
+      d.M = batch_;
+      d.N = op.classes;
+      d.K = op.cin;
+      d.a_kind = rfk::Operand::KMajor2D;
+      d.a = tptr(op.in[0]);
+      d.a_ld = op.cin;
+      d.b_kind = rfk::Operand::KMajor2D;
+      d.b = d_bf16_ + w.bf16_off;
+      d.b_ld = op.cin;
+      d.out = tptr(op.out);
+      d.ldc = op.classes;
       d.bias = d_param_ + params_[op.b_param].offset;
       trace_flops_ = 2.0 * batch_ * op.classes * op.cin;
       gemm(d, st);
@@ -563,6 +606,51 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       gemm(d, st);
       break;
     }
+    case OpKind::AvgPool2d: {
+      const Tensor& x = tensors_[op.in[0]];
+      const Tensor& y = tensors_[op.out];
+      rfk::PoolGeom g{x.N, x.H, x.W, x.C, y.H, y.W, op.k, op.stride, op.pad};
+      check(rfk::avgpool2d_bwd(gptr(op.out), g, gptr(op.in[0]), acc(0), st), "avgpool2d_bwd");
+      break;
+    }
+    case OpKind::Linear: {
+      const Param& w = params_[op.w_param];
+      const __nv_bfloat16* dy = gptr(op.out);
+      trace_flops_ = 2.0 * batch_ * op.classes * op.cin;
+      check(rfk::colsum_bf16(dy, batch_, op.classes, d_grad_ + params_[op.b_param].offset, false, st), "db");
+      __nv_bfloat16* dx = gptr(op.in[0]);
+      if (dx) {
+        rfk::GemmDesc d;  // dX[batch][Kin] = dY[batch][out] W[out][Kin]
+        d.M = batch_;
+        d.N = op.cin;
+        d.K = op.classes;
+        d.a_kind = rfk::Operand::KMajor2D;
+        d.a = dy;
+        d.a_ld = op.classes;
+        d.b_kind = rfk::Operand::MNMajor2D;
+        d.b = d_bf16_ + w.bf16_off;
+        d.b_ld = op.cin;
+        d.out = dx;
+        d.ldc = op.cin;
+        d.accumulate_out = acc(0);
+        gemm(d, st);
+      }
+      rfk::GemmDesc d;  // dW[out][Kin] = dY^T X
+      d.M = op.classes;
+      d.N = op.cin;
+      d.K = batch_;
+      d.a_kind = rfk::Operand::MNMajor2D;
+      d.a = dy;
+      d.a_ld = op.classes;
+      d.b_kind = rfk::Operand::MNMajor2D;
+      d.b = tptr(op.in[0]);
+      d.b_ld = op.cin;
+      d.out = d_grad_ + w.offset;
+      d.ldc = op.cin;
+      d.out_f32 = true;
+      gemm(d, st);
+      break;
+    }
     case OpKind::Concat: {
       const Tensor& a = tensors_[op.in[0]];
       const Tensor& b2 = tensors_[op.in[1]];
@@ -596,7 +684,7 @@ void Net::prep_weights_table(cudaStream_t st) {
     std::vector<rfk::WeightPrepLayer> tab;
     long start = 0;
     for (const auto& p : params_) {
-      if (p.kind != 0 && p.kind != 3) continue;
+      if (p.kind != 0 && p.kind != 3 && p.kind != 5) continue;
       const Op& op = ops_[p.op];
       rfk::WeightPrepLayer L{};
       L.w = d_param_ + p.offset;
@@ -792,26 +880,35 @@ std::vector<std::array<double, 10>> Net::gemm_profile_detail(int iters, cudaStre
   double a, b;
   long c;
   if (gemm_trace_.empty()) gemm_profile(1, st, &a, &b, &c);
-  std::vector<cudaEvent_t> ev(gemm_trace_.size() + 1);
+  // the whole GEMM list as one CUDA graph with an event node after every
+  // launch: device times in step order, no host launch overhead
+  const size_t n = gemm_trace_.size();
+  std::vector<cudaEvent_t> ev(n + 1);
   for (auto& e : ev) check(cudaEventCreate(&e), "event");
-  std::vector<double> ms(gemm_trace_.size(), 0.0);
+  cudaGraphExec_t g = capture(
+      [&](cudaStream_t s) {
+        check(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal), "event");
+        for (size_t i = 0; i < n; ++i) {
+          check(rfk::gemm_launch(gemm_trace_[i].desc, s), "gemm");
+          check(cudaEventRecordWithFlags(ev[i + 1], s, cudaEventRecordExternal), "event");
+        }
+      },
+      nullptr);
+  std::vector<double> ms(n, 0.0);
   for (int it = 0; it < iters + 1; ++it) {
-    check(cudaEventRecord(ev[0], st), "event");
-    for (size_t i = 0; i < gemm_trace_.size(); ++i) {
-      check(rfk::gemm_launch(gemm_trace_[i].desc, st), "gemm");
-      check(cudaEventRecord(ev[i + 1], st), "event");
-    }
-    check(cudaEventSynchronize(ev.back()), "sync");
+    check(cudaGraphLaunch(g, st), "graph");
+    check(cudaStreamSynchronize(st), "sync");
     if (it == 0) continue;  // warm-up
-    for (size_t i = 0; i < gemm_trace_.size(); ++i) {
+    for (size_t i = 0; i < n; ++i) {
       float t = 0;
       cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
       ms[i] += t / iters;
     }
   }
+  cudaGraphExecDestroy(g);
   for (auto e : ev) cudaEventDestroy(e);
   std::vector<std::array<double, 10>> out;
-  for (size_t i = 0; i < gemm_trace_.size(); ++i) {
+  for (size_t i = 0; i < n; ++i) {
     const auto& d = gemm_trace_[i].desc;
     out.push_back({(double)d.M, (double)d.N, (double)d.K, (double)(int)d.a_kind, (double)(int)d.b_kind,
                    (double)d.splits, ms[i], gemm_trace_[i].flops, gemm_trace_[i].bytes,
@@ -877,37 +974,52 @@ double Net::gemm_try(int idx, int block_n, int splits, int iters, cudaStream_t s
   void* scratch = nullptr;
   check(cudaMalloc(&scratch, (size_t)d.splits * d.M * d.N * 4), "scratch");
   d.out = scratch;
+  // device time: `iters` launches captured in one CUDA graph (no host
+  // tensor-map encoding or launch overhead between them)
+  cudaGraphExec_t g = capture(
+      [&](cudaStream_t s) {
+        for (int i = 0; i < iters; ++i) check(rfk::gemm_launch(d, s), "gemm");
+      },
+      nullptr);
   cudaEvent_t e0, e1;
   check(cudaEventCreate(&e0), "event");
   check(cudaEventCreate(&e1), "event");
-  for (int i = 0; i < 2; ++i) check(rfk::gemm_launch(d, st), "gemm");
+  check(cudaGraphLaunch(g, st), "warmup");
   check(cudaEventRecord(e0, st), "event");
-  for (int i = 0; i < iters; ++i) check(rfk::gemm_launch(d, st), "gemm");
+  check(cudaGraphLaunch(g, st), "graph");
   check(cudaEventRecord(e1, st), "event");
   check(cudaEventSynchronize(e1), "sync");
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaGraphExecDestroy(g);
   cudaFree(scratch);
   return ms / iters;
 }
 
 std::vector<double> Net::instr_profile(int iters, cudaStream_t st) {
   if (!setup_done_) throw std::invalid_argument("setup the network first");
+  // the step as one CUDA graph with an event node after every instruction:
+  // in-graph device times, no host launch overhead
   const size_t n = sched_.size();
   std::vector<cudaEvent_t> ev(n + 2);
   for (auto& e : ev) check(cudaEventCreate(&e), "event");
+  cudaGraphExec_t g = capture(
+      [&](cudaStream_t s) {
+        check(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal), "event");
+        for (size_t k = 0; k < n; ++k) {
+          run_instr(sched_[k], s);
+          check(cudaEventRecordWithFlags(ev[k + 1], s, cudaEventRecordExternal), "event");
+        }
+        update(0.f, 0.f, 0.f, s);  // lr 0: parameters unchanged
+        check(cudaEventRecordWithFlags(ev[n + 1], s, cudaEventRecordExternal), "event");
+      },
+      nullptr);
   std::vector<double> ms(n + 1, 0.0);
   for (int it = 0; it < iters + 1; ++it) {
-    check(cudaEventRecord(ev[0], st), "event");
-    for (size_t k = 0; k < n; ++k) {
-      run_instr(sched_[k], st);
-      check(cudaEventRecord(ev[k + 1], st), "event");
-    }
-    update(0.f, 0.f, 0.f, st);  // lr 0: parameters unchanged
-    check(cudaEventRecord(ev[n + 1], st), "event");
-    check(cudaEventSynchronize(ev[n + 1]), "sync");
+    check(cudaGraphLaunch(g, st), "graph");
+    check(cudaStreamSynchronize(st), "sync");
     if (it == 0) continue;  // warm-up
     for (size_t k = 0; k <= n; ++k) {
       float t = 0;
@@ -915,6 +1027,7 @@ std::vector<double> Net::instr_profile(int iters, cudaStream_t st) {
       ms[k] += t / iters;
     }
   }
+  cudaGraphExecDestroy(g);
   for (auto e : ev) cudaEventDestroy(e);
   return ms;
 }

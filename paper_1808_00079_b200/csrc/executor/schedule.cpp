@@ -24,6 +24,8 @@ const char* op_kind_name(OpKind k) {
     case OpKind::FC: return "fc";
     case OpKind::Concat: return "concat";
     case OpKind::Loss: return "loss";
+    case OpKind::AvgPool2d: return "avgpool2d";
+    case OpKind::Linear: return "linear";
   }
   return "?";
 }
@@ -199,6 +201,46 @@ int Net::avgpool(int x, const std::string& name) {
   return tensors_.size() - 1;
 }
 
+int Net::avgpool2d(int x, int k, int stride, int pad, const std::string& name) {
+  const Tensor tx = tensors_.at(x);
+  require(k >= 1 && stride >= 1 && pad >= 0 && 2 * pad <= k, "bad avgpool2d window");
+  const int P = (tx.H + 2 * pad - k) / stride + 1, Q = (tx.W + 2 * pad - k) / stride + 1;
+  require(P > 0 && Q > 0, "avgpool2d output is empty");
+  Op op;
+  op.kind = OpKind::AvgPool2d;
+  op.name = name;
+  op.in = {x};
+  op.k = k;
+  op.stride = stride;
+  op.pad = pad;
+  op.out = add_tensor(name, tx.N, P, Q, tx.C, DType::BF16);
+  add_op(op);
+  return tensors_.size() - 1;
+}
+
+// Hidden fully connected layer (VGG / AlexNet classifier): the NHWC input is
+// flattened to H*W*C features; bf16 output [N, out] with bias.  The weight's
+// canonical (PyTorch) layout is [out][C*H*W]; the GEMM copy is [out][H*W*C].
+int Net::linear(int x, int out_features, const std::string& name) {
+  const Tensor tx = tensors_.at(x);
+  require(tx.dtype == DType::BF16, "linear input must be bf16");
+  require(out_features % 8 == 0, "linear output features must be a multiple of 8");
+  Op op;
+  op.kind = OpKind::Linear;
+  op.name = name;
+  op.in = {x};
+  op.classes = out_features;
+  op.lin_h = tx.H;
+  op.lin_w = tx.W;
+  op.lin_c = tx.C;
+  op.cin = tx.H * tx.W * tx.C;
+  op.out = add_tensor(name, tx.N, 1, 1, out_features, DType::BF16);
+  const int id = add_op(op);
+  ops_[id].w_param = add_param(name + ".weight", 5, id, (long)out_features * ops_[id].cin, {out_features, ops_[id].cin});
+  ops_[id].b_param = add_param(name + ".bias", 4, id, out_features, {out_features});
+  return ops_[id].out;
+}
+
 int Net::fc(int x, int classes, const std::string& name) {
   const Tensor tx = tensors_.at(x);
   require(tx.H == 1 && tx.W == 1, "fc input must be pooled [N, C]");
@@ -330,6 +372,7 @@ static std::vector<int> backward_needs(const Op& op) {
     case OpKind::ReLU: return {op.out};
     case OpKind::MaxPool: return {op.in[0], op.out};
     case OpKind::FC: return {op.in[0]};
+    case OpKind::Linear: return {op.in[0]};
     case OpKind::Loss: return {op.in[0]};
     default: return {};
   }
@@ -667,7 +710,7 @@ long Net::flops_per_step() const {
       const long fwd = 2L * y.rows() * op.cout * op.R * op.S * op.cin_real;
       const bool dgrad = op.in[0] != input_t_;
       f += fwd * (dgrad ? 3 : 2);
-    } else if (op.kind == OpKind::FC) {
+    } else if (op.kind == OpKind::FC || op.kind == OpKind::Linear) {
       f += 2L * batch_ * op.classes * op.cin * 3;
     }
   }

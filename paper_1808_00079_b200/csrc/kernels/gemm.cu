@@ -14,11 +14,13 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <mutex>
 
 #include "kernels/kernels.h"
+#include "kernels/launch.cuh"
 #include "kernels/ptx.cuh"
 
 namespace rfk {
@@ -53,6 +55,7 @@ struct alignas(64) KParams {
   int out_mode;  // 0 generic stores, 1 TMA store, 2 TMA reduce-add (accumulate_out)
   int stages;  // smem ring depth (<= Cfg::kStages)
   int m_tiles, n_tiles, splits;  // persistent tile space
+  int experiment;  // tuning only: 2 drop the output, 3 also skip TMEM loads, 4 also skip the MMAs
 };
 
 template <int BN>
@@ -162,6 +165,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // everything above (barrier init, TMEM allocation, descriptor prefetch)
+  // overlaps the previous kernel's tail under programmatic dependent launch
+  pdl_enter();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const uint32_t sa = smem_u32(smem + stage * C::kStage);
           const uint32_t sb = sa + kTileA;
 #pragma unroll
-          for (int kk = 0; kk < kBlockK / 16; ++kk) {
+          for (int kk = 0; kk < (p.experiment == 4 ? 0 : kBlockK / 16); ++kk) {
             const uint64_t da = a_mn ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
                                      : umma_desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll 1
       for (int c0 = (int)half * 32; c0 < BN; c0 += 64) {
         uint32_t r[32];
-        if (!empty_k) {
+        if (!empty_k && p.experiment < 3) {
           tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
           tmem_ld_wait();
         } else {
@@ -365,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int col0 = tc.n0 + c0;
-        if (col0 >= p.N) continue;  // warp-uniform
+        if (col0 >= p.N || p.experiment >= 2) continue;  // warp-uniform
         const bool full_cols = col0 + 32 <= p.N;
         if (p.bias) {
 #pragma unroll
@@ -566,9 +572,19 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, cudaStr
   kp.splits = splits;
   const long kb_per_cta = (long)kp.kb_per_split * ((total + grid - 1) / grid);
   kp.stages = (int)std::max<long>(2, std::min<long>(C::kStages, kb_per_cta));
+  static const int force_stages = [] {
+    const char* e = std::getenv("RFK_GEMM_STAGES");  // tuning experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force_stages >= 2) kp.stages = std::min(force_stages, C::kStages);
+  static const int experiment = [] {
+    const char* e = std::getenv("RFK_GEMM_EXPERIMENT");  // tuning experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  kp.experiment = experiment;
+  if (experiment == 1) kp.out_mode = 0;
   const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
-  gemm_kernel<BN><<<grid, kThreads, smem, st>>>(kp);
-  return cudaGetLastError();
+  return launch_k(gemm_kernel<BN>, grid, kThreads, smem, st, kp);
 }
 
 }  // namespace

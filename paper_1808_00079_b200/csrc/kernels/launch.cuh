@@ -1,0 +1,49 @@
+// Kernel launch with programmatic dependent launch (PDL).
+//
+// Every kernel of the step starts with pdl_enter(): it waits for the
+// preceding kernel in the stream to finish (griddepcontrol.wait) and then
+// lets the next kernel be scheduled (griddepcontrol.launch_dependents).  Host
+// launches carry the programmatic-stream-serialization attribute, so inside
+// the step's CUDA graph the next kernel's launch, CTA rasterisation and
+// pre-wait prologue (barrier init, TMEM allocation, descriptor prefetch)
+// overlap the tail of the previous kernel instead of following it.
+// RFK_PDL=0 turns the attribute off (plain stream order).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <utility>
+
+namespace rfk {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RFK_PDL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+}  // namespace rfk

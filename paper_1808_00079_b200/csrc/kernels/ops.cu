@@ -10,9 +10,16 @@
 
 #include <cstdint>
 
+#include "kernels/launch.cuh"
 #include "kernels/ops.h"
 
 namespace rfk {
+
+#define RFK_CHECK_LAUNCH(call)            \
+  do {                                    \
+    const cudaError_t e_ = (call);        \
+    if (e_ != cudaSuccess) return e_;     \
+  } while (0)
 
 namespace {
 
@@ -72,6 +79,7 @@ __device__ __forceinline__ RedShape red_shape(int C) {
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) colstats_kernel(const __nv_bfloat16* __restrict__ x, long M, int C,
                                                             long rows_per_block, float* __restrict__ partials) {
+  pdl_enter();
   // handles C <= 2048 per pass; channel chunks via blockIdx.y
   __shared__ float sh[2][kThreads][8];
   const int cchunk = blockIdx.y;  // chunk of 2048 channels
@@ -157,6 +165,7 @@ __global__ void bn_finalize_kernel(const float* __restrict__ partials, int parts
                                    float* __restrict__ mean, float* __restrict__ invstd, float* __restrict__ scale,
                                    float* __restrict__ shift, float* __restrict__ run_mean, float* __restrict__ run_var,
                                    float momentum, int update_running) {
+  pdl_enter();
   const int c = blockIdx.x * 32 + threadIdx.x;
   float s0, s1;
   sum_partials(partials, parts, C, c, s0, s1);
@@ -192,6 +201,7 @@ __global__ void __launch_bounds__(kThreads) bn_apply_kernel(const __nv_bfloat16*
                                                            const __nv_bfloat16* skip, const float* __restrict__ scale,
                                                            const float* __restrict__ shift, int relu, long nvec, int C,
                                                            __nv_bfloat16* out) {
+  pdl_enter();
   const int cv = C / 8;
   const long stride = (long)gridDim.x * blockDim.x;
   for (long v0 = (long)blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * kVec) {
@@ -236,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 3) bn_bwd_reduce_kernel(
     const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
     const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ shift, long M, int C,
     long rows_per_block, float* __restrict__ partials) {
+  pdl_enter();
   __shared__ float sh[2][kThreads][8];
   const int cchunk = blockIdx.y;
   const int Cc = min(2048, C - cchunk * 2048);
@@ -312,6 +323,7 @@ __global__ void bn_bwd_finalize_kernel(const float* __restrict__ partials, int p
                                        const float* __restrict__ gamma, const float* __restrict__ mean,
                                        const float* __restrict__ invstd, float* __restrict__ dgamma,
                                        float* __restrict__ dbeta, float* __restrict__ coef) {
+  pdl_enter();
   const int c = blockIdx.x * 32 + threadIdx.x;
   float sg, sgy;
   sum_partials(partials, parts, C, c, sg, sgy);
@@ -335,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 4) bn_bwd_apply_kernel(
     const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
     const float* __restrict__ scale, const float* __restrict__ shift, const float* __restrict__ coef, unsigned nvec,
     int C, __nv_bfloat16* __restrict__ dy, int acc_dy, __nv_bfloat16* __restrict__ dskip, int acc_dskip) {
+  pdl_enter();
   const unsigned cv = (unsigned)C / 8;
   const unsigned stride = gridDim.x * blockDim.x;
   for (unsigned v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += 2 * stride) {
@@ -404,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 4) bn_bwd_apply_kernel(
 
 __global__ void __launch_bounds__(kThreads) relu_fwd_kernel(const __nv_bfloat16* __restrict__ x, long nvec,
                                                            __nv_bfloat16* __restrict__ y) {
+  pdl_enter();
   for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
     float f[8];
     unpack8(ldg16(x + v * 8), f);
@@ -416,6 +430,7 @@ __global__ void __launch_bounds__(kThreads) relu_fwd_kernel(const __nv_bfloat16*
 __global__ void __launch_bounds__(kThreads) relu_bwd_kernel(const __nv_bfloat16* __restrict__ y,
                                                            const __nv_bfloat16* __restrict__ dy, long nvec,
                                                            __nv_bfloat16* __restrict__ dx, int acc) {
+  pdl_enter();
   for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
     float fy[8], fd[8];
     unpack8(ldg16(y + v * 8), fy);
@@ -435,6 +450,7 @@ __global__ void __launch_bounds__(kThreads) relu_bwd_kernel(const __nv_bfloat16*
 // ------------------------------------------------------------ pooling
 __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, PoolGeom g,
                                                               __nv_bfloat16* __restrict__ y) {
+  pdl_enter();
   const int cv = g.C / 8;
   const long total = (long)g.N * g.P * g.Q * cv;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -463,10 +479,87 @@ __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat
   }
 }
 
+// Windowed average pooling (torch AvgPool2d, count_include_pad=True: the sum
+// over the in-bounds taps is always divided by k*k).
+__global__ void __launch_bounds__(kThreads) avgpool2d_fwd_kernel(const __nv_bfloat16* __restrict__ x, PoolGeom g,
+                                                                __nv_bfloat16* __restrict__ y) {
+  pdl_enter();
+  const int cv = g.C / 8;
+  const long total = (long)g.N * g.P * g.Q * cv;
+  const float inv = 1.f / (float)(g.k * g.k);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    long t = i / cv;
+    const int q = (int)(t % g.Q);
+    t /= g.Q;
+    const int p = (int)(t % g.P);
+    const int n = (int)(t / g.P);
+    float m[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = 0.f;
+    for (int r = 0; r < g.k; ++r) {
+      const int h = p * g.stride - g.pad + r;
+      if (h < 0 || h >= g.H) continue;
+      for (int s = 0; s < g.k; ++s) {
+        const int w = q * g.stride - g.pad + s;
+        if (w < 0 || w >= g.W) continue;
+        float f[8];
+        unpack8(ldg16(x + (((long)n * g.H + h) * g.W + w) * g.C + c8 * 8), f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m[k] += f[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] *= inv;
+    *reinterpret_cast<uint4*>(y + i * 8) = pack8(m);
+  }
+}
+
+// Gather form of the backward (no atomics): every input pixel sums dy over
+// the windows that cover it, in a fixed (p, q) order.
+__global__ void __launch_bounds__(kThreads) avgpool2d_bwd_kernel(const __nv_bfloat16* __restrict__ dy, PoolGeom g,
+                                                                __nv_bfloat16* __restrict__ dx, int acc) {
+  pdl_enter();
+  const int cv = g.C / 8;
+  const long total = (long)g.N * g.H * g.W * cv;
+  const float inv = 1.f / (float)(g.k * g.k);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % cv);
+    long t = i / cv;
+    const int w = (int)(t % g.W);
+    t /= g.W;
+    const int h = (int)(t % g.H);
+    const int n = (int)(t / g.H);
+    // windows p with p*stride - pad <= h < p*stride - pad + k
+    const int p0 = max(0, (h + g.pad - g.k + g.stride) / g.stride), p1 = min(g.P - 1, (h + g.pad) / g.stride);
+    const int q0 = max(0, (w + g.pad - g.k + g.stride) / g.stride), q1 = min(g.Q - 1, (w + g.pad) / g.stride);
+    float m[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = 0.f;
+    for (int p = p0; p <= p1; ++p)
+      for (int q = q0; q <= q1; ++q) {
+        float f[8];
+        unpack8(ldg16(dy + (((long)n * g.P + p) * g.Q + q) * g.C + c8 * 8), f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m[k] += f[k];
+      }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] *= inv;
+    if (acc) {
+      float prev[8];
+      unpack8(*reinterpret_cast<const uint4*>(dx + i * 8), prev);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m[k] += prev[k];
+    }
+    *reinterpret_cast<uint4*>(dx + i * 8) = pack8(m);
+  }
+}
+
 // Backward, pass 1: first argmax (row-major window position, ties to the
 // first hit) of every window and channel, one byte each.
 __global__ void __launch_bounds__(kThreads) maxpool_argmax_kernel(const __nv_bfloat16* __restrict__ x, PoolGeom g,
                                                                  uint8_t* __restrict__ idx) {
+  pdl_enter();
   const int cv = g.C / 8;
   const long total = (long)g.N * g.P * g.Q * cv;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -511,6 +604,7 @@ __global__ void __launch_bounds__(kThreads) maxpool_argmax_kernel(const __nv_bfl
 __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __restrict__ idx,
                                                               const __nv_bfloat16* __restrict__ dy, PoolGeom g,
                                                               __nv_bfloat16* __restrict__ dx, int acc) {
+  pdl_enter();
   const int cv = g.C / 8;
   const long total = (long)g.N * g.H * g.W * cv;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -554,6 +648,7 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __
 // global average pool: block per (n, 256-channel chunk); fixed-order sums
 __global__ void __launch_bounds__(kThreads) avgpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, int HW, int C,
                                                               __nv_bfloat16* __restrict__ out) {
+  pdl_enter();
   const int n = blockIdx.x;
   const int c = blockIdx.y * kThreads + threadIdx.x;
   if (c >= C) return;
@@ -565,6 +660,7 @@ __global__ void __launch_bounds__(kThreads) avgpool_fwd_kernel(const __nv_bfloat
 
 __global__ void __launch_bounds__(kThreads) avgpool_bwd_kernel(const __nv_bfloat16* __restrict__ dout, int HW, int C,
                                                               long nvec, __nv_bfloat16* __restrict__ dx, int acc) {
+  pdl_enter();
   const float inv = 1.f / (float)HW;
   for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
     const long e = v * 8;
@@ -590,6 +686,7 @@ __global__ void __launch_bounds__(kThreads) softmax_ce_fwd_kernel(const float* _
                                                                  const int* __restrict__ labels, int K,
                                                                  float* __restrict__ row_loss,
                                                                  float* __restrict__ lse_out) {
+  pdl_enter();
   __shared__ float red[kThreads];
   const int n = blockIdx.x;
   const float* z = logits + (long)n * K;
@@ -619,6 +716,7 @@ __global__ void __launch_bounds__(kThreads) softmax_ce_fwd_kernel(const float* _
 }
 
 __global__ void mean_kernel(const float* __restrict__ v, int n, float* __restrict__ out) {
+  pdl_enter();
   __shared__ float red[kThreads];
   float s = 0.f;
   for (int i = threadIdx.x; i < n; i += kThreads) s += v[i];
@@ -636,6 +734,7 @@ __global__ void __launch_bounds__(kThreads) softmax_ce_bwd_kernel(const float* _
                                                                  const int* __restrict__ labels,
                                                                  const float* __restrict__ lse, int Nrows, int K,
                                                                  float* __restrict__ dlogits) {
+  pdl_enter();
   const long total = (long)Nrows * K;
   const float invn = 1.f / (float)Nrows;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -647,12 +746,14 @@ __global__ void __launch_bounds__(kThreads) softmax_ce_bwd_kernel(const float* _
 }
 
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ x, long n, __nv_bfloat16* __restrict__ y) {
+  pdl_enter();
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16_rn(x[i]);
 }
 
 __global__ void __launch_bounds__(kThreads) cast_f32_bf16_vec_kernel(const float* __restrict__ x, long nvec,
                                                                     __nv_bfloat16* __restrict__ y) {
+  pdl_enter();
   for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
     float f[8];
     ld8f(x + v * 8, f);
@@ -663,6 +764,7 @@ __global__ void __launch_bounds__(kThreads) cast_f32_bf16_vec_kernel(const float
 // fp32 [R, C] -> bf16 [R, ldo] (pad columns untouched)
 __global__ void cast_f32_bf16_2d_kernel(const float* __restrict__ x, int R, int C, int ldo,
                                         __nv_bfloat16* __restrict__ y) {
+  pdl_enter();
   const long total = (long)R * C;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x)
     y[(i / C) * ldo + (i % C)] = __float2bfloat16_rn(x[i]);
@@ -671,6 +773,7 @@ __global__ void cast_f32_bf16_2d_kernel(const float* __restrict__ x, int R, int 
 // column sums of a bf16 [R, C] matrix, fixed order
 __global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ x, int R, int C, float* __restrict__ out,
                                    int acc) {
+  pdl_enter();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   float s = 0.f;
@@ -680,6 +783,7 @@ __global__ void colsum_bf16_kernel(const __nv_bfloat16* __restrict__ x, int R, i
 
 // column sums of an fp32 [R, C] matrix (bias gradient), fixed order
 __global__ void colsum_f32_kernel(const float* __restrict__ x, int R, int C, float* __restrict__ out, int acc) {
+  pdl_enter();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   float s = 0.f;
@@ -692,6 +796,7 @@ __global__ void colsum_f32_kernel(const float* __restrict__ x, int R, int C, flo
 // summation order z = 0, 1, ... is fixed (deterministic)
 __global__ void __launch_bounds__(kThreads) reduce_splits_kernel(const float* __restrict__ parts, int splits, long n4,
                                                                 float* __restrict__ out, int acc) {
+  pdl_enter();
   const float4* p4 = reinterpret_cast<const float4*>(parts);
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -730,6 +835,7 @@ __global__ void __launch_bounds__(kThreads) reduce_splits_kernel(const float* __
 __global__ void __launch_bounds__(kThreads) sgd_kernel(float* __restrict__ w, const float* __restrict__ g,
                                                       float* __restrict__ m, long n4, float lr, float momentum,
                                                       float wd, __nv_bfloat16* __restrict__ wb) {
+  pdl_enter();
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
     float4 wv = reinterpret_cast<float4*>(w)[i];
     const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
@@ -759,6 +865,7 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel(float* __restrict__ w, co
 // Wt[ci][R-1-r][S-1-s][co] with co padded to CoutPad.
 __global__ void conv_weight_prep_kernel(const float* __restrict__ w, int Cout, int R, int S, int Cpad, int Cin,
                                         int CoutPad, __nv_bfloat16* __restrict__ wb, __nv_bfloat16* __restrict__ wt) {
+  pdl_enter();
   const long total = (long)Cout * R * S * Cpad;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
     const int c = (int)(i % Cpad);
@@ -775,6 +882,7 @@ __global__ void conv_weight_prep_kernel(const float* __restrict__ w, int Cout, i
 
 __global__ void __launch_bounds__(kThreads) weight_prep_batched_kernel(const WeightPrepLayer* __restrict__ tab,
                                                                       int layers, long total) {
+  pdl_enter();
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
     int lo = 0, hi = layers - 1;  // last layer with start <= i
     while (lo < hi) {
@@ -804,6 +912,7 @@ __global__ void __launch_bounds__(kThreads) weight_prep_batched_kernel(const Wei
 // NCHW fp32 -> NHWC bf16 with zero channel padding to Cpad
 __global__ void pack_input_kernel(const float* __restrict__ x, int N, int C, int H, int W, int Cpad,
                                   __nv_bfloat16* __restrict__ out) {
+  pdl_enter();
   const long total = (long)N * H * W * Cpad;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
     const int c = (int)(i % Cpad);
@@ -821,6 +930,7 @@ __global__ void pack_input_kernel(const float* __restrict__ x, int N, int C, int
 // across the warp (consecutive w), the NHWC write is one 16-byte store
 __global__ void pack_input_vec_kernel(const float* __restrict__ x, int N, int C, int H, int W, int Cpad,
                                       __nv_bfloat16* __restrict__ out) {
+  pdl_enter();
   const long HW = (long)H * W;
   const int groups = Cpad / 8;
   const long total = (long)N * HW * groups;
@@ -846,6 +956,7 @@ __global__ void pack_input_vec_kernel(const float* __restrict__ x, int N, int C,
 // the pixel decode is done once per thread.
 __global__ void __launch_bounds__(kThreads) im2col_kernel(const __nv_bfloat16* __restrict__ x, ConvShape g, int Kpad,
                                                          __nv_bfloat16* __restrict__ out) {
+  pdl_enter();
   const int kv = Kpad / 8;
   const long total = (long)g.N * g.P * g.Q * kv;
   const int Kreal = g.R * g.S * g.C;
@@ -891,6 +1002,7 @@ __global__ void __launch_bounds__(kThreads) im2col_kernel(const __nv_bfloat16* _
 // as 2-byte global loads, so the kernel runs at the output write rate.
 __global__ void __launch_bounds__(kThreads) im2col_rows_kernel(const __nv_bfloat16* __restrict__ x, ConvShape g,
                                                               int Kpad, __nv_bfloat16* __restrict__ out) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned short rows_s[];  // [R][W + 2 pad][Cs], then the k table
   const int Wp = g.W + 2 * g.pad;
   const int cv = g.Cs / 8;  // 16-byte vectors per pixel
@@ -934,6 +1046,7 @@ __global__ void __launch_bounds__(kThreads) im2col_rows_kernel(const __nv_bfloat
 __global__ void __launch_bounds__(kThreads) zero_insert_kernel(const __nv_bfloat16* __restrict__ dy, int N, int P,
                                                               int Q, int C, int Hu, int Wu, int stride,
                                                               __nv_bfloat16* __restrict__ u) {
+  pdl_enter();
   const int cv = C / 8;
   const long total = (long)N * Hu * Wu * cv;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -954,6 +1067,7 @@ __global__ void __launch_bounds__(kThreads) zero_insert_kernel(const __nv_bfloat
 __global__ void __launch_bounds__(kThreads) concat_kernel(const __nv_bfloat16* __restrict__ a, int Ca,
                                                          const __nv_bfloat16* __restrict__ b, int Cb, long M,
                                                          __nv_bfloat16* __restrict__ c) {
+  pdl_enter();
   const int Cc = Ca + Cb, cv = Cc / 8;
   const long total = M * cv;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -970,6 +1084,7 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(const __nv_bfloat16* _
 __global__ void __launch_bounds__(kThreads) split_grad_kernel(const __nv_bfloat16* __restrict__ dc, int Ca, int Cb,
                                                              long M, __nv_bfloat16* __restrict__ da, int acc_a,
                                                              __nv_bfloat16* __restrict__ db, int acc_b) {
+  pdl_enter();
   const int Cc = Ca + Cb, cv = Cc / 8;
   const long total = M * cv;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
@@ -999,6 +1114,7 @@ __global__ void __launch_bounds__(kThreads) split_grad_kernel(const __nv_bfloat1
 
 __global__ void __launch_bounds__(kThreads) add_bf16_kernel(const __nv_bfloat16* __restrict__ a, long nvec,
                                                            __nv_bfloat16* __restrict__ dst) {
+  pdl_enter();
   for (long v = (long)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
     float x[8], y[8];
     unpack8(ldg16(a + v * 8), x);
@@ -1024,23 +1140,23 @@ int colstats_blocks(long M) {
 cudaError_t colstats(const __nv_bfloat16* x, long M, int C, float* partials, int blocks, cudaStream_t st) {
   if (C % 8 || (C > 2048 && C % 2048)) return cudaErrorInvalidValue;
   dim3 grid(blocks, (C + 2047) / 2048);
-  colstats_kernel<0><<<grid, kThreads, 0, st>>>(x, M, C, rows_per_block_for(M, blocks), partials);
+  RFK_CHECK_LAUNCH(launch_k(colstats_kernel<0>, grid, kThreads, 0, st, x, M, C, rows_per_block_for(M, blocks), partials));
   return cudaGetLastError();
 }
 
 cudaError_t bn_finalize(const float* partials, int parts, int C, long count, const float* gamma, const float* beta,
                         float eps, float* mean, float* invstd, float* scale, float* shift, float* run_mean,
                         float* run_var, float momentum, bool update_running, cudaStream_t st) {
-  bn_finalize_kernel<<<(C + 31) / 32, dim3(32, kFinY), 0, st>>>(partials, parts, C, (float)count, gamma, beta, eps, mean,
+  RFK_CHECK_LAUNCH(launch_k(bn_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, partials, parts, C, (float)count, gamma, beta, eps, mean,
                                                             invstd, scale, shift, run_mean, run_var, momentum,
-                                                            update_running ? 1 : 0);
+                                                            update_running ? 1 : 0));
   return cudaGetLastError();
 }
 
 cudaError_t bn_apply(const __nv_bfloat16* y, const __nv_bfloat16* skip, const float* scale, const float* shift,
                      bool relu, long M, int C, __nv_bfloat16* out, cudaStream_t st) {
   const long nvec = M * C / 8;
-  bn_apply_kernel<<<grid_for(nvec, kThreads * 4), kThreads, 0, st>>>(y, skip, scale, shift, relu ? 1 : 0, nvec, C, out);
+  RFK_CHECK_LAUNCH(launch_k(bn_apply_kernel, grid_for(nvec, kThreads * 4), kThreads, 0, st, y, skip, scale, shift, relu ? 1 : 0, nvec, C, out));
   return cudaGetLastError();
 }
 
@@ -1055,17 +1171,17 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
   dim3 grid(blocks, (C + 2047) / 2048);
   const long rpb = rows_per_block_for(M, blocks);
   switch (mask_mode) {
-    case 0: bn_bwd_reduce_kernel<0><<<grid, kThreads, 0, st>>>(y, dout, out, mean, scale, shift, M, C, rpb, partials); break;
-    case 1: bn_bwd_reduce_kernel<1><<<grid, kThreads, 0, st>>>(y, dout, out, mean, scale, shift, M, C, rpb, partials); break;
-    default: bn_bwd_reduce_kernel<2><<<grid, kThreads, 0, st>>>(y, dout, out, mean, scale, shift, M, C, rpb, partials);
+    case 0: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<0>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials)); break;
+    case 1: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<1>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials)); break;
+    default: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<2>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials));
   }
-  bn_bwd_finalize_kernel<<<(C + 31) / 32, dim3(32, kFinY), 0, st>>>(partials, blocks, C, (float)M, gamma, mean, invstd,
-                                                                dgamma, dbeta, coef);
+  RFK_CHECK_LAUNCH(launch_k(bn_bwd_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, partials, blocks, C, (float)M, gamma, mean, invstd,
+                                                                dgamma, dbeta, coef));
   const int g = grid_for(nvec, kThreads * 2, 148 * 4);  // one wave at 4 blocks per SM
   const unsigned nv = (unsigned)nvec;
   const int ad = acc_dy ? 1 : 0, as = acc_dskip ? 1 : 0;
 #define RF_BWD_APPLY(MODE, SKIP) \
-  bn_bwd_apply_kernel<MODE, SKIP><<<g, kThreads, 0, st>>>(y, dout, out, scale, shift, coef, nv, C, dy, ad, dskip, as)
+  RFK_CHECK_LAUNCH(launch_k(bn_bwd_apply_kernel<MODE, SKIP>, g, kThreads, 0, st, y, dout, out, scale, shift, coef, nv, C, dy, ad, dskip, as))
   if (dskip) {
     switch (mask_mode) {
       case 0: RF_BWD_APPLY(0, true); break;
@@ -1084,19 +1200,33 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
 }
 
 cudaError_t relu_fwd(const __nv_bfloat16* x, long n, __nv_bfloat16* y, cudaStream_t st) {
-  relu_fwd_kernel<<<grid_for(n / 8, kThreads * 4), kThreads, 0, st>>>(x, n / 8, y);
+  RFK_CHECK_LAUNCH(launch_k(relu_fwd_kernel, grid_for(n / 8, kThreads * 4), kThreads, 0, st, x, n / 8, y));
   return cudaGetLastError();
 }
 
 cudaError_t relu_bwd(const __nv_bfloat16* y, const __nv_bfloat16* dy, long n, __nv_bfloat16* dx, bool acc,
                      cudaStream_t st) {
-  relu_bwd_kernel<<<grid_for(n / 8, kThreads * 4), kThreads, 0, st>>>(y, dy, n / 8, dx, acc ? 1 : 0);
+  RFK_CHECK_LAUNCH(launch_k(relu_bwd_kernel, grid_for(n / 8, kThreads * 4), kThreads, 0, st, y, dy, n / 8, dx, acc ? 1 : 0));
   return cudaGetLastError();
 }
 
 cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st) {
   const long work = (long)g.N * g.P * g.Q * (g.C / 8);
-  maxpool_fwd_kernel<<<grid_for(work, kThreads * 2), kThreads, 0, st>>>(x, g, y);
+  RFK_CHECK_LAUNCH(launch_k(maxpool_fwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y));
+  return cudaGetLastError();
+}
+
+cudaError_t avgpool2d_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st) {
+  if (g.C % 8) return cudaErrorInvalidValue;
+  const long work = (long)g.N * g.P * g.Q * (g.C / 8);
+  RFK_CHECK_LAUNCH(launch_k(avgpool2d_fwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y));
+  return cudaGetLastError();
+}
+
+cudaError_t avgpool2d_bwd(const __nv_bfloat16* dy, const PoolGeom& g, __nv_bfloat16* dx, bool acc, cudaStream_t st) {
+  if (g.C % 8) return cudaErrorInvalidValue;
+  const long work = (long)g.N * g.H * g.W * (g.C / 8);
+  RFK_CHECK_LAUNCH(launch_k(avgpool2d_bwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, dy, g, dx, acc ? 1 : 0));
   return cudaGetLastError();
 }
 
@@ -1106,99 +1236,99 @@ cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __
   if (g.k * g.k > 256) return cudaErrorInvalidValue;
   uint8_t* idx = static_cast<uint8_t*>(idx_ws);
   const long wins = (long)g.N * g.P * g.Q * (g.C / 8);
-  maxpool_argmax_kernel<<<grid_for(wins, kThreads * 2), kThreads, 0, st>>>(x, g, idx);
+  RFK_CHECK_LAUNCH(launch_k(maxpool_argmax_kernel, grid_for(wins, kThreads * 2), kThreads, 0, st, x, g, idx));
   const long work = (long)g.N * g.H * g.W * (g.C / 8);
-  maxpool_bwd_kernel<<<grid_for(work, kThreads * 2), kThreads, 0, st>>>(idx, dy, g, dx, acc ? 1 : 0);
+  RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx, acc ? 1 : 0));
   return cudaGetLastError();
 }
 
 cudaError_t avgpool_fwd(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, cudaStream_t st) {
-  avgpool_fwd_kernel<<<dim3(N, (C + kThreads - 1) / kThreads), kThreads, 0, st>>>(x, HW, C, out);
+  RFK_CHECK_LAUNCH(launch_k(avgpool_fwd_kernel, dim3(N, (C + kThreads - 1) / kThreads), kThreads, 0, st, x, HW, C, out));
   return cudaGetLastError();
 }
 
 cudaError_t avgpool_bwd(const __nv_bfloat16* dout, int N, int HW, int C, __nv_bfloat16* dx, bool acc,
                         cudaStream_t st) {
   const long nvec = (long)N * HW * C / 8;
-  avgpool_bwd_kernel<<<grid_for(nvec, kThreads * 4), kThreads, 0, st>>>(dout, HW, C, nvec, dx, acc ? 1 : 0);
+  RFK_CHECK_LAUNCH(launch_k(avgpool_bwd_kernel, grid_for(nvec, kThreads * 4), kThreads, 0, st, dout, HW, C, nvec, dx, acc ? 1 : 0));
   return cudaGetLastError();
 }
 
 cudaError_t softmax_ce_fwd(const float* logits, const int* labels, int N, int K, float* row_loss, float* lse,
                            float* loss, cudaStream_t st) {
-  softmax_ce_fwd_kernel<<<N, kThreads, 0, st>>>(logits, labels, K, row_loss, lse);
-  mean_kernel<<<1, kThreads, 0, st>>>(row_loss, N, loss);
+  RFK_CHECK_LAUNCH(launch_k(softmax_ce_fwd_kernel, N, kThreads, 0, st, logits, labels, K, row_loss, lse));
+  RFK_CHECK_LAUNCH(launch_k(mean_kernel, 1, kThreads, 0, st, row_loss, N, loss));
   return cudaGetLastError();
 }
 
 cudaError_t softmax_ce_bwd(const float* logits, const int* labels, const float* lse, int N, int K, float* dlogits,
                            cudaStream_t st) {
-  softmax_ce_bwd_kernel<<<grid_for((long)N * K, kThreads), kThreads, 0, st>>>(logits, labels, lse, N, K, dlogits);
+  RFK_CHECK_LAUNCH(launch_k(softmax_ce_bwd_kernel, grid_for((long)N * K, kThreads), kThreads, 0, st, logits, labels, lse, N, K, dlogits));
   return cudaGetLastError();
 }
 
 cudaError_t cast_f32_bf16(const float* x, long n, __nv_bfloat16* y, cudaStream_t st) {
-  cast_f32_bf16_kernel<<<grid_for(n, kThreads * 4), kThreads, 0, st>>>(x, n, y);
+  RFK_CHECK_LAUNCH(launch_k(cast_f32_bf16_kernel, grid_for(n, kThreads * 4), kThreads, 0, st, x, n, y));
   return cudaGetLastError();
 }
 
 cudaError_t cast_f32_bf16_vec(const float* x, long n, __nv_bfloat16* y, cudaStream_t st) {
   if (n % 8) return cudaErrorInvalidValue;
-  cast_f32_bf16_vec_kernel<<<grid_for(n / 8, kThreads * 4), kThreads, 0, st>>>(x, n / 8, y);
+  RFK_CHECK_LAUNCH(launch_k(cast_f32_bf16_vec_kernel, grid_for(n / 8, kThreads * 4), kThreads, 0, st, x, n / 8, y));
   return cudaGetLastError();
 }
 
 cudaError_t cast_f32_bf16_2d(const float* x, int R, int C, int ldo, __nv_bfloat16* y, cudaStream_t st) {
-  cast_f32_bf16_2d_kernel<<<grid_for((long)R * C, kThreads * 4), kThreads, 0, st>>>(x, R, C, ldo, y);
+  RFK_CHECK_LAUNCH(launch_k(cast_f32_bf16_2d_kernel, grid_for((long)R * C, kThreads * 4), kThreads, 0, st, x, R, C, ldo, y));
   return cudaGetLastError();
 }
 
 cudaError_t colsum_bf16(const __nv_bfloat16* x, int R, int C, float* out, bool acc, cudaStream_t st) {
-  colsum_bf16_kernel<<<(C + kThreads - 1) / kThreads, kThreads, 0, st>>>(x, R, C, out, acc ? 1 : 0);
+  RFK_CHECK_LAUNCH(launch_k(colsum_bf16_kernel, (C + kThreads - 1) / kThreads, kThreads, 0, st, x, R, C, out, acc ? 1 : 0));
   return cudaGetLastError();
 }
 
 cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaStream_t st) {
-  colsum_f32_kernel<<<(C + kThreads - 1) / kThreads, kThreads, 0, st>>>(x, R, C, out, acc ? 1 : 0);
+  RFK_CHECK_LAUNCH(launch_k(colsum_f32_kernel, (C + kThreads - 1) / kThreads, kThreads, 0, st, x, R, C, out, acc ? 1 : 0));
   return cudaGetLastError();
 }
 
 cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bool acc, cudaStream_t st) {
   if (n % 4) return cudaErrorInvalidValue;
-  reduce_splits_kernel<<<grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st>>>(parts, splits, n / 4, out,
-                                                                               acc ? 1 : 0);
+  RFK_CHECK_LAUNCH(launch_k(reduce_splits_kernel, grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st, parts, splits, n / 4, out,
+                                                                               acc ? 1 : 0));
   return cudaGetLastError();
 }
 
 cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, float momentum, float wd,
                        __nv_bfloat16* wb, cudaStream_t st) {
   if (n % 4) return cudaErrorInvalidValue;
-  sgd_kernel<<<grid_for(n / 4, kThreads * 2), kThreads, 0, st>>>(w, g, m, n / 4, lr, momentum, wd, wb);
+  RFK_CHECK_LAUNCH(launch_k(sgd_kernel, grid_for(n / 4, kThreads * 2), kThreads, 0, st, w, g, m, n / 4, lr, momentum, wd, wb));
   return cudaGetLastError();
 }
 
 cudaError_t conv_weight_prep(const float* w, int Cout, int R, int S, int Cpad, int Cin, int CoutPad,
                              __nv_bfloat16* wb, __nv_bfloat16* wt, cudaStream_t st) {
   const long total = (long)Cout * R * S * Cpad;
-  conv_weight_prep_kernel<<<grid_for(total, kThreads * 4), kThreads, 0, st>>>(w, Cout, R, S, Cpad, Cin, CoutPad, wb,
-                                                                              wt);
+  RFK_CHECK_LAUNCH(launch_k(conv_weight_prep_kernel, grid_for(total, kThreads * 4), kThreads, 0, st, w, Cout, R, S, Cpad, Cin, CoutPad, wb,
+                                                                              wt));
   return cudaGetLastError();
 }
 
 cudaError_t weight_prep_batched(const WeightPrepLayer* table_dev, int layers, long total, cudaStream_t st) {
   if (layers <= 0 || total <= 0) return cudaSuccess;
-  weight_prep_batched_kernel<<<grid_for(total, kThreads * 8, 148 * 16), kThreads, 0, st>>>(table_dev, layers, total);
+  RFK_CHECK_LAUNCH(launch_k(weight_prep_batched_kernel, grid_for(total, kThreads * 8, 148 * 16), kThreads, 0, st, table_dev, layers, total));
   return cudaGetLastError();
 }
 
 cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __nv_bfloat16* out, cudaStream_t st) {
   if (Cpad % 8 == 0) {
     const long work = (long)N * H * W * (Cpad / 8);
-    pack_input_vec_kernel<<<grid_for(work, kThreads * 2), kThreads, 0, st>>>(x, N, C, H, W, Cpad, out);
+    RFK_CHECK_LAUNCH(launch_k(pack_input_vec_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, N, C, H, W, Cpad, out));
     return cudaGetLastError();
   }
   const long total = (long)N * H * W * Cpad;
-  pack_input_kernel<<<grid_for(total, kThreads * 4), kThreads, 0, st>>>(x, N, C, H, W, Cpad, out);
+  RFK_CHECK_LAUNCH(launch_k(pack_input_kernel, grid_for(total, kThreads * 4), kThreads, 0, st, x, N, C, H, W, Cpad, out));
   return cudaGetLastError();
 }
 
@@ -1212,38 +1342,38 @@ cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bf
       attr_set = true;
     }
     const long rows = (long)g.N * g.P;
-    im2col_rows_kernel<<<(int)std::min<long>(rows, 148 * 8), kThreads, rows_smem, st>>>(x, g, Kpad, out);
+    RFK_CHECK_LAUNCH(launch_k(im2col_rows_kernel, (int)std::min<long>(rows, 148 * 8), kThreads, rows_smem, st, x, g, Kpad, out));
     return cudaGetLastError();
   }
   const long total = (long)g.N * g.P * g.Q * (Kpad / 8);
-  im2col_kernel<<<grid_for(total, kThreads * 2, 148 * 32), kThreads, 0, st>>>(x, g, Kpad, out);
+  RFK_CHECK_LAUNCH(launch_k(im2col_kernel, grid_for(total, kThreads * 2, 148 * 32), kThreads, 0, st, x, g, Kpad, out));
   return cudaGetLastError();
 }
 
 cudaError_t zero_insert(const __nv_bfloat16* dy, int N, int P, int Q, int C, int Hu, int Wu, int stride,
                         __nv_bfloat16* u, cudaStream_t st) {
   const long work = (long)N * Hu * Wu * (C / 8);
-  zero_insert_kernel<<<grid_for(work, kThreads * 4), kThreads, 0, st>>>(dy, N, P, Q, C, Hu, Wu, stride, u);
+  RFK_CHECK_LAUNCH(launch_k(zero_insert_kernel, grid_for(work, kThreads * 4), kThreads, 0, st, dy, N, P, Q, C, Hu, Wu, stride, u));
   return cudaGetLastError();
 }
 
 cudaError_t concat(const __nv_bfloat16* a, int Ca, const __nv_bfloat16* b, int Cb, long M, __nv_bfloat16* c,
                    cudaStream_t st) {
   const long work = M * ((Ca + Cb) / 8);
-  concat_kernel<<<grid_for(work, kThreads * 4), kThreads, 0, st>>>(a, Ca, b, Cb, M, c);
+  RFK_CHECK_LAUNCH(launch_k(concat_kernel, grid_for(work, kThreads * 4), kThreads, 0, st, a, Ca, b, Cb, M, c));
   return cudaGetLastError();
 }
 
 cudaError_t split_grad(const __nv_bfloat16* dc, int Ca, int Cb, long M, __nv_bfloat16* da, bool acc_a,
                        __nv_bfloat16* db, bool acc_b, cudaStream_t st) {
   const long work = M * ((Ca + Cb) / 8);
-  split_grad_kernel<<<grid_for(work, kThreads * 4), kThreads, 0, st>>>(dc, Ca, Cb, M, da, acc_a ? 1 : 0, db,
-                                                                       acc_b ? 1 : 0);
+  RFK_CHECK_LAUNCH(launch_k(split_grad_kernel, grid_for(work, kThreads * 4), kThreads, 0, st, dc, Ca, Cb, M, da, acc_a ? 1 : 0, db,
+                                                                       acc_b ? 1 : 0));
   return cudaGetLastError();
 }
 
 cudaError_t add_bf16(const __nv_bfloat16* a, long n, __nv_bfloat16* dst, cudaStream_t st) {
-  add_bf16_kernel<<<grid_for(n / 8, kThreads * 4), kThreads, 0, st>>>(a, n / 8, dst);
+  RFK_CHECK_LAUNCH(launch_k(add_bf16_kernel, grid_for(n / 8, kThreads * 4), kThreads, 0, st, a, n / 8, dst));
   return cudaGetLastError();
 }
 

@@ -33,6 +33,9 @@ cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16
 // idx_ws: N*P*Q*C bytes of scratch (window argmax)
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __nv_bfloat16* dy, const PoolGeom& g,
                         __nv_bfloat16* dx, bool acc, void* idx_ws, cudaStream_t st);
+// windowed average pooling (count_include_pad) and its gather backward
+cudaError_t avgpool2d_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st);
+cudaError_t avgpool2d_bwd(const __nv_bfloat16* dy, const PoolGeom& g, __nv_bfloat16* dx, bool acc, cudaStream_t st);
 cudaError_t avgpool_fwd(const __nv_bfloat16* x, int N, int HW, int C, __nv_bfloat16* out, cudaStream_t st);
 cudaError_t avgpool_bwd(const __nv_bfloat16* dout, int N, int HW, int C, __nv_bfloat16* dx, bool acc,
                         cudaStream_t st);

@@ -13,46 +13,63 @@
 namespace reforward {
 
 // ============================================================ VertexSet
-VertexSet::VertexSet(std::size_t n) : bits_(n), w_((n + 63) / 64, 0) {}
+VertexSet::VertexSet(std::size_t n) : bits_(n), nw_((n + 63) / 64) {
+  if (nw_ > kInline) heap_.reset(new std::uint64_t[nw_]());
+}
 
-void VertexSet::clear() { std::fill(w_.begin(), w_.end(), 0); }
+void VertexSet::clear() { std::fill(data(), data() + nw_, 0); }
 
 std::size_t VertexSet::count() const {
   std::size_t c = 0;
-  for (std::uint64_t x : w_) c += static_cast<std::size_t>(std::popcount(x));
+  const std::uint64_t* w = data();
+  for (std::size_t i = 0; i < nw_; ++i) c += static_cast<std::size_t>(std::popcount(w[i]));
   return c;
 }
 
 bool VertexSet::any() const {
-  return std::any_of(w_.begin(), w_.end(), [](std::uint64_t x) { return x != 0; });
+  const std::uint64_t* w = data();
+  for (std::size_t i = 0; i < nw_; ++i)
+    if (w[i]) return true;
+  return false;
+}
+
+bool VertexSet::operator==(const VertexSet& o) const {
+  return nw_ == o.nw_ && std::memcmp(data(), o.data(), nw_ * sizeof(std::uint64_t)) == 0;
 }
 
 VertexSet& VertexSet::operator|=(const VertexSet& o) {
-  for (std::size_t i = 0; i < w_.size(); ++i) w_[i] |= o.w_[i];
+  std::uint64_t* w = data();
+  const std::uint64_t* v = o.data();
+  for (std::size_t i = 0; i < nw_; ++i) w[i] |= v[i];
   return *this;
 }
 
 VertexSet& VertexSet::operator&=(const VertexSet& o) {
-  for (std::size_t i = 0; i < w_.size(); ++i) w_[i] &= o.w_[i];
+  std::uint64_t* w = data();
+  const std::uint64_t* v = o.data();
+  for (std::size_t i = 0; i < nw_; ++i) w[i] &= v[i];
   return *this;
 }
 
 bool VertexSet::is_subset_of(const VertexSet& o) const {
-  for (std::size_t i = 0; i < w_.size(); ++i)
-    if (w_[i] & ~o.w_[i]) return false;
+  const std::uint64_t *w = data(), *v = o.data();
+  for (std::size_t i = 0; i < nw_; ++i)
+    if (w[i] & ~v[i]) return false;
   return true;
 }
 
 bool VertexSet::intersects(const VertexSet& o) const {
-  for (std::size_t i = 0; i < w_.size(); ++i)
-    if (w_[i] & o.w_[i]) return true;
+  const std::uint64_t *w = data(), *v = o.data();
+  for (std::size_t i = 0; i < nw_; ++i)
+    if (w[i] & v[i]) return true;
   return false;
 }
 
 std::vector<std::uint32_t> VertexSet::to_indices() const {
   std::vector<std::uint32_t> idx;
-  for (std::size_t wi = 0; wi < w_.size(); ++wi)
-    for (std::uint64_t x = w_[wi]; x; x &= x - 1)
+  const std::uint64_t* w = data();
+  for (std::size_t wi = 0; wi < nw_; ++wi)
+    for (std::uint64_t x = w[wi]; x; x &= x - 1)
       idx.push_back(static_cast<std::uint32_t>(wi * 64 + static_cast<std::size_t>(std::countr_zero(x))));
   return idx;
 }
@@ -61,15 +78,16 @@ int VertexSet::compare_lex(const VertexSet& a, const VertexSet& b) {
   // The first index present in exactly one set decides.  The set holding it
   // is smaller unless the other set has nothing at or past that index (then
   // the other set is a proper prefix and sorts first).
-  const std::size_t nw = a.w_.size();
+  const std::size_t nw = a.nw_;
+  const std::uint64_t *aw = a.data(), *bw = b.data();
   for (std::size_t wi = 0; wi < nw; ++wi) {
-    const std::uint64_t d = a.w_[wi] ^ b.w_[wi];
+    const std::uint64_t d = aw[wi] ^ bw[wi];
     if (d == 0) continue;
     const std::uint64_t bit = d & (~d + 1);
-    const VertexSet& holder_missing = (a.w_[wi] & bit) ? b : a;
-    bool more = (holder_missing.w_[wi] & ~(bit - 1)) != 0;
-    for (std::size_t k = wi + 1; !more && k < nw; ++k) more = holder_missing.w_[k] != 0;
-    const bool a_has = (a.w_[wi] & bit) != 0;
+    const std::uint64_t* missing = (aw[wi] & bit) ? bw : aw;
+    bool more = (missing[wi] & ~(bit - 1)) != 0;
+    for (std::size_t k = wi + 1; !more && k < nw; ++k) more = missing[k] != 0;
+    const bool a_has = (aw[wi] & bit) != 0;
     if (a_has) return more ? -1 : 1;
     return more ? 1 : -1;
   }

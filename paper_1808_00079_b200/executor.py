@@ -18,7 +18,8 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 from ._lib import load_library
 
-OP_KINDS = ["input", "conv", "bn", "bn_add_relu", "relu", "maxpool", "avgpool", "fc", "concat", "loss"]
+OP_KINDS = ["input", "conv", "bn", "bn_add_relu", "relu", "maxpool", "avgpool", "fc", "concat", "loss", "avgpool2d",
+            "linear"]
 POLICIES = ("reforward", "store_all", "lcg", "sqrt")
 
 
@@ -47,6 +48,9 @@ _SIGS = {
     "rfx_net_maxpool": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p,
                                   C.POINTER(C.c_int32)]),
     "rfx_net_avgpool": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_avgpool2d": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_char_p,
+                                    C.POINTER(C.c_int32)]),
+    "rfx_net_linear": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
     "rfx_net_fc": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
     "rfx_net_concat": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
     "rfx_net_loss": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
@@ -209,6 +213,12 @@ class ReforwardNet:
 
     def avgpool(self, x, name="avgpool"):
         return self._op(self.L.rfx_net_avgpool, x, name.encode())
+
+    def avgpool2d(self, x, k, stride, pad=0, name="avgpool2d"):
+        return self._op(self.L.rfx_net_avgpool2d, x, k, stride, pad, name.encode())
+
+    def linear(self, x, out_features, name="linear"):
+        return self._op(self.L.rfx_net_linear, x, out_features, name.encode())
 
     def fc(self, x, classes, name="fc"):
         return self._op(self.L.rfx_net_fc, x, classes, name.encode())

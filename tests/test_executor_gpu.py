@@ -24,7 +24,9 @@ pytestmark = pytest.mark.gpu
 
 LOSS_RTOL, LOSS_ATOL, GRAD_RTOL, COS_MIN = 2e-2, 2e-2, 5e-2, 0.9
 
-CASES = [("chain8", 4, 32, 10), ("resnet18", 4, 64, 10), ("resnet50", 2, 64, 16)]
+CASES = [("chain8", 4, 32, 10), ("resnet18", 4, 64, 10), ("resnet50", 2, 64, 16), ("densenet_tiny", 4, 32, 10),
+         ("vgg11", 4, 32, 10), ("alexnet", 4, 64, 10)]
+EXACT_GRADS = ("chain8", "vgg11", "alexnet")  # no batch norm: per-parameter relative error
 
 
 def _run(arch, batch, hw, classes, policy, oracle_weights, x, y):
@@ -56,7 +58,7 @@ def test_parity_with_cpu_oracle_and_bit_identity(arch, batch, hw, classes):
     assert rep_r.tracked_peak == rep_r.planned_total == ref_peak
     assert rep_r.planned_total < rep_s.planned_total
     assert abs(loss_r - ref_loss) <= LOSS_RTOL * abs(ref_loss) + LOSS_ATOL, (loss_r, ref_loss)
-    if arch == "chain8":
+    if arch in EXACT_GRADS:
         worst = max(rel_err(g_r[n], ref_grads[n].numpy()) for n in ref_grads)
         assert worst <= GRAD_RTOL, worst
     else:

@@ -343,7 +343,8 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "imgs/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if ARCH == "resnet50" else METRIC.replace("ResNet-50", ARCH), "value": value,
+            "unit": "imgs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (N,3,224,224) random images + random labels; random-init weights",

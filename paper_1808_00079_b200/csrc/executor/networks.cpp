@@ -176,8 +176,8 @@ void build_named(Net& n, const std::string& arch, int H, int W, int classes) {
                    d161[4] = {6, 12, 36, 24};
   static const int dtiny[4] = {2, 2, 2, 2};
   if (arch == "densenet121") return build_densenet(n, d121, 32, 64, H, W, classes);
-  // same topology at test scale: growth 8, 16 initial features
-  if (arch == "densenet_tiny") return build_densenet(n, dtiny, 8, 16, H, W, classes);
+  // same topology at test scale: two layers per block
+  if (arch == "densenet_tiny") return build_densenet(n, dtiny, 32, 64, H, W, classes);
   if (arch == "densenet169") return build_densenet(n, d169, 32, 64, H, W, classes);
   if (arch == "densenet201") return build_densenet(n, d201, 32, 64, H, W, classes);
   if (arch == "densenet161") return build_densenet(n, d161, 48, 96, H, W, classes);

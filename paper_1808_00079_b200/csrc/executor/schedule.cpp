@@ -107,7 +107,9 @@ int Net::conv(int x, int cout, int R, int S, int stride, int pad, const std::str
   op.cout = cout;
   op.cpad = round64(tx.C);
   op.coutpad = round64(cout);
-  op.explicit_im2col = tx.C < 32;
+  // narrow inputs (the 3-channel image) go through an explicit im2col; a
+  // plain 1x1 stride-1 conv reads any channel count directly
+  op.explicit_im2col = tx.C < 32 && !(R == 1 && S == 1 && stride == 1 && pad == 0);
   op.kpad = op.explicit_im2col ? round64(R * S * op.cin_real) : 0;
   op.out = add_tensor(name, tx.N, P, Q, cout, DType::BF16);
   const int id = add_op(op);

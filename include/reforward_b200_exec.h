@@ -123,6 +123,13 @@ int rfx_net_schedule(const rfx_net* net, int32_t* kinds, int32_t* ops, int32_t* 
 int rfx_net_setup(rfx_net* net, uint64_t seed);
 /* images: NCHW fp32 [batch, C, H, W]; labels int32 [batch]; from_host: 1 host
  * pointers (copied inside the call), 0 device pointers */
+/* Double-buffered input pipeline (slot 0/1): stage_batch copies a host batch
+ * (pinned for overlap) to the slot on copy_stream once the slot's previous
+ * batch was consumed; use_batch makes `stream` wait for it, packs it into the
+ * network input and frees the slot.  Stage batch k+1 while step k runs. */
+int rfx_net_stage_batch(rfx_net* net, const float* images_host, const int32_t* labels_host, int32_t slot,
+                        void* copy_stream);
+int rfx_net_use_batch(rfx_net* net, int32_t slot, void* stream);
 int rfx_net_load_batch(rfx_net* net, const float* images, const int32_t* labels, int32_t from_host,
                        void* stream);
 int rfx_net_forward_backward(rfx_net* net, void* stream);

@@ -219,6 +219,13 @@ int rfx_net_setup(rfx_net* n, uint64_t seed) {
   return guard([&] { n->net->setup(seed); });
 }
 
+int rfx_net_stage_batch(rfx_net* n, const float* images_host, const int32_t* labels_host, int32_t slot,
+                        void* copy_stream) {
+  return guard([&] { n->net->stage_batch(images_host, labels_host, slot, S(copy_stream)); });
+}
+int rfx_net_use_batch(rfx_net* n, int32_t slot, void* st) {
+  return guard([&] { n->net->use_batch(slot, S(st)); });
+}
 int rfx_net_load_batch(rfx_net* n, const float* images, const int32_t* labels, int32_t from_host, void* st) {
   return guard([&] { n->net->load_batch(images, labels, from_host != 0, S(st)); });
 }

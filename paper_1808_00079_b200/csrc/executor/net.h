@@ -147,6 +147,13 @@ class Net {
   // ---------------------------------------------------------- runtime
   void setup(uint64_t seed);  // allocate device memory, init parameters
   void load_batch(const float* images, const int* labels, bool from_host, cudaStream_t st);
+  // Double-buffered input pipeline: stage_batch copies a host batch (pinned
+  // for overlap) into staging slot 0/1 on `copy_st` once the slot's previous
+  // batch has been consumed; use_batch makes `st` wait for the slot, packs it
+  // into the network input and releases the slot.  Staging batch k+1 while
+  // step k runs hides the host->device copy behind the step.
+  void stage_batch(const float* images_host, const int* labels_host, int slot, cudaStream_t copy_st);
+  void use_batch(int slot, cudaStream_t st);
   void forward_backward(cudaStream_t st);  // loss + gradients (no update)
   void update(float lr, float momentum, float wd, cudaStream_t st);  // SGD + weight prep
   void step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph);
@@ -254,6 +261,10 @@ class Net {
   float* d_state_ = nullptr;
   __nv_bfloat16* d_input_ = nullptr;
   float* d_images_ = nullptr;
+  float* d_stage_images_[2] = {nullptr, nullptr};
+  int* d_stage_labels_[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ready_[2] = {nullptr, nullptr}, stage_free_[2] = {nullptr, nullptr};
+  void ensure_staging();
   int* d_labels_ = nullptr;
   float* d_loss_ = nullptr;
   float* d_rowloss_ = nullptr;

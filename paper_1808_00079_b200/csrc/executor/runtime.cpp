@@ -46,6 +46,15 @@ void Net::free_device() {
   gemm_trace_.clear();
   if (d_prep_table_) cudaFree(d_prep_table_);
   d_prep_table_ = nullptr;
+  for (int k = 0; k < 2; ++k) {
+    if (d_stage_images_[k]) cudaFree(d_stage_images_[k]);
+    if (d_stage_labels_[k]) cudaFree(d_stage_labels_[k]);
+    if (stage_ready_[k]) cudaEventDestroy(stage_ready_[k]);
+    if (stage_free_[k]) cudaEventDestroy(stage_free_[k]);
+    d_stage_images_[k] = nullptr;
+    d_stage_labels_[k] = nullptr;
+    stage_ready_[k] = stage_free_[k] = nullptr;
+  }
   for (void* p : {(void*)d_arena_, (void*)d_grad_arena_, (void*)d_ws_, (void*)d_param_, (void*)d_grad_,
                   (void*)d_mom_, (void*)d_bf16_, (void*)d_state_, (void*)d_input_, (void*)d_images_,
                   (void*)d_labels_, (void*)d_loss_, (void*)d_rowloss_, (void*)d_lse_, (void*)d_hyper_})
@@ -719,6 +728,39 @@ void Net::load_batch(const float* images, const int* labels, bool from_host, cud
                         st),
         "labels");
   check(rfk::pack_input(src, batch_, in_c_real_, in.H, in.W, in.C, d_input_, st), "pack_input");
+}
+
+void Net::ensure_staging() {
+  if (d_stage_images_[0]) return;
+  const Tensor& in = tensors_[input_t_];
+  const long nimg = (long)batch_ * in_c_real_ * in.H * in.W;
+  for (int s = 0; s < 2; ++s) {
+    check(cudaMalloc(&d_stage_images_[s], nimg * 4), "staging images");
+    check(cudaMalloc(&d_stage_labels_[s], batch_ * 4), "staging labels");
+    check(cudaEventCreateWithFlags(&stage_ready_[s], cudaEventDisableTiming), "event");
+    check(cudaEventCreateWithFlags(&stage_free_[s], cudaEventDisableTiming), "event");
+  }
+}
+
+void Net::stage_batch(const float* images_host, const int* labels_host, int slot, cudaStream_t copy_st) {
+  if (!setup_done_) throw std::invalid_argument("setup the network first");
+  if (slot < 0 || slot > 1) throw std::invalid_argument("staging slot must be 0 or 1");
+  ensure_staging();
+  const Tensor& in = tensors_[input_t_];
+  const long nimg = (long)batch_ * in_c_real_ * in.H * in.W;
+  check(cudaStreamWaitEvent(copy_st, stage_free_[slot], 0), "wait");  // previous batch of the slot consumed
+  check(cudaMemcpyAsync(d_stage_images_[slot], images_host, nimg * 4, cudaMemcpyHostToDevice, copy_st), "h2d");
+  check(cudaMemcpyAsync(d_stage_labels_[slot], labels_host, batch_ * 4, cudaMemcpyHostToDevice, copy_st), "h2d");
+  check(cudaEventRecord(stage_ready_[slot], copy_st), "event");
+}
+
+void Net::use_batch(int slot, cudaStream_t st) {
+  if (slot < 0 || slot > 1 || !d_stage_images_[slot]) throw std::invalid_argument("slot was never staged");
+  const Tensor& in = tensors_[input_t_];
+  check(cudaStreamWaitEvent(st, stage_ready_[slot], 0), "wait");
+  check(cudaMemcpyAsync(d_labels_, d_stage_labels_[slot], batch_ * 4, cudaMemcpyDeviceToDevice, st), "labels");
+  check(rfk::pack_input(d_stage_images_[slot], batch_, in_c_real_, in.H, in.W, in.C, d_input_, st), "pack_input");
+  check(cudaEventRecord(stage_free_[slot], st), "event");
 }
 
 void Net::set_comm(int nranks, int rank, const char id[128], long bucket_bytes) {

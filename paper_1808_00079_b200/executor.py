@@ -69,6 +69,8 @@ _SIGS = {
     "rfx_net_schedule": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
     "rfx_net_setup": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "rfx_net_stage_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "rfx_net_use_batch": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "rfx_net_load_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "rfx_net_forward_backward": (C.c_int, [C.c_void_p, C.c_void_p]),
     "rfx_net_update": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_void_p]),
@@ -103,6 +105,16 @@ _SIGS = {
 }
 
 _bound = None
+
+
+def torch_float32():
+    import torch
+    return torch.float32
+
+
+def torch_int32():
+    import torch
+    return torch.int32
 
 
 def _lib():
@@ -321,6 +333,17 @@ class ReforwardNet:
         lb = np.ascontiguousarray(labels, dtype=np.int32)
         _check(self.L.rfx_net_load_batch(self.h, im.ctypes.data_as(C.c_void_p), lb.ctypes.data_as(C.c_void_p), 1,
                                          _stream(stream)))
+
+    def stage_batch(self, images, labels, slot: int, copy_stream=None) -> None:
+        """Async H2D of a host batch (pinned torch tensors) into staging slot 0/1 on copy_stream."""
+        assert not images.is_cuda and images.dtype == torch_float32() and images.is_contiguous()
+        assert labels.dtype == torch_int32() and labels.is_contiguous()
+        _check(self.L.rfx_net_stage_batch(self.h, C.c_void_p(images.data_ptr()), C.c_void_p(labels.data_ptr()),
+                                          slot, _stream(copy_stream)))
+
+    def use_batch(self, slot: int, stream=None) -> None:
+        """Make `stream` wait for staging slot `slot`, pack it into the input, free the slot."""
+        _check(self.L.rfx_net_use_batch(self.h, slot, _stream(stream)))
 
     def forward_backward(self, stream=None) -> None:
         _check(self.L.rfx_net_forward_backward(self.h, _stream(stream)))

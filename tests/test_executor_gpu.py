@@ -121,3 +121,29 @@ def test_bn_running_stats_update_once_per_step():
     torch.cuda.synchronize()
     m2, v2 = net2.read_bn_running(bn_ops[0].id)
     assert np.array_equal(m, m2) and np.array_equal(v, v2)
+
+
+def test_staged_batches_match_load_batch():
+    """Double-buffered staging (stage_batch on a copy stream + use_batch) feeds
+    the step exactly like load_batch."""
+    net = ReforwardNet.named("resnet18", 4, 32, 32, 10)
+    net.plan("reforward")
+    net.setup(seed=4)
+    batches = [random_batch(net, seed=s) for s in (1, 2, 3)]
+    ref = []
+    for x, y in batches:
+        net.load_batch(x, y)
+        net.forward_backward()
+        torch.cuda.synchronize()
+        ref.append(net.read_loss())
+    copy = torch.cuda.Stream()
+    pinned = [(x.pin_memory(), y.pin_memory()) for x, y in batches]
+    net.stage_batch(*pinned[0], 0, copy_stream=copy)
+    got = []
+    for k in range(3):
+        if k + 1 < 3:
+            net.stage_batch(*pinned[k + 1], (k + 1) % 2, copy_stream=copy)
+        net.use_batch(k % 2)
+        net.forward_backward()
+        got.append(net.read_loss())
+    assert got == ref

@@ -62,6 +62,9 @@ void rfx_net_free(rfx_net* net);
 int rfx_net_input(rfx_net* net, int32_t H, int32_t W, int32_t C, int32_t* out);
 int rfx_net_conv(rfx_net* net, int32_t x, int32_t cout, int32_t R, int32_t S, int32_t stride, int32_t pad,
                  const char* name, int32_t* out);
+/* convolution with rectangular padding (pad_h, pad_w); stride 1 unless square */
+int rfx_net_conv2(rfx_net* net, int32_t x, int32_t cout, int32_t R, int32_t S, int32_t stride, int32_t pad_h,
+                  int32_t pad_w, const char* name, int32_t* out);
 int rfx_net_bn(rfx_net* net, int32_t y, int32_t relu, const char* name, int32_t* out);
 int rfx_net_bn_add_relu(rfx_net* net, int32_t y, int32_t skip, const char* name, int32_t* out);
 int rfx_net_relu(rfx_net* net, int32_t x, const char* name, int32_t* out);
@@ -85,6 +88,7 @@ int32_t rfx_net_num_ops(const rfx_net* net);
 int rfx_net_op_info(const rfx_net* net, int32_t op, char* name, size_t name_cap, int32_t* kind,
                     int32_t* inputs /* up to 2, -1 pads */, int32_t* out);
 /* attrs[8] = {R, S, stride, pad, k (pool window / bn relu flag), classes, cin_real, cout} */
+/* attrs[9] = {R, S, stride, pad_h, k, classes, cin_real, cout, pad_w} */
 int rfx_net_op_attrs(const rfx_net* net, int32_t op, int32_t* attrs);
 int64_t rfx_net_flops_per_step(const rfx_net* net);
 

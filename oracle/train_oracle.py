@@ -106,7 +106,7 @@ class OracleNet:
         a = self.attrs[op.id]
         if k == "conv":
             w = self.rb(self.weights[op.name + ".weight"])
-            return F.conv2d(ins[0], w, stride=a["stride"], padding=a["pad"])
+            return F.conv2d(ins[0], w, stride=a["stride"], padding=(a["pad"], a["pad_w"]))
         if k in ("bn", "bn_add_relu"):
             y = ins[0]
             mean = y.mean(dim=(0, 2, 3), keepdim=True)

@@ -69,6 +69,10 @@ int rfx_net_conv(rfx_net* n, int32_t x, int32_t cout, int32_t R, int32_t S_, int
                  const char* name, int32_t* out) {
   return guard([&] { *out = n->net->conv(x, cout, R, S_, stride, pad, nm(name)); });
 }
+int rfx_net_conv2(rfx_net* n, int32_t x, int32_t cout, int32_t R, int32_t S_, int32_t stride, int32_t pad_h,
+                  int32_t pad_w, const char* name, int32_t* out) {
+  return guard([&] { *out = n->net->conv2(x, cout, R, S_, stride, pad_h, pad_w, nm(name)); });
+}
 int rfx_net_bn(rfx_net* n, int32_t y, int32_t relu, const char* name, int32_t* out) {
   return guard([&] { *out = n->net->bn(y, relu != 0, nm(name)); });
 }
@@ -147,6 +151,7 @@ int rfx_net_op_attrs(const rfx_net* n, int32_t o, int32_t* a) {
     a[5] = op.classes;
     a[6] = op.cin_real;
     a[7] = op.cout;
+    a[8] = op.kind == rfx::OpKind::Conv ? op.pad_w : op.pad;
   });
 }
 

@@ -69,7 +69,8 @@ struct Op {
   std::vector<int> in;
   int out = -1;
   // conv
-  int R = 1, S = 1, stride = 1, pad = 0;
+  int R = 1, S = 1, stride = 1, pad = 0;  // pad = height padding (and width unless pad_w is set)
+  int pad_w = 0;
   int cin = 0, cin_real = 0, cout = 0, cpad = 0, coutpad = 0;
   bool explicit_im2col = false;
   int kpad = 0;              // explicit im2col K (padded)
@@ -125,6 +126,8 @@ class Net {
   // ---------------------------------------------------------- building
   int input(int H, int W, int C);  // NCHW fp32 images -> NHWC bf16 (C padded to 8)
   int conv(int x, int cout, int R, int S, int stride, int pad, const std::string& name);
+  // rectangular padding (Inception's 1x7 / 7x1 / 1x3 / 3x1 convolutions)
+  int conv2(int x, int cout, int R, int S, int stride, int pad_h, int pad_w, const std::string& name);
   int bn(int y, bool relu, const std::string& name);
   int bn_add_relu(int y, int skip, const std::string& name);
   int relu(int x, const std::string& name);

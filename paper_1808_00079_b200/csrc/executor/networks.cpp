@@ -171,7 +171,107 @@ void build_alexnet(Net& n, int H, int W, int classes) {
   n.loss(x, "loss");
 }
 
+namespace {
+// Inception's BasicConv2d: conv (no bias) + BN + ReLU, rectangular padding
+int bconv(Net& n, int x, int c, int R, int S, int stride, int ph, int pw, const std::string& name) {
+  const int y = n.conv2(x, c, R, S, stride, ph, pw, name + ".conv");
+  return n.bn(y, true, name + ".bn");
+}
+// torch.cat([...], 1) of the branches as a chain of two-input concats
+int cat(Net& n, const std::vector<int>& xs, const std::string& name) {
+  int x = xs[0];
+  for (size_t i = 1; i < xs.size(); ++i) x = n.concat(x, xs[i], name + ".cat" + std::to_string(i));
+  return x;
+}
+int inception_a(Net& n, int x, int pool_features, const std::string& nm) {
+  const int b1 = bconv(n, x, 64, 1, 1, 1, 0, 0, nm + ".branch1x1");
+  int b5 = bconv(n, x, 48, 1, 1, 1, 0, 0, nm + ".branch5x5_1");
+  b5 = bconv(n, b5, 64, 5, 5, 1, 2, 2, nm + ".branch5x5_2");
+  int b3 = bconv(n, x, 64, 1, 1, 1, 0, 0, nm + ".branch3x3dbl_1");
+  b3 = bconv(n, b3, 96, 3, 3, 1, 1, 1, nm + ".branch3x3dbl_2");
+  b3 = bconv(n, b3, 96, 3, 3, 1, 1, 1, nm + ".branch3x3dbl_3");
+  int bp = n.avgpool2d(x, 3, 1, 1, nm + ".branch_pool.avg");
+  bp = bconv(n, bp, pool_features, 1, 1, 1, 0, 0, nm + ".branch_pool");
+  return cat(n, {b1, b5, b3, bp}, nm);
+}
+int inception_b(Net& n, int x, const std::string& nm) {
+  const int b3 = bconv(n, x, 384, 3, 3, 2, 0, 0, nm + ".branch3x3");
+  int bd = bconv(n, x, 64, 1, 1, 1, 0, 0, nm + ".branch3x3dbl_1");
+  bd = bconv(n, bd, 96, 3, 3, 1, 1, 1, nm + ".branch3x3dbl_2");
+  bd = bconv(n, bd, 96, 3, 3, 2, 0, 0, nm + ".branch3x3dbl_3");
+  const int bp = n.maxpool(x, 3, 2, 0, nm + ".branch_pool");
+  return cat(n, {b3, bd, bp}, nm);
+}
+int inception_c(Net& n, int x, int c7, const std::string& nm) {
+  const int b1 = bconv(n, x, 192, 1, 1, 1, 0, 0, nm + ".branch1x1");
+  int b7 = bconv(n, x, c7, 1, 1, 1, 0, 0, nm + ".branch7x7_1");
+  b7 = bconv(n, b7, c7, 1, 7, 1, 0, 3, nm + ".branch7x7_2");
+  b7 = bconv(n, b7, 192, 7, 1, 1, 3, 0, nm + ".branch7x7_3");
+  int bd = bconv(n, x, c7, 1, 1, 1, 0, 0, nm + ".branch7x7dbl_1");
+  bd = bconv(n, bd, c7, 7, 1, 1, 3, 0, nm + ".branch7x7dbl_2");
+  bd = bconv(n, bd, c7, 1, 7, 1, 0, 3, nm + ".branch7x7dbl_3");
+  bd = bconv(n, bd, c7, 7, 1, 1, 3, 0, nm + ".branch7x7dbl_4");
+  bd = bconv(n, bd, 192, 1, 7, 1, 0, 3, nm + ".branch7x7dbl_5");
+  int bp = n.avgpool2d(x, 3, 1, 1, nm + ".branch_pool.avg");
+  bp = bconv(n, bp, 192, 1, 1, 1, 0, 0, nm + ".branch_pool");
+  return cat(n, {b1, b7, bd, bp}, nm);
+}
+int inception_d(Net& n, int x, const std::string& nm) {
+  int b3 = bconv(n, x, 192, 1, 1, 1, 0, 0, nm + ".branch3x3_1");
+  b3 = bconv(n, b3, 320, 3, 3, 2, 0, 0, nm + ".branch3x3_2");
+  int b7 = bconv(n, x, 192, 1, 1, 1, 0, 0, nm + ".branch7x7x3_1");
+  b7 = bconv(n, b7, 192, 1, 7, 1, 0, 3, nm + ".branch7x7x3_2");
+  b7 = bconv(n, b7, 192, 7, 1, 1, 3, 0, nm + ".branch7x7x3_3");
+  b7 = bconv(n, b7, 192, 3, 3, 2, 0, 0, nm + ".branch7x7x3_4");
+  const int bp = n.maxpool(x, 3, 2, 0, nm + ".branch_pool");
+  return cat(n, {b3, b7, bp}, nm);
+}
+int inception_e(Net& n, int x, const std::string& nm) {
+  const int b1 = bconv(n, x, 320, 1, 1, 1, 0, 0, nm + ".branch1x1");
+  const int b3 = bconv(n, x, 384, 1, 1, 1, 0, 0, nm + ".branch3x3_1");
+  const int b3a = bconv(n, b3, 384, 1, 3, 1, 0, 1, nm + ".branch3x3_2a");
+  const int b3b = bconv(n, b3, 384, 3, 1, 1, 1, 0, nm + ".branch3x3_2b");
+  const int b3c = cat(n, {b3a, b3b}, nm + ".branch3x3");
+  int bd = bconv(n, x, 448, 1, 1, 1, 0, 0, nm + ".branch3x3dbl_1");
+  bd = bconv(n, bd, 384, 3, 3, 1, 1, 1, nm + ".branch3x3dbl_2");
+  const int bda = bconv(n, bd, 384, 1, 3, 1, 0, 1, nm + ".branch3x3dbl_3a");
+  const int bdb = bconv(n, bd, 384, 3, 1, 1, 1, 0, nm + ".branch3x3dbl_3b");
+  const int bdc = cat(n, {bda, bdb}, nm + ".branch3x3dbl");
+  int bp = n.avgpool2d(x, 3, 1, 1, nm + ".branch_pool.avg");
+  bp = bconv(n, bp, 192, 1, 1, 1, 0, 0, nm + ".branch_pool");
+  return cat(n, {b1, b3c, bdc, bp}, nm);
+}
+}  // namespace
+
+// torchvision Inception-v3 (Szegedy et al. 2016), training graph without the
+// auxiliary classifier and dropout; BN eps 1e-5 like every BN here.
+void build_inception3(Net& n, int H, int W, int classes) {
+  int x = n.input(H, W, 3);
+  x = bconv(n, x, 32, 3, 3, 2, 0, 0, "Conv2d_1a_3x3");
+  x = bconv(n, x, 32, 3, 3, 1, 0, 0, "Conv2d_2a_3x3");
+  x = bconv(n, x, 64, 3, 3, 1, 1, 1, "Conv2d_2b_3x3");
+  x = n.maxpool(x, 3, 2, 0, "maxpool1");
+  x = bconv(n, x, 80, 1, 1, 1, 0, 0, "Conv2d_3b_1x1");
+  x = bconv(n, x, 192, 3, 3, 1, 0, 0, "Conv2d_4a_3x3");
+  x = n.maxpool(x, 3, 2, 0, "maxpool2");
+  x = inception_a(n, x, 32, "Mixed_5b");
+  x = inception_a(n, x, 64, "Mixed_5c");
+  x = inception_a(n, x, 64, "Mixed_5d");
+  x = inception_b(n, x, "Mixed_6a");
+  x = inception_c(n, x, 128, "Mixed_6b");
+  x = inception_c(n, x, 160, "Mixed_6c");
+  x = inception_c(n, x, 160, "Mixed_6d");
+  x = inception_c(n, x, 192, "Mixed_6e");
+  x = inception_d(n, x, "Mixed_7a");
+  x = inception_e(n, x, "Mixed_7b");
+  x = inception_e(n, x, "Mixed_7c");
+  x = n.avgpool(x, "avgpool");
+  x = n.fc(x, classes, "fc");
+  n.loss(x, "loss");
+}
+
 void build_named(Net& n, const std::string& arch, int H, int W, int classes) {
+  if (arch == "inception_v3") return build_inception3(n, H, W, classes);
   static const int d121[4] = {6, 12, 24, 16}, d169[4] = {6, 12, 32, 32}, d201[4] = {6, 12, 48, 32},
                    d161[4] = {6, 12, 36, 24};
   static const int dtiny[4] = {2, 2, 2, 2};

@@ -291,6 +291,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       d.b_kind = rfk::Operand::KMajor2D;
       d.b = d_bf16_ + w.bf16_off;
       if (op.explicit_im2col) {
+        if (op.pad != op.pad_w) throw std::runtime_error("explicit im2col needs square padding");
         rfk::ConvShape cs{x.N, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
         check(rfk::im2col(tb(op.in[0]), cs, op.kpad, ws_im2col, st), "im2col");
         d.a_kind = rfk::Operand::KMajor2D;
@@ -298,7 +299,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         d.a_ld = op.kpad;
         d.K = op.kpad;
         d.b_ld = op.kpad;
-      } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0) {
+      } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0 && op.pad_w == 0) {
         d.a_kind = rfk::Operand::KMajor2D;
         d.a = tptr(op.in[0]);
         d.a_ld = op.cin;
@@ -307,7 +308,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       } else {
         d.a_kind = rfk::Operand::Im2colK;
         d.a = tptr(op.in[0]);
-        d.a_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad, op.stride, op.stride};
+        d.a_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad_w, op.stride, op.stride};
         d.K = op.R * op.S * op.cpad;
         d.b_ld = (long)op.R * op.S * op.cpad;
       }
@@ -457,7 +458,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         d.out = dx;
         d.ldc = op.cin;
         d.accumulate_out = acc(0);
-        if (op.R == 1 && op.S == 1 && op.pad == 0) {
+        if (op.R == 1 && op.S == 1 && op.pad == 0 && op.pad_w == 0) {
           d.M = (int)y.rows();
           d.K = op.cout;
           d.a_kind = rfk::Operand::KMajor2D;
@@ -483,10 +484,10 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           d.b_cpad = op.cpad;
           d.b_rows = op.cout;
           d.a_kind = rfk::Operand::Im2colK;
-          const int pd = op.R - 1 - op.pad;
+          const int pd = op.R - 1 - op.pad, pdw = op.S - 1 - op.pad_w;
           if (op.stride == 1) {
             d.a = dy;
-            d.a_geom = rfk::ConvGeom{y.N, y.H, y.W, op.cout, x.H, x.W, op.R, op.S, pd, pd, 1, 1};
+            d.a_geom = rfk::ConvGeom{y.N, y.H, y.W, op.cout, x.H, x.W, op.R, op.S, pd, pdw, 1, 1};
           } else {
             const int Hu = x.H - op.R + 1 + 2 * op.pad, Wu = x.W - op.S + 1 + 2 * op.pad;
             check(rfk::zero_insert(dy, y.N, y.H, y.W, op.cout, Hu, Wu, op.stride, ws_zero, st), "zero_insert");
@@ -515,7 +516,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         d.b_kind = rfk::Operand::MNMajor2D;
         d.b = ws_im2col;
         d.b_ld = op.kpad;
-      } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0) {
+      } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0 && op.pad_w == 0) {
         d.b_kind = rfk::Operand::MNMajor2D;
         d.b = tptr(op.in[0]);
         d.b_ld = op.cin;
@@ -523,7 +524,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       } else {
         d.b_kind = rfk::Operand::Im2colMN;
         d.b = tptr(op.in[0]);
-        d.b_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad, op.stride, op.stride};
+        d.b_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad_w, op.stride, op.stride};
       }
       if (op.wg_splits > 1) {
         // split-K partials in the workspace, summed in split order by a

@@ -89,10 +89,16 @@ int Net::input(int H, int W, int C) {
 }
 
 int Net::conv(int x, int cout, int R, int S, int stride, int pad, const std::string& name) {
+  return conv2(x, cout, R, S, stride, pad, pad, name);
+}
+
+int Net::conv2(int x, int cout, int R, int S, int stride, int pad, int pad_w, const std::string& name) {
   const Tensor& tx = tensors_.at(x);
   require(tx.dtype == DType::BF16, "conv input must be bf16");
   require(cout % 8 == 0, "conv output channels must be a multiple of 8");
-  const int P = (tx.H + 2 * pad - R) / stride + 1, Q = (tx.W + 2 * pad - S) / stride + 1;
+  require(pad >= 0 && pad_w >= 0 && pad < R && pad_w < S, "conv padding must be smaller than the filter");
+  require(stride == 1 || pad == pad_w, "strided convolutions need square padding");
+  const int P = (tx.H + 2 * pad - R) / stride + 1, Q = (tx.W + 2 * pad_w - S) / stride + 1;
   require(P > 0 && Q > 0, "conv output is empty");
   Op op;
   op.kind = OpKind::Conv;
@@ -102,6 +108,7 @@ int Net::conv(int x, int cout, int R, int S, int stride, int pad, const std::str
   op.S = S;
   op.stride = stride;
   op.pad = pad;
+  op.pad_w = pad_w;
   op.cin = tx.C;
   op.cin_real = (x == input_t_) ? in_c_real_ : tx.C;
   op.cout = cout;
@@ -109,7 +116,7 @@ int Net::conv(int x, int cout, int R, int S, int stride, int pad, const std::str
   op.coutpad = round64(cout);
   // narrow inputs (the 3-channel image) go through an explicit im2col; a
   // plain 1x1 stride-1 conv reads any channel count directly
-  op.explicit_im2col = tx.C < 32 && !(R == 1 && S == 1 && stride == 1 && pad == 0);
+  op.explicit_im2col = tx.C < 32 && !(R == 1 && S == 1 && stride == 1 && pad == 0 && pad_w == 0);
   op.kpad = op.explicit_im2col ? round64(R * S * op.cin_real) : 0;
   op.out = add_tensor(name, tx.N, P, Q, cout, DType::BF16);
   const int id = add_op(op);
@@ -670,7 +677,7 @@ void Net::layout() {
       if (op.explicit_im2col) ws_im2col_ = std::max(ws_im2col_, align_up(y.rows() * op.kpad * 2));
       if (op.stride > 1 && op.R > 1)
         ws_zero_ = std::max(ws_zero_, align_up((long)x.N * (x.H - op.R + 1 + 2 * op.pad) *
-                                               (x.W - op.S + 1 + 2 * op.pad) * op.cout * 2));
+                                               (x.W - op.S + 1 + 2 * op.pad_w) * op.cout * 2));
       const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
       op.wg_bn = kw <= 64 ? 64 : (kw <= 128 ? 128 : 256);
       const long tiles = ((op.cout + 127) / 128) * ((kw + op.wg_bn - 1) / op.wg_bn);

@@ -452,14 +452,14 @@ __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat
                                                               __nv_bfloat16* __restrict__ y) {
   pdl_enter();
   const int cv = g.C / 8;
-  const long total = (long)g.N * g.P * g.Q * cv;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const int c8 = (int)(i % cv);
-    long t = i / cv;
-    const int q = (int)(t % g.Q);
-    t /= g.Q;
-    const int p = (int)(t % g.P);
-    const int n = (int)(t / g.P);
+  const unsigned total = (unsigned)g.N * g.P * g.Q * cv;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % (unsigned)cv);
+    unsigned t = i / (unsigned)cv;
+    const int q = (int)(t % (unsigned)g.Q);
+    t /= (unsigned)g.Q;
+    const int p = (int)(t % (unsigned)g.P);
+    const int n = (int)(t / (unsigned)g.P);
     float m[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) m[k] = -INFINITY;
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat
         for (int k = 0; k < 8; ++k) m[k] = fmaxf(m[k], f[k]);
       }
     }
-    *reinterpret_cast<uint4*>(y + i * 8) = pack8(m);
+    *reinterpret_cast<uint4*>(y + (size_t)i * 8) = pack8(m);
   }
 }
 
@@ -485,15 +485,15 @@ __global__ void __launch_bounds__(kThreads) avgpool2d_fwd_kernel(const __nv_bflo
                                                                 __nv_bfloat16* __restrict__ y) {
   pdl_enter();
   const int cv = g.C / 8;
-  const long total = (long)g.N * g.P * g.Q * cv;
+  const unsigned total = (unsigned)g.N * g.P * g.Q * cv;
   const float inv = 1.f / (float)(g.k * g.k);
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const int c8 = (int)(i % cv);
-    long t = i / cv;
-    const int q = (int)(t % g.Q);
-    t /= g.Q;
-    const int p = (int)(t % g.P);
-    const int n = (int)(t / g.P);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % (unsigned)cv);
+    unsigned t = i / (unsigned)cv;
+    const int q = (int)(t % (unsigned)g.Q);
+    t /= (unsigned)g.Q;
+    const int p = (int)(t % (unsigned)g.P);
+    const int n = (int)(t / (unsigned)g.P);
     float m[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) m[k] = 0.f;
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kThreads) avgpool2d_fwd_kernel(const __nv_bflo
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) m[k] *= inv;
-    *reinterpret_cast<uint4*>(y + i * 8) = pack8(m);
+    *reinterpret_cast<uint4*>(y + (size_t)i * 8) = pack8(m);
   }
 }
 
@@ -521,15 +521,15 @@ __global__ void __launch_bounds__(kThreads) avgpool2d_bwd_kernel(const __nv_bflo
                                                                 __nv_bfloat16* __restrict__ dx, int acc) {
   pdl_enter();
   const int cv = g.C / 8;
-  const long total = (long)g.N * g.H * g.W * cv;
+  const unsigned total = (unsigned)g.N * g.H * g.W * cv;
   const float inv = 1.f / (float)(g.k * g.k);
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const int c8 = (int)(i % cv);
-    long t = i / cv;
-    const int w = (int)(t % g.W);
-    t /= g.W;
-    const int h = (int)(t % g.H);
-    const int n = (int)(t / g.H);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % (unsigned)cv);
+    unsigned t = i / (unsigned)cv;
+    const int w = (int)(t % (unsigned)g.W);
+    t /= (unsigned)g.W;
+    const int h = (int)(t % (unsigned)g.H);
+    const int n = (int)(t / (unsigned)g.H);
     // windows p with p*stride - pad <= h < p*stride - pad + k
     const int p0 = max(0, (h + g.pad - g.k + g.stride) / g.stride), p1 = min(g.P - 1, (h + g.pad) / g.stride);
     const int q0 = max(0, (w + g.pad - g.k + g.stride) / g.stride), q1 = min(g.Q - 1, (w + g.pad) / g.stride);
@@ -547,11 +547,11 @@ __global__ void __launch_bounds__(kThreads) avgpool2d_bwd_kernel(const __nv_bflo
     for (int k = 0; k < 8; ++k) m[k] *= inv;
     if (acc) {
       float prev[8];
-      unpack8(*reinterpret_cast<const uint4*>(dx + i * 8), prev);
+      unpack8(*reinterpret_cast<const uint4*>(dx + (size_t)i * 8), prev);
 #pragma unroll
       for (int k = 0; k < 8; ++k) m[k] += prev[k];
     }
-    *reinterpret_cast<uint4*>(dx + i * 8) = pack8(m);
+    *reinterpret_cast<uint4*>(dx + (size_t)i * 8) = pack8(m);
   }
 }
 
@@ -561,14 +561,14 @@ __global__ void __launch_bounds__(kThreads) maxpool_argmax_kernel(const __nv_bfl
                                                                  uint8_t* __restrict__ idx) {
   pdl_enter();
   const int cv = g.C / 8;
-  const long total = (long)g.N * g.P * g.Q * cv;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const int c8 = (int)(i % cv);
-    long t = i / cv;
-    const int q = (int)(t % g.Q);
-    t /= g.Q;
-    const int p = (int)(t % g.P);
-    const int n = (int)(t / g.P);
+  const unsigned total = (unsigned)g.N * g.P * g.Q * cv;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % (unsigned)cv);
+    unsigned t = i / (unsigned)cv;
+    const int q = (int)(t % (unsigned)g.Q);
+    t /= (unsigned)g.Q;
+    const int p = (int)(t % (unsigned)g.P);
+    const int n = (int)(t / (unsigned)g.P);
     float m[8];
     uint32_t best[8];
 #pragma unroll
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(kThreads) maxpool_argmax_kernel(const __nv_bfl
     uint2 o;
     o.x = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
     o.y = best[4] | (best[5] << 8) | (best[6] << 16) | (best[7] << 24);
-    *reinterpret_cast<uint2*>(idx + i * 8) = o;
+    *reinterpret_cast<uint2*>(idx + (size_t)i * 8) = o;
   }
 }
 
@@ -606,14 +606,14 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __
                                                               __nv_bfloat16* __restrict__ dx, int acc) {
   pdl_enter();
   const int cv = g.C / 8;
-  const long total = (long)g.N * g.H * g.W * cv;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const int c8 = (int)(i % cv);
-    long t = i / cv;
-    const int w = (int)(t % g.W);
-    t /= g.W;
-    const int h = (int)(t % g.H);
-    const int n = (int)(t / g.H);
+  const unsigned total = (unsigned)g.N * g.H * g.W * cv;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % (unsigned)cv);
+    unsigned t = i / (unsigned)cv;
+    const int w = (int)(t % (unsigned)g.W);
+    t /= (unsigned)g.W;
+    const int h = (int)(t % (unsigned)g.H);
+    const int n = (int)(t / (unsigned)g.H);
     float sum[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) sum[k] = 0.f;
@@ -637,11 +637,11 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __
       }
     if (acc) {
       float pv[8];
-      unpack8(*reinterpret_cast<const uint4*>(dx + i * 8), pv);
+      unpack8(*reinterpret_cast<const uint4*>(dx + (size_t)i * 8), pv);
 #pragma unroll
       for (int k = 0; k < 8; ++k) sum[k] += pv[k];
     }
-    *reinterpret_cast<uint4*>(dx + i * 8) = pack8(sum);
+    *reinterpret_cast<uint4*>(dx + (size_t)i * 8) = pack8(sum);
   }
 }
 
@@ -1027,17 +1027,23 @@ __global__ void __launch_bounds__(kThreads) im2col_rows_kernel(const __nv_bfloat
       reinterpret_cast<uint4*>(rows_s)[i] = v;
     }
     __syncthreads();
+    // each thread owns one 8-wide K group (its 8 gather offsets stay in
+    // registers) and walks the output pixels; consecutive threads write
+    // consecutive 16-byte vectors of a pixel's K row
     uint4* o = reinterpret_cast<uint4*>(out + rowid * g.Q * Kpad);
-    for (int i = threadIdx.x; i < g.Q * kv; i += blockDim.x) {
-      const int q = i / kv, k0 = (i % kv) * 8;
-      const unsigned short* px = rows_s + q * g.stride * g.Cs;
-      uint32_t e[8];
+    const int step = blockDim.x / kv;
+    if ((int)threadIdx.x < step * kv) {
+      const int kg = threadIdx.x % kv;
+      int off[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int off = ktab[k0 + j];
-        e[j] = off >= 0 ? px[off] : 0u;
+      for (int j = 0; j < 8; ++j) off[j] = ktab[kg * 8 + j];
+      for (int q = threadIdx.x / kv; q < g.Q; q += step) {
+        const unsigned short* px = rows_s + q * g.stride * g.Cs;
+        uint32_t e[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) e[j] = off[j] >= 0 ? px[off[j]] : 0u;
+        o[q * kv + kg] = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16), e[6] | (e[7] << 16));
       }
-      o[i] = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16), e[6] | (e[7] << 16));
     }
   }
 }
@@ -1211,12 +1217,14 @@ cudaError_t relu_bwd(const __nv_bfloat16* y, const __nv_bfloat16* dy, long n, __
 }
 
 cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st) {
+  if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   const long work = (long)g.N * g.P * g.Q * (g.C / 8);
   RFK_CHECK_LAUNCH(launch_k(maxpool_fwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y));
   return cudaGetLastError();
 }
 
 cudaError_t avgpool2d_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st) {
+  if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   if (g.C % 8) return cudaErrorInvalidValue;
   const long work = (long)g.N * g.P * g.Q * (g.C / 8);
   RFK_CHECK_LAUNCH(launch_k(avgpool2d_fwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y));
@@ -1224,6 +1232,7 @@ cudaError_t avgpool2d_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat
 }
 
 cudaError_t avgpool2d_bwd(const __nv_bfloat16* dy, const PoolGeom& g, __nv_bfloat16* dx, bool acc, cudaStream_t st) {
+  if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   if (g.C % 8) return cudaErrorInvalidValue;
   const long work = (long)g.N * g.H * g.W * (g.C / 8);
   RFK_CHECK_LAUNCH(launch_k(avgpool2d_bwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, dy, g, dx, acc ? 1 : 0));
@@ -1232,6 +1241,7 @@ cudaError_t avgpool2d_bwd(const __nv_bfloat16* dy, const PoolGeom& g, __nv_bfloa
 
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __nv_bfloat16* dy, const PoolGeom& g,
                         __nv_bfloat16* dx, bool acc, void* idx_ws, cudaStream_t st) {
+  if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   (void)y;
   if (g.k * g.k > 256) return cudaErrorInvalidValue;
   uint8_t* idx = static_cast<uint8_t*>(idx_ws);
@@ -1335,7 +1345,7 @@ cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __n
 cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st) {
   if (Kpad % 8) return cudaErrorInvalidValue;
   const long rows_smem = (long)g.R * (g.W + 2 * g.pad) * g.Cs * 2 + (long)Kpad * 4;
-  if (g.Cs % 8 == 0 && rows_smem <= 96 * 1024) {
+  if (g.Cs % 8 == 0 && rows_smem <= 96 * 1024 && Kpad / 8 <= kThreads) {
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(im2col_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);

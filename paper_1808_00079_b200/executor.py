@@ -42,6 +42,7 @@ _SIGS = {
     "rfx_net_input": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]),
     "rfx_net_conv": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                C.c_char_p, C.POINTER(C.c_int32)]),
+    "rfx_net_conv2": (C.c_int, [C.c_void_p] + [C.c_int32] * 7 + [C.c_char_p, C.POINTER(C.c_int32)]),
     "rfx_net_bn": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
     "rfx_net_bn_add_relu": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
     "rfx_net_relu": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.POINTER(C.c_int32)]),
@@ -211,6 +212,10 @@ class ReforwardNet:
     def conv(self, x, cout, k, stride=1, pad=0, name="conv", R=None, S=None):
         return self._op(self.L.rfx_net_conv, x, cout, R or k, S or k, stride, pad, name.encode())
 
+    def conv2(self, x, cout, R, S, stride=1, pad_h=0, pad_w=0, name="conv"):
+        """Convolution with rectangular filter and padding (Inception 1x7 / 7x1 / 1x3 / 3x1)."""
+        return self._op(self.L.rfx_net_conv2, x, cout, R, S, stride, pad_h, pad_w, name.encode())
+
     def bn(self, y, relu=True, name="bn"):
         return self._op(self.L.rfx_net_bn, y, int(relu), name.encode())
 
@@ -263,9 +268,9 @@ class ReforwardNet:
         return out
 
     def op_attrs(self, op: int) -> Dict[str, int]:
-        a = (C.c_int32 * 8)()
+        a = (C.c_int32 * 9)()
         _check(self.L.rfx_net_op_attrs(self.h, op, a))
-        return dict(zip(("R", "S", "stride", "pad", "k", "classes", "cin_real", "cout"), list(a)))
+        return dict(zip(("R", "S", "stride", "pad", "k", "classes", "cin_real", "cout", "pad_w"), list(a)))
 
     def graph(self) -> Tuple[List[Tuple[str, int]], List[Tuple[str, str]]]:
         """The tensor graph handed to the planner: (name, cost) vertices, named edges."""
@@ -281,6 +286,47 @@ class ReforwardNet:
     def plan(self, policy: str = "reforward") -> MemoryReport:
         _check(self.L.rfx_net_plan(self.h, policy.encode()))
         return self.report()
+
+    def graph_key(self) -> str:
+        """Hash of the tensor graph the planner sees (names, costs, edges)."""
+        import hashlib
+        verts, edges = self.graph()
+        h = hashlib.sha256()
+        for n, c in verts:
+            h.update(f"{n}:{c};".encode())
+        for a, b in edges:
+            h.update(f"{a}>{b};".encode())
+        return h.hexdigest()
+
+    def plan_cached(self, policy: str, path: str) -> MemoryReport:
+        """plan(policy), memoised in a JSON file keyed by the graph hash.
+
+        A cached plan is replayed with plan_with_stored, which re-scores it
+        (Eq. 1) on the current graph; the stored total must match the cache.
+        Used for graphs whose exact plan takes minutes (Inception-v3)."""
+        import json
+        import os
+        key = self.graph_key()
+        if os.path.exists(path):
+            with open(path) as f:
+                c = json.load(f)
+            if c.get("graph_key") == key and c.get("policy") == policy:
+                names = {t.name: t.id for t in self.tensors()}
+                rep = self.plan_with_stored([names[n] for n in c["stored"]], f"{policy} (cached)")
+                if rep.planned_total != c["planned_total"]:
+                    raise RuntimeError(f"cached plan {path} scores {rep.planned_total}, expected {c['planned_total']}")
+                return rep
+        import time
+        t0 = time.time()
+        rep = self.plan(policy)
+        stored, _ = self.plan_sets()
+        ts = self.tensors()
+        os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+        with open(path, "w") as f:
+            json.dump({"policy": policy, "graph_key": key, "planned_total": rep.planned_total,
+                       "store_all_total": rep.store_all_total, "plan_seconds": time.time() - t0,
+                       "stored": [ts[i].name for i in stored]}, f, indent=0)
+        return rep
 
     def plan_with_stored(self, stored: Sequence[int], label: str = "custom") -> MemoryReport:
         n = self.L.rfx_net_num_tensors(self.h)

@@ -55,6 +55,12 @@ def cases():
     out.append(("2D K-major 6272x512x4608", n * h * h, co, 9 * ci,
                 dict(M=n * h * h, N=co, K=9 * ci, a_kind=K.KMAJOR, a=a3.data_ptr(), a_ld=9 * ci, b_kind=K.KMAJOR,
                      b=wk.data_ptr(), b_ld=9 * ci, out=o2.data_ptr(), ldc=co, splits=1), (a3, wk, o2), {}))
+    # launch + prologue + epilogue floor: one 128x128 tile per SM, one K block
+    Mt = 128 * 148
+    at, bt, ot = bf(Mt, 64), bf(128, 64), bf(Mt, 128)
+    out.append(("floor: 148 tiles, K=64", Mt, 128, 64,
+                dict(M=Mt, N=128, K=64, a_kind=K.KMAJOR, a=at.data_ptr(), a_ld=64, b_kind=K.KMAJOR, b=bt.data_ptr(),
+                     b_ld=64, out=ot.data_ptr(), ldc=128, splits=1), (at, bt, ot), {}))
     # large square 2-D GEMM: the engine's best case
     S = 8192
     a4, b4, o4 = bf(S, S), bf(S, S), bf(S, S)

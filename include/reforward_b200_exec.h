@@ -40,6 +40,7 @@ typedef struct rfx_gemm_args {
   int32_t block_n;
   int64_t b_extent;                  /* valid MN extent of an MN-major B (0 = N) */
   int32_t b_taps, b_cpad, b_rows;    /* kind 4 (conv weights as dgrad B): R*S, Cpad, Cout */
+  int32_t band;                      /* stride-1 im2col A: use the shifted-band kernel when eligible */
 } rfx_gemm_args;
 /* kind 4 = conv weights [Cout][R][S][Cpad] read as the dgrad B operand (flipped taps) */
 
@@ -54,7 +55,7 @@ int rfx_gemm(const rfx_gemm_args* args, void* stream);
 typedef struct rfx_net rfx_net;
 
 int rfx_net_create(int32_t batch, rfx_net** out);
-/* arch: resnet18|resnet34|resnet50|resnet101|resnet152|chain8|vgg16|alexnet|densenet121 */
+/* arch: resnet18..152, densenet121/161/169/201, densenet_tiny, vgg11..19, alexnet, inception_v3, chain8 */
 int rfx_net_create_named(const char* arch, int32_t batch, int32_t H, int32_t W, int32_t classes,
                          rfx_net** out);
 void rfx_net_free(rfx_net* net);

@@ -32,6 +32,7 @@ extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
   d.b_taps = a->b_taps > 0 ? a->b_taps : 1;
   d.b_cpad = a->b_cpad;
   d.b_rows = a->b_rows;
+  d.band = a->band != 0;
   cudaError_t e = rfk::gemm_launch(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     rfexec::set_last_error(std::string("rfx_gemm: ") + cudaGetErrorString(e));

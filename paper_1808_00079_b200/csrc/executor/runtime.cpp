@@ -1,6 +1,7 @@
 // Device side of the executor: arenas, parameters, per-op forward/backward
 // dispatch onto the sm_100a kernels, SGD, CUDA-graph capture of the step.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -13,6 +14,18 @@ namespace rfx {
 
 namespace {
 int round8(int c) { return (c + 7) / 8 * 8; }
+
+// The shifted-band implicit GEMM (gemm_band.cu) is exact (tests/test_gemm_gpu.py)
+// and moves ~5x fewer A bytes than TMA im2col, but measures no faster yet on
+// ResNet-50's 3x3 convs (its per-tile load phase is not bandwidth-bound; see
+// DESIGN.md), so it is opt-in: RFK_BAND=1.
+bool band_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("RFK_BAND");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
 
 float bf16_to_float(uint16_t b) {
   uint32_t u = static_cast<uint32_t>(b) << 16;
@@ -309,6 +322,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         d.a_kind = rfk::Operand::Im2colK;
         d.a = tptr(op.in[0]);
         d.a_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad_w, op.stride, op.stride};
+        d.band = band_enabled();  // opt-in shifted-band kernel for stride-1 shapes (gemm_band.cu)
         d.K = op.R * op.S * op.cpad;
         d.b_ld = (long)op.R * op.S * op.cpad;
       }
@@ -484,6 +498,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           d.b_cpad = op.cpad;
           d.b_rows = op.cout;
           d.a_kind = rfk::Operand::Im2colK;
+          d.band = band_enabled();
           const int pd = op.R - 1 - op.pad, pdw = op.S - 1 - op.pad_w;
           if (op.stride == 1) {
             d.a = dy;

@@ -57,9 +57,14 @@ struct GemmDesc {
   bool remap = false;
   int rP = 0, rQ = 0, rH = 0, rW = 0, rsh = 1, rsw = 1;
   int block_n = 0;  // 0 = pick automatically (64 / 128 / 256)
+  // Im2colK A of a stride-1 conv: use the shifted-band kernel (gemm_band.cu)
+  // when gemm_band_ok() accepts the shape
+  bool band = false;
 };
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream);
+bool gemm_band_ok(const GemmDesc& d);
+cudaError_t gemm_band_launch(const GemmDesc& d, cudaStream_t stream);
 int gemm_m_tiles(const GemmDesc& d);
 int gemm_block_n(const GemmDesc& d);  // tile width the launch will use
 

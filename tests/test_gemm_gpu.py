@@ -197,3 +197,64 @@ def test_gemm_split_partials_isolated():
     K.gemm(args)
     torch.cuda.synchronize()
     _check(out.sum(0), a.float() @ b.float().t())
+
+
+# Shifted-band implicit GEMM (gemm_band.cu): stride-1 convs with Q >= 24, the
+# ResNet / DenseNet / Inception 3x3 (and 1x7 / 7x1) shapes.
+BAND_CASES = [(2, 28, 28, 64, 64, 3, 3, 1, 1), (1, 56, 56, 64, 64, 3, 3, 1, 1), (2, 28, 28, 128, 128, 3, 3, 1, 1),
+              (2, 30, 30, 96, 64, 3, 3, 0, 0), (2, 35, 35, 64, 96, 5, 5, 2, 2), (2, 28, 28, 64, 192, 1, 7, 0, 3),
+              (2, 28, 28, 64, 72, 7, 1, 3, 0), (1, 32, 40, 160, 200, 3, 3, 1, 1)]
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,R,S,ph,pw", BAND_CASES)
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_conv_fprop_band(N, H, W, Ci, Co, R, S, ph, pw, accumulate):
+    x = _bf(N, Ci, H, W, seed=21)
+    w = _bf(Co, Ci, R, S, scale=0.1, seed=22)
+    ref = F.conv2d(x.float(), w.float(), padding=(ph, pw)).permute(0, 2, 3, 1).contiguous()
+    P, Q = H + 2 * ph - R + 1, W + 2 * pw - S + 1
+    cpad = (Ci + 63) // 64 * 64
+    xn = x.permute(0, 2, 3, 1).contiguous()
+    wp = torch.zeros(Co, R, S, cpad, device=dev, dtype=torch.bfloat16)
+    wp[..., :Ci] = w.permute(0, 2, 3, 1)
+    g = K.ConvGeom(N, H, W, Ci, P, Q, R, S, ph, pw, 1, 1)
+    M = N * P * Q
+    base = _bf(N, P, Q, Co, seed=23) if accumulate else torch.zeros(N, P, Q, Co, device=dev, dtype=torch.bfloat16)
+    out = base.clone()
+    stats = torch.zeros(160, 2, Co, device=dev)
+    args = K.GemmArgs(M=M, N=Co, K=R * S * cpad, a_kind=K.IM2COL_K, a=xn.data_ptr(), a_geom=g, b_kind=K.KMAJOR,
+                      b=wp.data_ptr(), b_ld=R * S * cpad, out=out.data_ptr(), ldc=Co, splits=1,
+                      stats=None if accumulate else stats.data_ptr(), accumulate_out=int(accumulate), band=1)
+    K.gemm(args)
+    torch.cuda.synchronize()
+    want = ref + base.float() if accumulate else ref
+    _check(out, want)
+    if not accumulate:
+        r2 = out.float().reshape(M, Co)  # statistics are of the stored bf16 values
+        _check(stats[:, 0].sum(0), r2.sum(0), rtol=1e-3)
+        _check(stats[:, 1].sum(0), (r2 * r2).sum(0), rtol=1e-3)
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,R,pad", [(2, 28, 28, 64, 64, 3, 1), (1, 56, 56, 64, 128, 3, 1),
+                                               (2, 28, 28, 128, 64, 3, 1)])
+def test_conv_dgrad_band(N, H, W, Ci, Co, R, pad):
+    dy = _bf(N, Co, H, W, seed=24)
+    w = _bf(Co, Ci, R, R, scale=0.1, seed=25)
+    ref = torch.nn.grad.conv2d_input((N, Ci, H, W), w.float(), dy.float(), stride=1, padding=pad)
+    ref = ref.permute(0, 2, 3, 1).contiguous()
+    cpad = (Ci + 63) // 64 * 64
+    wp = _pad_w(w, cpad)
+    dyn = dy.permute(0, 2, 3, 1).contiguous()
+    pd = R - 1 - pad
+    ga = K.ConvGeom(N, H, W, Co, H, W, R, R, pd, pd, 1, 1)
+    copad = (Co + 63) // 64 * 64
+    out = torch.zeros(N, H, W, Ci, device=dev, dtype=torch.bfloat16)
+    args = K.GemmArgs(M=N * H * W, N=Ci, K=R * R * copad, a_kind=K.IM2COL_K, a=dyn.data_ptr(), a_geom=ga,
+                      b_kind=4, b=wp.data_ptr(), out=out.data_ptr(), ldc=Ci, splits=1, band=1)
+    args.b_extent = Ci
+    args.b_taps = R * R
+    args.b_cpad = cpad
+    args.b_rows = Co
+    K.gemm(args)
+    torch.cuda.synchronize()
+    _check(out, ref)

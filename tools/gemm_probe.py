@@ -55,6 +55,25 @@ def cases():
     out.append(("2D K-major 6272x512x4608", n * h * h, co, 9 * ci,
                 dict(M=n * h * h, N=co, K=9 * ci, a_kind=K.KMAJOR, a=a3.data_ptr(), a_ld=9 * ci, b_kind=K.KMAJOR,
                      b=wk.data_ptr(), b_ld=9 * ci, out=o2.data_ptr(), ldc=co, splits=1), (a3, wk, o2), {}))
+    # layer-1 3x3 conv (56x56x64 -> 64) on the im2col and the shifted-band paths
+    n1, h1 = 32, 56
+    x1 = bf(n1, h1, h1, 64)
+    w1 = bf(64, 9 * 64)
+    o1 = bf(n1, h1, h1, 64)
+    s1 = torch.zeros(160, 2, 64, device=dev)
+    g1 = K.ConvGeom(n1, h1, h1, 64, h1, h1, 3, 3, 1, 1, 1, 1)
+    for band in (0, 1):
+        out.append((f"3x3 56x56x64 fprop +stats band={band}", n1 * h1 * h1, 64, 576,
+                    dict(M=n1 * h1 * h1, N=64, K=576, a_kind=K.IM2COL_K, a=x1.data_ptr(), a_geom=g1,
+                         b_kind=K.KMAJOR, b=w1.data_ptr(), b_ld=576, out=o1.data_ptr(), ldc=64,
+                         stats=s1.data_ptr(), splits=1, band=band), (x1, w1, o1, s1), {}))
+    # same work without any out-of-bounds columns: 58x58 input, pad 0 -> 56x56
+    x2 = bf(n1, 58, 58, 64)
+    g2 = K.ConvGeom(n1, 58, 58, 64, h1, h1, 3, 3, 0, 0, 1, 1)
+    out.append(("3x3 58x58 pad0 fprop +stats band=1", n1 * h1 * h1, 64, 576,
+                dict(M=n1 * h1 * h1, N=64, K=576, a_kind=K.IM2COL_K, a=x2.data_ptr(), a_geom=g2,
+                     b_kind=K.KMAJOR, b=w1.data_ptr(), b_ld=576, out=o1.data_ptr(), ldc=64,
+                     stats=s1.data_ptr(), splits=1, band=1), (x2, w1, o1, s1), {}))
     # launch + prologue + epilogue floor: one 128x128 tile per SM, one K block
     Mt = 128 * 148
     at, bt, ot = bf(Mt, 64), bf(128, 64), bf(Mt, 128)

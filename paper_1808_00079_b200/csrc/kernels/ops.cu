@@ -195,42 +195,51 @@ __device__ __forceinline__ void ld8f(const float* p, float (&f)[8]) {
 
 // Each thread streams kVec 16-byte vectors per iteration, all loads issued
 // before any math, so every SM keeps enough bytes in flight for HBM.
-constexpr int kVec = 2;
+// Four 16-byte vectors per thread in flight (plus the skip operand), 32-bit
+// indexing, SKIP / RELU resolved at compile time.
+constexpr int kVec = 4;
 
+template <bool SKIP, bool RELU>
 __global__ void __launch_bounds__(kThreads) bn_apply_kernel(const __nv_bfloat16* __restrict__ y,
                                                            const __nv_bfloat16* skip, const float* __restrict__ scale,
-                                                           const float* __restrict__ shift, int relu, long nvec, int C,
+                                                           const float* __restrict__ shift, unsigned nvec, int C,
                                                            __nv_bfloat16* out) {
   pdl_enter();
-  const int cv = C / 8;
-  const long stride = (long)gridDim.x * blockDim.x;
-  for (long v0 = (long)blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * kVec) {
+  const unsigned cv = (unsigned)C / 8;
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned v0 = blockIdx.x * blockDim.x + threadIdx.x; v0 < nvec; v0 += stride * kVec) {
     uint4 yv[kVec], kv[kVec];
 #pragma unroll
     for (int u = 0; u < kVec; ++u) {
-      const long v = v0 + u * stride;
+      const unsigned v = v0 + u * stride;
       if (v < nvec) {
-        yv[u] = ldg16(y + v * 8);
-        if (skip) kv[u] = *reinterpret_cast<const uint4*>(skip + v * 8);
+        yv[u] = ldg16(y + (size_t)v * 8);
+        if (SKIP) kv[u] = *reinterpret_cast<const uint4*>(skip + (size_t)v * 8);
       }
     }
 #pragma unroll
     for (int u = 0; u < kVec; ++u) {
-      const long v = v0 + u * stride;
+      const unsigned v = v0 + u * stride;
       if (v >= nvec) break;
       const int c0 = (int)(v % cv) * 8;
-      float f[8], sc[8], sh[8], k[8];
+      float f[8], sc[8], sh[8];
       unpack8(yv[u], f);
       ld8f(scale + c0, sc);
       ld8f(shift + c0, sh);
-      if (skip) unpack8(kv[u], k);
+      if (SKIP) {
+        float k[8];
+        unpack8(kv[u], k);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float o = fmaf(f[i], sc[i], sh[i]);
-        if (skip) o += k[i];
-        f[i] = relu ? fmaxf(o, 0.f) : o;
+        for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], sc[i], sh[i]) + k[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = fmaf(f[i], sc[i], sh[i]);
       }
-      *reinterpret_cast<uint4*>(out + v * 8) = pack8(f);
+      if (RELU) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = fmaxf(f[i], 0.f);
+      }
+      *reinterpret_cast<uint4*>(out + (size_t)v * 8) = pack8(f);
     }
   }
 }
@@ -794,6 +803,53 @@ __global__ void colsum_f32_kernel(const float* __restrict__ x, int R, int C, flo
 // sum of split-K partials [splits][n] -> out (fixed order)
 // float4 per thread, split loop unrolled by 4 so several loads are in flight;
 // summation order z = 0, 1, ... is fixed (deterministic)
+// Many splits over a small output (the weight gradients of the deep, narrow
+// layers): 8 thread groups per output vector each sum every 8th split, then
+// a fixed pairwise tree in shared memory combines them -- 8x the loads in
+// flight, still one fixed summation order.
+__global__ void __launch_bounds__(kThreads) reduce_splits_grouped_kernel(const float* __restrict__ parts, int splits,
+                                                                        unsigned n4, float* __restrict__ out, int acc) {
+  pdl_enter();
+  __shared__ float4 sh[8][32];
+  const float4* p4 = reinterpret_cast<const float4*>(parts);
+  const unsigned lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const unsigned i = blockIdx.x * 32 + lane;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n4)
+    for (int z = (int)grp; z < splits; z += 8) {
+      const float4 a = __ldg(p4 + (size_t)z * n4 + i);
+      s.x += a.x;
+      s.y += a.y;
+      s.z += a.z;
+      s.w += a.w;
+    }
+  sh[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && i < n4) {
+    float4 r[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) r[g] = sh[g][lane];
+#pragma unroll
+    for (int w = 4; w > 0; w >>= 1)
+#pragma unroll
+      for (int g = 0; g < w; ++g) {
+        r[g].x += r[g + w].x;
+        r[g].y += r[g + w].y;
+        r[g].z += r[g + w].z;
+        r[g].w += r[g + w].w;
+      }
+    float4* o = reinterpret_cast<float4*>(out) + i;
+    if (acc) {
+      const float4 prev = *o;
+      r[0].x += prev.x;
+      r[0].y += prev.y;
+      r[0].z += prev.z;
+      r[0].w += prev.w;
+    }
+    *o = r[0];
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) reduce_splits_kernel(const float* __restrict__ parts, int splits, long n4,
                                                                 float* __restrict__ out, int acc) {
   pdl_enter();
@@ -1162,7 +1218,16 @@ cudaError_t bn_finalize(const float* partials, int parts, int C, long count, con
 cudaError_t bn_apply(const __nv_bfloat16* y, const __nv_bfloat16* skip, const float* scale, const float* shift,
                      bool relu, long M, int C, __nv_bfloat16* out, cudaStream_t st) {
   const long nvec = M * C / 8;
-  RFK_CHECK_LAUNCH(launch_k(bn_apply_kernel, grid_for(nvec, kThreads * 4), kThreads, 0, st, y, skip, scale, shift, relu ? 1 : 0, nvec, C, out));
+  if (nvec >= (1L << 31)) return cudaErrorInvalidValue;
+  const int g = grid_for(nvec, kThreads * kVec, 148 * 8);
+  const unsigned nv = (unsigned)nvec;
+  if (skip) {
+    if (relu) RFK_CHECK_LAUNCH(launch_k(bn_apply_kernel<true, true>, g, kThreads, 0, st, y, skip, scale, shift, nv, C, out));
+    else RFK_CHECK_LAUNCH(launch_k(bn_apply_kernel<true, false>, g, kThreads, 0, st, y, skip, scale, shift, nv, C, out));
+  } else {
+    if (relu) RFK_CHECK_LAUNCH(launch_k(bn_apply_kernel<false, true>, g, kThreads, 0, st, y, skip, scale, shift, nv, C, out));
+    else RFK_CHECK_LAUNCH(launch_k(bn_apply_kernel<false, false>, g, kThreads, 0, st, y, skip, scale, shift, nv, C, out));
+  }
   return cudaGetLastError();
 }
 
@@ -1305,6 +1370,11 @@ cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaS
 
 cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bool acc, cudaStream_t st) {
   if (n % 4) return cudaErrorInvalidValue;
+  if (splits >= 8 && n / 4 < (1L << 31)) {
+    RFK_CHECK_LAUNCH(launch_k(reduce_splits_grouped_kernel, (int)((n / 4 + 31) / 32), kThreads, 0, st, parts, splits,
+                              (unsigned)(n / 4), out, acc ? 1 : 0));
+    return cudaGetLastError();
+  }
   RFK_CHECK_LAUNCH(launch_k(reduce_splits_kernel, grid_for(n / 4, kThreads, 148 * 8), kThreads, 0, st, parts, splits, n / 4, out,
                                                                                acc ? 1 : 0));
   return cudaGetLastError();

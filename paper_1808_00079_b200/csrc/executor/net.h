@@ -77,6 +77,8 @@ struct Op {
   bool fuse_stats = false;   // conv epilogue emits BN partial sums for its consumer
   long stats_off = -1;       // its slot in the statistics workspace (floats)
   int wg_splits = 1, wg_bn = 128;  // wgrad split-K and tile N
+  int fp_splits = 1, fp_bn = 0;    // fprop split-K (bf16 finish kernel) and tile N
+  int dg_splits = 1, dg_bn = 0;    // dgrad split-K and tile N
   // pool
   int k = 1;
   // classifier / linear

@@ -326,8 +326,25 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         d.K = op.R * op.S * op.cpad;
         d.b_ld = (long)op.R * op.S * op.cpad;
       }
-      if (op.fuse_stats && !reforward) d.stats = ws_stats + op.stats_off;
+      float* stats = (op.fuse_stats && !reforward) ? ws_stats + op.stats_off : nullptr;
       trace_flops_ = 2.0 * y.rows() * op.cout * op.R * op.S * op.cin_real;
+      if (op.fp_splits > 1 && d.a_kind == rfk::Operand::Im2colK) {
+        // split-K into fp32 partials, then one pass sums them in split order,
+        // rounds to bf16 and emits the BN statistics rows
+        float* ws_split = reinterpret_cast<float*>(ws + ws_im2col_ + ws_partials_ + ws_zero_);
+        d.splits = op.fp_splits;
+        d.block_n = op.fp_bn;
+        d.out = ws_split;
+        d.out_f32 = true;
+        d.ldc = op.cout;
+        d.split_stride = y.rows() * op.cout;
+        gemm(d, st);
+        check(rfk::reduce_splits_bf16(ws_split, op.fp_splits, (int)y.rows(), op.cout, tb(op.out), op.cout, false, stats,
+                                      (int)kStatRows, st),
+              "reduce_splits_bf16");
+        break;
+      }
+      d.stats = stats;
       gemm(d, st);
       break;
     }
@@ -510,7 +527,23 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
             d.a_geom = rfk::ConvGeom{y.N, Hu, Wu, op.cout, x.H, x.W, op.R, op.S, pd, pd, 1, 1};
           }
         }
-        gemm(d, st);
+        if (op.dg_splits > 1 && d.a_kind == rfk::Operand::Im2colK) {
+          float* ws_split = reinterpret_cast<float*>(ws + ws_im2col_ + ws_partials_ + ws_zero_);
+          const bool accumulate = d.accumulate_out;
+          d.splits = op.dg_splits;
+          d.block_n = op.dg_bn;
+          d.out = ws_split;
+          d.out_f32 = true;
+          d.accumulate_out = false;
+          d.ldc = op.cin;
+          d.split_stride = (long)d.M * op.cin;
+          gemm(d, st);
+          check(rfk::reduce_splits_bf16(ws_split, op.dg_splits, d.M, op.cin, dx, op.cin, accumulate, nullptr,
+                                        (int)kStatRows, st),
+                "reduce_splits_bf16");
+        } else {
+          gemm(d, st);
+        }
       }
       // ---- wgrad
       const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;

@@ -1,6 +1,7 @@
 // Network building, planning (host planner on the tensor graph), the
 // re-forward schedule and the arena layouts.
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <map>
 #include <numeric>
@@ -583,6 +584,33 @@ void Net::build_schedule() {
 namespace {
 // split-K of a weight-gradient GEMM: enough splits for about one persistent
 // wave (148 CTAs), each split keeping >= 8 K blocks, at most 32 partials
+// Split-K for a bf16-output implicit GEMM (conv fprop / dgrad through TMA
+// im2col), from the sweep-fitted cost model of gemm.cu: t = waves * (k blocks
+// * 0.5 us + per-tile b) plus, when split, the fp32 partial round trip
+// (s * M * N * 4 bytes at ~3 TB/s) and one extra launch.  Returns {bn, splits}.
+std::pair<int, int> im2col_split_plan(long M, int N, long kb) {
+  if (const char* e = std::getenv("RFK_NO_SPLITK"); e && std::atoi(e)) return {0, 1};  // diagnostics
+  const long mt = (M + 127) / 128;
+  double best = -1;
+  std::pair<int, int> pick{0, 1};
+  for (int bn : {256, 128, 64}) {
+    if (bn > 64 && N <= bn / 2) continue;
+    const double b = bn == 64 ? 2.5 : (bn == 128 ? 3.5 : 7.0);
+    for (int s : {1, 2, 3, 4, 6, 8}) {
+      if (s > 1 && kb / s < 6) continue;
+      const long tiles = mt * ((N + bn - 1) / bn) * s;
+      const long waves = (tiles + 147) / 148;
+      double t = (double)waves * ((double)((kb + s - 1) / s) * 0.5 + b);
+      if (s > 1) t += (double)s * M * N * 4.0 / 3.0e6 + 3.0;
+      if (best < 0 || t < best - 1e-9) {
+        best = t;
+        pick = {bn, s};
+      }
+    }
+  }
+  return pick;
+}
+
 int wgrad_splits(long tiles, long kblocks) {
   long s = (148 + tiles - 1) / tiles;
   s = std::min(s, std::max(1L, kblocks / 8));
@@ -683,6 +711,30 @@ void Net::layout() {
       const long tiles = ((op.cout + 127) / 128) * ((kw + op.wg_bn - 1) / op.wg_bn);
       op.wg_splits = wgrad_splits(tiles, (y.rows() + 63) / 64);
       if (op.wg_splits > 1) ws_split_ = std::max(ws_split_, align_up((long)op.wg_splits * op.cout * kw * 4));
+      // fprop / dgrad through TMA im2col: split-K when the output tiles are
+      // too few to fill the GPU (the deep 14x14 / 7x7 layers)
+      op.fp_splits = op.dg_splits = 1;
+      op.fp_bn = op.dg_bn = 0;
+      const bool im2col_fwd = !op.explicit_im2col && !(op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0 &&
+                                                        op.pad_w == 0);
+      if (im2col_fwd && op.cout % 4 == 0 && op.cout / 4 <= 256) {
+        const auto pl = im2col_split_plan(y.rows(), op.cout, (long)op.R * op.S * (op.cpad / 64));
+        if (pl.second > 1) {
+          op.fp_bn = pl.first;
+          op.fp_splits = pl.second;
+          ws_split_ = std::max(ws_split_, align_up((long)pl.second * y.rows() * op.cout * 4));
+        }
+      }
+      const bool dgrad_taps = op.in[0] != input_t_ && !op.explicit_im2col && !(op.R == 1 && op.S == 1 &&
+                                                                                op.pad == 0 && op.pad_w == 0);
+      if (dgrad_taps && op.cin % 4 == 0 && op.cin / 4 <= 256) {
+        const auto pl = im2col_split_plan(x.rows(), op.cin, (long)op.R * op.S * (op.coutpad / 64));
+        if (pl.second > 1) {
+          op.dg_bn = pl.first;
+          op.dg_splits = pl.second;
+          ws_split_ = std::max(ws_split_, align_up((long)pl.second * x.rows() * op.cin * 4));
+        }
+      }
       // fused BN statistics slot for this conv
       bool fuse = tensors_[op.out].consumers.size() == 1;
       if (fuse) {

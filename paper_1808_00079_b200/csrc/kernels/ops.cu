@@ -8,6 +8,7 @@
 // re-forward gradients bit-identical to store-all gradients.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels/launch.cuh"
@@ -850,6 +851,90 @@ __global__ void __launch_bounds__(kThreads) reduce_splits_grouped_kernel(const f
   }
 }
 
+// Split-K finish for a bf16 activation output (conv fprop / dgrad of the
+// deep, low-parallelism layers): out[m][c] (+)= bf16(sum_z parts[z][m][c]) in
+// split order, and optionally the BN column sum / sum of squares of the
+// stored bf16 values, one row per block (the conv's statistics slot layout).
+// Block = (N/4 float4 lanes) x row groups over a contiguous row slab.
+__global__ void __launch_bounds__(kThreads) reduce_splits_bf16_kernel(const float* __restrict__ parts, int splits,
+                                                                     int M, int N, int rows_per_block,
+                                                                     __nv_bfloat16* out, long ldc, int acc,
+                                                                     float* __restrict__ stats) {
+  pdl_enter();
+  __shared__ float4 shs[kThreads], shq[kThreads];
+  const int lanes = N / 4, groups = kThreads / lanes;
+  const int t = threadIdx.x, lane = t % lanes, grp = t / lanes;
+  const long MN4 = (long)M * lanes;
+  const float4* p4 = reinterpret_cast<const float4*>(parts);
+  float4 cs = make_float4(0.f, 0.f, 0.f, 0.f), cq = cs;
+  const int r0 = blockIdx.x * rows_per_block, r1 = min(M, r0 + rows_per_block);
+  if (grp < groups) {
+    for (int r = r0 + grp; r < r1; r += groups) {
+      const long i = (long)r * lanes + lane;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int z = 0; z < splits; ++z) {
+        const float4 a = __ldg(p4 + (long)z * MN4 + i);
+        s.x += a.x;
+        s.y += a.y;
+        s.z += a.z;
+        s.w += a.w;
+      }
+      __nv_bfloat16* o = out + (long)r * ldc + lane * 4;
+      if (acc) {
+        const uint2 pv = *reinterpret_cast<const uint2*>(o);
+        const float2 p0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pv.x));
+        const float2 p1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pv.y));
+        s.x += p0.x;
+        s.y += p0.y;
+        s.z += p1.x;
+        s.w += p1.y;
+      }
+      const __nv_bfloat162 b0 = __floats2bfloat162_rn(s.x, s.y), b1 = __floats2bfloat162_rn(s.z, s.w);
+      uint2 ov;
+      ov.x = *reinterpret_cast<const uint32_t*>(&b0);
+      ov.y = *reinterpret_cast<const uint32_t*>(&b1);
+      *reinterpret_cast<uint2*>(o) = ov;
+      if (stats) {
+        const float2 f0 = __bfloat1622float2(b0), f1 = __bfloat1622float2(b1);
+        cs.x += f0.x;
+        cs.y += f0.y;
+        cs.z += f1.x;
+        cs.w += f1.y;
+        cq.x = fmaf(f0.x, f0.x, cq.x);
+        cq.y = fmaf(f0.y, f0.y, cq.y);
+        cq.z = fmaf(f1.x, f1.x, cq.z);
+        cq.w = fmaf(f1.y, f1.y, cq.w);
+      }
+    }
+  }
+  if (!stats) return;
+  shs[t] = cs;
+  shq[t] = cq;
+  __syncthreads();
+  if (grp == 0) {
+    for (int g = 1; g < groups; ++g) {
+      const float4 a = shs[g * lanes + lane], b = shq[g * lanes + lane];
+      cs.x += a.x;
+      cs.y += a.y;
+      cs.z += a.z;
+      cs.w += a.w;
+      cq.x += b.x;
+      cq.y += b.y;
+      cq.z += b.z;
+      cq.w += b.w;
+    }
+    float* row = stats + (long)blockIdx.x * 2 * N + lane * 4;
+    row[0] = cs.x;
+    row[1] = cs.y;
+    row[2] = cs.z;
+    row[3] = cs.w;
+    row[N + 0] = cq.x;
+    row[N + 1] = cq.y;
+    row[N + 2] = cq.z;
+    row[N + 3] = cq.w;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) reduce_splits_kernel(const float* __restrict__ parts, int splits, long n4,
                                                                 float* __restrict__ out, int acc) {
   pdl_enter();
@@ -1365,6 +1450,19 @@ cudaError_t colsum_bf16(const __nv_bfloat16* x, int R, int C, float* out, bool a
 
 cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaStream_t st) {
   RFK_CHECK_LAUNCH(launch_k(colsum_f32_kernel, (C + kThreads - 1) / kThreads, kThreads, 0, st, x, R, C, out, acc ? 1 : 0));
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_splits_bf16(const float* parts, int splits, int M, int N, __nv_bfloat16* out, long ldc, bool acc,
+                               float* stats, int max_blocks, cudaStream_t st) {
+  if (N % 4 || N / 4 > kThreads || ldc % 4) return cudaErrorInvalidValue;
+  const int groups = kThreads / (N / 4);
+  int blocks = (M + groups * 4 - 1) / (groups * 4);  // >= 4 rows per thread
+  blocks = std::max(1, std::min(blocks, max_blocks));
+  const int rpb = (M + blocks - 1) / blocks;
+  blocks = (M + rpb - 1) / rpb;
+  RFK_CHECK_LAUNCH(launch_k(reduce_splits_bf16_kernel, blocks, kThreads, 0, st, parts, splits, M, N, rpb, out, ldc,
+                            acc ? 1 : 0, stats));
   return cudaGetLastError();
 }
 

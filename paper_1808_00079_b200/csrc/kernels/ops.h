@@ -49,6 +49,10 @@ cudaError_t cast_f32_bf16_vec(const float* x, long n, __nv_bfloat16* y, cudaStre
 cudaError_t cast_f32_bf16_2d(const float* x, int R, int C, int ldo, __nv_bfloat16* y, cudaStream_t st);
 cudaError_t colsum_bf16(const __nv_bfloat16* x, int R, int C, float* out, bool acc, cudaStream_t st);
 cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaStream_t st);
+// split-K finish into a bf16 activation ([M][N] rows, stride ldc), optional
+// BN statistics rows (<= max_blocks rows of [2][N], the conv's stats slot)
+cudaError_t reduce_splits_bf16(const float* parts, int splits, int M, int N, __nv_bfloat16* out, long ldc, bool acc,
+                               float* stats, int max_blocks, cudaStream_t st);
 cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bool acc, cudaStream_t st);
 // wb (optional): bf16 copy of w refreshed in the same pass
 cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, float momentum, float wd,

@@ -13,6 +13,9 @@ probe = ReforwardNet.named(arch, batch, hw, hw, classes)
 probe.plan("reforward")
 o = OracleNet(probe, emulate_bf16=True)
 o.init_weights(seed=11, residual_gamma=0.1)
+if arch in ("vgg11", "alexnet"):
+    last = [op for op in probe.ops() if op.kind == "fc"][-1].name + ".weight"
+    o.weights[last] = o.weights[last] * 0.1
 x, y = random_batch(probe, seed=5)
 stored, seg = probe.plan_sets()
 ref_loss, ref_grads, _ = o.run_step(x, y, probe.schedule(), stored, seg)

@@ -79,6 +79,8 @@ struct Op {
   int wg_splits = 1, wg_bn = 128;  // wgrad split-K and tile N
   int fp_splits = 1, fp_bn = 0;    // fprop split-K (bf16 finish kernel) and tile N
   int dg_splits = 1, dg_bn = 0;    // dgrad split-K and tile N
+  int fused_bn = -1;               // conv: BN op whose re-forward runs in this conv's epilogue
+  bool reforward_in_producer = false;  // BN: re-forwarded by its producing conv's epilogue
   // pool
   int k = 1;
   // classifier / linear

@@ -345,6 +345,15 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         break;
       }
       d.stats = stats;
+      if (reforward && op.fused_bn >= 0) {
+        const Op& bn = ops_[op.fused_bn];
+        const BNState& b = bns_[bn.bn];
+        d.bn_out = tptr(bn.out);
+        d.bn_scale = d_state_ + b.scale;
+        d.bn_shift = d_state_ + b.shift;
+        d.bn_relu = bn.k == 1;
+        d.band = false;
+      }
       gemm(d, st);
       break;
     }
@@ -727,6 +736,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
 }
 
 void Net::run_instr(const Instr& ins, cudaStream_t st) {
+  if (ins.kind == InstrKind::Forward && ins.reforward && ops_[ins.op].reforward_in_producer) return;  // done by the conv
   if (ins.kind == InstrKind::Forward) op_forward(ops_[ins.op], ins.reforward, ins.phase, st);
   else if (ins.kind == InstrKind::Backward) op_backward(ops_[ins.op], st);
 }

@@ -751,6 +751,24 @@ void Net::layout() {
     if (op.kind == OpKind::MaxPool)  // window argmax bytes for the backward (shares the zero-insert region)
       ws_zero_ = std::max(ws_zero_, align_up(tensors_[op.out].elems()));
   }
+  // Re-forward fusion: a conv whose only consumer is a plain BN in the same
+  // segment applies that BN (statistics of the first forward) in its own
+  // epilogue when both are re-forwarded; the BN's re-forward is then a no-op.
+  for (auto& op : ops_) {
+    op.fused_bn = -1;
+    op.reforward_in_producer = false;
+  }
+  for (int o = 0; o < (int)ops_.size(); ++o) {
+    Op& op = ops_[o];
+    if (op.kind != OpKind::Conv || !op.fuse_stats || op.fp_splits > 1) continue;
+    const int b = tensors_[op.out].consumers[0];
+    Op& bn = ops_[b];
+    if (bn.kind != OpKind::BN || bn.out < 0 || op.cout % 8) continue;
+    const int s_y = plan_.seg_of[op.out], s_o = plan_.seg_of[bn.out];
+    if (s_y < 0 || s_o != s_y) continue;
+    op.fused_bn = b;
+    bn.reforward_in_producer = true;
+  }
   for (auto& op : ops_)
     if (op.kind == OpKind::Conv && op.fuse_stats) {
       op.stats_off = ws_stats_ / 4;  // [kStatRows][2][cout]: one row per persistent GEMM CTA

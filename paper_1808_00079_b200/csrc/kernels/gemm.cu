@@ -37,6 +37,7 @@ struct alignas(64) KParams {
   CUtensorMap ta;  // 64-byte aligned, must be first
   CUtensorMap tb;
   CUtensorMap tc;  // output {N, M, splits}: 32x32 bf16 or 16x32 fp32 boxes, SWIZZLE_64B
+  CUtensorMap tc2;  // second bf16 output of the fused BN apply (same geometry)
   int M, N, K;
   int num_kb;          // total K blocks
   int kb_per_split;
@@ -55,6 +56,10 @@ struct alignas(64) KParams {
   int out_mode;  // 0 generic stores, 1 TMA store, 2 TMA reduce-add (accumulate_out)
   int stages;  // smem ring depth (<= Cfg::kStages)
   int m_tiles, n_tiles, splits;  // persistent tile space
+  // fused BatchNorm apply (re-forward): out2 = [relu](bf16(D) * scale + shift)
+  const float* bn_scale;
+  const float* bn_shift;
+  int bn_relu, fuse_bn;
   int experiment;  // tuning only: 2 drop the output, 3 also skip TMEM loads, 4 also skip the MMAs
 };
 
@@ -121,6 +126,8 @@ __device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const 
   if (lane == 0) {
     if (mode == 2)
       tma_reduce_add_3d(&p.tc, b, cx, my, z);
+    else if (mode == 3)
+      tma_store_3d(&p.tc2, b, cx, my, z);
     else
       tma_store_3d(&p.tc, b, cx, my, z);
     bulk_commit();
@@ -150,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     tma_prefetch(&p.ta);
     tma_prefetch(&p.tb);
     if (p.out_mode) tma_prefetch(&p.tc);
+    if (p.fuse_bn) tma_prefetch(&p.tc2);
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -405,6 +413,31 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (mode != 0) {
           sbuf = stg + buf * 2048;
           tma_out(w, col0, my, tc.z);
+          if (p.fuse_bn) {
+            // the BN that consumes this conv, applied to exactly the bf16
+            // values just stored (same expression as bn_apply_kernel)
+            uint32_t w2[16];
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              const int c = col0 + 2 * i;
+              const float4 sc = __ldg(reinterpret_cast<const float4*>(p.bn_scale + c));
+              const float4 sh = __ldg(reinterpret_cast<const float4*>(p.bn_shift + c));
+              const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+              const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i + 1]));
+              float o0 = fmaf(a.x, sc.x, sh.x), o1 = fmaf(a.y, sc.y, sh.y);
+              float o2 = fmaf(b.x, sc.z, sh.z), o3 = fmaf(b.y, sc.w, sh.w);
+              if (p.bn_relu) {
+                o0 = fmaxf(o0, 0.f);
+                o1 = fmaxf(o1, 0.f);
+                o2 = fmaxf(o2, 0.f);
+                o3 = fmaxf(o3, 0.f);
+              }
+              w2[i] = row_ok ? pack_bf16(o0, o1) : 0u;
+              w2[i + 1] = row_ok ? pack_bf16(o2, o3) : 0u;
+            }
+            epi_tma_out<C::kStgBufs>(p, stg + buf * 2048, w2, lane, 3, col0, my, tc.z);
+            if (C::kStgBufs == 2) buf ^= 1;
+          }
         } else {
           // generic: stage, then write whole 64-byte row segments with 4
           // lanes per row (8 rows per instruction)
@@ -633,7 +666,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   load_driver_entry_points();
   if (!g_encode_tiled || !g_encode_im2col) return cudaErrorNotSupported;
   if (d.M <= 0 || d.N <= 0) return cudaSuccess;
-  if (d.band && d.a_kind == Operand::Im2colK && gemm_band_ok(d)) return gemm_band_launch(d, stream);
+  if (d.band && !d.bn_out && d.a_kind == Operand::Im2colK && gemm_band_ok(d)) return gemm_band_launch(d, stream);
   const int bn = gemm_block_n(d);
   if (bn != 64 && bn != 128 && bn != 256) return cudaErrorInvalidValue;
   if (d.stats && d.out_f32) return cudaErrorInvalidValue;  // statistics are of the stored bf16 values
@@ -731,6 +764,26 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
                          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
         kp.out_mode = d.accumulate_out ? 2 : 1;
     }
+  }
+  if (d.bn_out) {
+    // fused BN apply: needs the TMA-store epilogue, a plain bf16 output and
+    // 16-byte aligned per-channel parameters
+    if (kp.out_mode != 1 || d.out_f32 || splits > 1 || d.stats || d.N % 8 ||
+        (reinterpret_cast<uintptr_t>(d.bn_out) & 15) || (reinterpret_cast<uintptr_t>(d.bn_scale) & 15) ||
+        (reinterpret_cast<uintptr_t>(d.bn_shift) & 15))
+      return cudaErrorInvalidValue;
+    cuuint64_t dims[3] = {(cuuint64_t)d.N, (cuuint64_t)d.M, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)d.ldc * 2, (cuuint64_t)d.M * d.ldc * 2};
+    cuuint32_t box[3] = {32u, 32u, 1u};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (g_encode_tiled(&kp.tc2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d.bn_out, dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    kp.fuse_bn = 1;
+    kp.bn_scale = d.bn_scale;
+    kp.bn_shift = d.bn_shift;
+    kp.bn_relu = d.bn_relu ? 1 : 0;
   }
   kp.remap = d.remap;
   kp.rP = d.rP;

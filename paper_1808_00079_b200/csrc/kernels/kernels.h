@@ -60,6 +60,12 @@ struct GemmDesc {
   // Im2colK A of a stride-1 conv: use the shifted-band kernel (gemm_band.cu)
   // when gemm_band_ok() accepts the shape
   bool band = false;
+  // fused BatchNorm apply on the bf16 output (re-forward, statistics known):
+  // bn_out = [relu](out * bn_scale + bn_shift), per column
+  void* bn_out = nullptr;
+  const float* bn_scale = nullptr;
+  const float* bn_shift = nullptr;
+  bool bn_relu = false;
 };
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream);

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -39,13 +40,14 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kThreads = 64 + 32 * kEpiWarps + 32;  // + the band fix-up warp (flat mode)
 constexpr int kSmemMax = 232448;
 constexpr int kStaging = kEpiWarps * 2048;
 
 struct alignas(64) BandParams {
   CUtensorMap ta;  // 4-D tiled map over the NHWC input {C, W, H, N}, box {64, Wp, BR, 1}
   CUtensorMap tb;  // weights
+  CUtensorMap ta2;  // flat mode: the input as a 2-D [N*H*W pixels][C] map, box {64, Wp}
   int N;                       // GEMM N (output channels)
   int cblocks, taps, R, S;     // K = taps x cblocks x 64
   int Wp, P, Q, ph, pw, BR;    // plane geometry
@@ -61,8 +63,11 @@ struct alignas(64) BandParams {
   int b_stages;
   int band_stages;  // band ring depth (2..4)
   int row_boxes;   // band as BR one-row boxes instead of one BR-row box (tuning)
+  int flat;        // band rows as 2-D boxes over the flat pixel array + fix-up of the padding lines
+  int H, W;
   int b_resident;  // all taps x chunks of B fit the ring: loaded once per CTA, never released
   int experiment;  // tuning only: 2 drop the output, 4 also skip the MMAs
+  unsigned long long* dbg;  // tuning only: per-tile timestamps of CTA 0
 };
 
 __device__ __forceinline__ uint64_t desc_sw128_rows(uint32_t addr) {
@@ -87,7 +92,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
   float* wsum = reinterpret_cast<float*>(stage_buf + kStaging);
   uint64_t* band_full = reinterpret_cast<uint64_t*>(wsum + kEpiWarps * 2 * HB);
   uint64_t* band_empty = band_full + 4;
-  uint64_t* b_full = band_empty + 4;
+  uint64_t* band_ready = band_empty + 4;  // flat mode: padding lines zeroed
+  uint64_t* b_full = band_ready + 4;
   uint64_t* b_empty = b_full + p.b_stages;
   uint64_t* acc_full = b_empty + p.b_stages;
   uint64_t* acc_empty = acc_full + 2;
@@ -97,11 +103,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
   const int total = p.m_tiles * p.n_tiles;
 
   if (warp == 0 && elect_one()) {
-    tma_prefetch(&p.ta);
+    tma_prefetch(p.flat ? &p.ta2 : &p.ta);
     tma_prefetch(&p.tb);
     for (int s = 0; s < p.band_stages; ++s) {
       mbar_init(&band_full[s], 1);
       mbar_init(&band_empty[s], 1);
+      mbar_init(&band_ready[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
@@ -146,8 +153,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
         const int rho0 = j0 / p.Wp;
         for (int cb = 0; cb < p.cblocks; ++cb) {
           mbar_wait(&band_empty[bs], bph ^ 1);
+          if (p.dbg && blockIdx.x == 0 && t / gridDim.x < 16) p.dbg[(t / gridDim.x) * 4 + 0] = global_ns();
+          if (p.flat) {
+            // one 2-D box of Wp consecutive pixels per band row that lies in
+            // the image; the fix-up warp zeroes the rest
+            int valid = 0;
+            for (int rr = 0; rr < p.BR; ++rr) {
+              const int h = rho0 - p.ph + rr;
+              valid += (h >= 0 && h < p.H) ? 1 : 0;
+            }
+            mbar_arrive_expect_tx(&band_full[bs], (uint32_t)(valid * p.Wp * 128));
+            for (int rr = 0; rr < p.BR; ++rr) {
+              const int h = rho0 - p.ph + rr;
+              if (h < 0 || h >= p.H) continue;
+              tma_load_2d(band + bs * p.band_bytes + rr * p.Wp * 128, &p.ta2, &band_full[bs], cb * 64,
+                          (img * p.H + h) * p.W - p.pw);
+            }
+          } else
           mbar_arrive_expect_tx(&band_full[bs], p.box_bytes);
-          if (p.row_boxes) {  // one {64, Wp, 1, 1} box per band row
+          if (p.flat) {
+          } else if (p.row_boxes) {  // one {64, Wp, 1, 1} box per band row
             for (int rr = 0; rr < p.BR; ++rr)
               tma_load_4d(band + bs * p.band_bytes + rr * p.Wp * 128, &p.ta, &band_full[bs], cb * 64, -p.pw,
                           rho0 - p.ph + rr, img);
@@ -190,10 +215,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
       const int acc = local & 1;
       mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
       tc_fence_after();
+      if (p.dbg && blockIdx.x == 0 && local < 16 && lane_id() == 0) p.dbg[local * 4 + 3] = global_ns();
       const uint32_t d_tmem = tmem + (uint32_t)(acc * kTmemCols);
       for (int cb = 0; cb < p.cblocks; ++cb) {
-        mbar_wait(&band_full[bs], bph);
+        mbar_wait(p.flat ? &band_ready[bs] : &band_full[bs], bph);
         tc_fence_after();
+        if (p.dbg && blockIdx.x == 0 && local < 16 && cb == 0 && lane_id() == 0) p.dbg[local * 4 + 1] = global_ns();
         const uint32_t sa0 = smem_u32(band + bs * p.band_bytes);
         for (int tap = 0; tap < p.taps; ++tap) {
           const int slot = p.b_resident ? cb * p.taps + tap : s;
@@ -225,6 +252,45 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
         if (++bs == p.band_stages) {
           bs = 0;
           bph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 2 + kEpiWarps) {
+    // ------------------------------------------------ band fix-up (flat mode)
+    // Zero the band lines the flat 2-D boxes filled with neighbouring pixels
+    // (columns outside the image) or never loaded (rows outside the image),
+    // then publish the band to the MMA warp.
+    if (p.flat) {
+      const uint32_t lane = lane_id();
+      int bs = 0;
+      uint32_t bph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int mt = t % p.m_tiles;
+        const int j0 = (mt % p.tiles_per_img) * kBM;
+        const int rho0 = j0 / p.Wp;
+        for (int cb = 0; cb < p.cblocks; ++cb) {
+          mbar_wait(&band_full[bs], bph);
+          uint8_t* b0 = band + bs * p.band_bytes;
+          for (int rr = 0; rr < p.BR; ++rr) {
+            const int h = rho0 - p.ph + rr;
+            const bool row_in = h >= 0 && h < p.H;
+            // lines of this row to clear: all of them, or the pad columns
+            const int n_lines = row_in ? (p.Wp - p.W) : p.Wp;
+            for (int i = (int)lane; i < n_lines * 8; i += 32) {
+              const int li = i >> 3, chunk = i & 7;
+              int col;
+              if (!row_in) col = li;
+              else col = li < p.pw ? li : p.W + li;  // [0, pw) and [pw + W, Wp)
+              *reinterpret_cast<uint4*>(b0 + (rr * p.Wp + col) * 128 + chunk * 16) = make_uint4(0u, 0u, 0u, 0u);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&band_ready[bs]);
+          if (++bs == p.band_stages) {
+            bs = 0;
+            bph ^= 1;
+          }
         }
       }
     }
@@ -275,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
       }
       mbar_wait(&acc_full[acc], (local >> 1) & 1);
       tc_fence_after();
+      if (p.dbg && blockIdx.x == 0 && local < 16 && ew == 0 && lane == 0) p.dbg[local * 4 + 2] = global_ns();
       const int jl = j0 + (int)(quarter * 32 + lane);  // this lane's plane position
       const bool row_ok = jl < p.plane && (jl % p.Wp) < p.Q;
 #pragma unroll 1
@@ -405,6 +472,11 @@ cudaError_t band_launch(BandParams& bp, cudaStream_t st) {
     return e ? std::atoi(e) : 0;
   }();
   bp.experiment = experiment;
+  static unsigned long long* dbg = nullptr;
+  if (std::getenv("RFK_BAND_DEBUG")) {
+    if (!dbg) cudaMalloc(&dbg, 64 * 8);
+    bp.dbg = dbg;
+  }
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -413,7 +485,17 @@ cudaError_t band_launch(BandParams& bp, cudaStream_t st) {
     if (sms <= 0) sms = 148;
   }
   const int grid = std::min(bp.m_tiles * bp.n_tiles, sms);
-  return launch_k(gemm_band_kernel<BN>, grid, kThreads, smem, st, bp);
+  cudaError_t e = launch_k(gemm_band_kernel<BN>, grid, kThreads, smem, st, bp);
+  if (bp.dbg && e == cudaSuccess) {  // tuning only: timeline of CTA 0
+    unsigned long long h[64];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, bp.dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 8; ++i)
+      printf("tile %d: band issue %+8.0f  band ready %+8.0f  mma start %+8.0f  epi ready %+8.0f ns\n", i,
+             (double)(h[i * 4 + 0] - h[0]), (double)(h[i * 4 + 1] - h[0]), (double)(h[i * 4 + 3] - h[0]),
+             (double)(h[i * 4 + 2] - h[0]));
+  }
+  return e;
 }
 
 }  // namespace
@@ -421,7 +503,7 @@ cudaError_t band_launch(BandParams& bp, cudaStream_t st) {
 bool gemm_band_ok(const GemmDesc& d) {
   const ConvGeom& g = d.a_geom;
   if (g.stride_h != 1 || g.stride_w != 1 || g.R * g.S < 2) return false;
-  const int Wp = g.W + 2 * g.pad_w;
+  const int Wp = (g.W + 2 * g.pad_w + 7) / 8 * 8;
   if (Wp > 256 || g.Q < 24) return false;  // junk columns (S - 1 of Wp) must stay a small fraction
   const int BR = band_rows(Wp, g.R);
   const int band_bytes = (BR * Wp * 128 + 1023) / 1024 * 1024;
@@ -447,7 +529,11 @@ cudaError_t gemm_band_launch(const GemmDesc& d, cudaStream_t stream) {
   bp.S = g.S;
   bp.taps = g.R * g.S;
   bp.cblocks = (g.C + 63) / 64;
-  bp.Wp = g.W + 2 * g.pad_w;
+  // plane width rounded to a multiple of 8 pixels: the TMA box then covers
+  // whole 1024-byte swizzle atoms per band row (measured: a 58-pixel box row
+  // loads ~5x slower per byte than a 64-pixel one); the extra columns are
+  // out-of-bounds zeros and junk outputs
+  bp.Wp = (g.W + 2 * g.pad_w + 7) / 8 * 8;
   bp.P = g.P;
   bp.Q = g.Q;
   bp.ph = g.pad_h;
@@ -466,6 +552,23 @@ cudaError_t gemm_band_launch(const GemmDesc& d, cudaStream_t stream) {
   {
     cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.N};
     cuuint64_t strides[3] = {(cuuint64_t)g.C * 2, (cuuint64_t)g.W * g.C * 2, (cuuint64_t)g.H * g.W * g.C * 2};
+    static const int flat = [] {
+      const char* e = std::getenv("RFK_BAND_FLAT");  // tuning experiments only
+      return e ? std::atoi(e) : 1;
+    }();
+    bp.flat = flat;
+    bp.H = g.H;
+    bp.W = g.W;
+    {
+      cuuint64_t d2[2] = {(cuuint64_t)g.C, (cuuint64_t)g.N * g.H * g.W};
+      cuuint64_t s2[1] = {(cuuint64_t)g.C * 2};
+      cuuint32_t b2[2] = {64, (cuuint32_t)bp.Wp};
+      cuuint32_t e2[2] = {1, 1};
+      if (g_band_encode(&bp.ta2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(d.a), d2, s2, b2, e2,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
     static const int row_boxes = [] {
       const char* e = std::getenv("RFK_BAND_ROWBOX");  // tuning experiments only
       return e ? std::atoi(e) : 0;

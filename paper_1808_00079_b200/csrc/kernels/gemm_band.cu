@@ -63,6 +63,7 @@ struct alignas(64) BandParams {
   int b_stages;
   int band_stages;  // band ring depth (2..4)
   int row_boxes;   // band as BR one-row boxes instead of one BR-row box (tuning)
+  int prefetch_tiles;  // L2 prefetch distance in tiles of this CTA (0 = off)
   int flat;        // band rows as 2-D boxes over the flat pixel array + fix-up of the padding lines
   int H, W;
   int b_resident;  // all taps x chunks of B fit the ring: loaded once per CTA, never released
@@ -151,6 +152,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
         const int mt = t % p.m_tiles, n0 = (t / p.m_tiles) * BN;
         const int img = mt / p.tiles_per_img, j0 = (mt % p.tiles_per_img) * kBM;
         const int rho0 = j0 / p.Wp;
+        // warm L2 with this CTA's band a few tiles ahead: the band loads are
+        // DRAM-latency bound with only band_stages of them in shared memory
+        if (p.prefetch_tiles > 0) {
+          const int tf = t + p.prefetch_tiles * (int)gridDim.x;
+          if (tf < total) {
+            const int mf = tf % p.m_tiles;
+            const int imf = mf / p.tiles_per_img, jf = (mf % p.tiles_per_img) * kBM;
+            for (int cbf = 0; cbf < p.cblocks; ++cbf)
+              tma_prefetch_l2_4d(&p.ta, cbf * 64, -p.pw, jf / p.Wp - p.ph, imf);
+          }
+        }
         for (int cb = 0; cb < p.cblocks; ++cb) {
           mbar_wait(&band_empty[bs], bph ^ 1);
           if (p.dbg && blockIdx.x == 0 && t / gridDim.x < 16) p.dbg[(t / gridDim.x) * 4 + 0] = global_ns();
@@ -503,7 +515,7 @@ cudaError_t band_launch(BandParams& bp, cudaStream_t st) {
 bool gemm_band_ok(const GemmDesc& d) {
   const ConvGeom& g = d.a_geom;
   if (g.stride_h != 1 || g.stride_w != 1 || g.R * g.S < 2) return false;
-  const int Wp = (g.W + 2 * g.pad_w + 7) / 8 * 8;
+  const int Wp = g.W + 2 * g.pad_w;
   if (Wp > 256 || g.Q < 24) return false;  // junk columns (S - 1 of Wp) must stay a small fraction
   const int BR = band_rows(Wp, g.R);
   const int band_bytes = (BR * Wp * 128 + 1023) / 1024 * 1024;
@@ -529,11 +541,7 @@ cudaError_t gemm_band_launch(const GemmDesc& d, cudaStream_t stream) {
   bp.S = g.S;
   bp.taps = g.R * g.S;
   bp.cblocks = (g.C + 63) / 64;
-  // plane width rounded to a multiple of 8 pixels: the TMA box then covers
-  // whole 1024-byte swizzle atoms per band row (measured: a 58-pixel box row
-  // loads ~5x slower per byte than a 64-pixel one); the extra columns are
-  // out-of-bounds zeros and junk outputs
-  bp.Wp = (g.W + 2 * g.pad_w + 7) / 8 * 8;
+  bp.Wp = g.W + 2 * g.pad_w;  // (rounding it up to 8 pixels measured slower)
   bp.P = g.P;
   bp.Q = g.Q;
   bp.ph = g.pad_h;
@@ -554,9 +562,14 @@ cudaError_t gemm_band_launch(const GemmDesc& d, cudaStream_t stream) {
     cuuint64_t strides[3] = {(cuuint64_t)g.C * 2, (cuuint64_t)g.W * g.C * 2, (cuuint64_t)g.H * g.W * g.C * 2};
     static const int flat = [] {
       const char* e = std::getenv("RFK_BAND_FLAT");  // tuning experiments only
-      return e ? std::atoi(e) : 1;
+      return e ? std::atoi(e) : 0;
     }();
     bp.flat = flat;
+    static const int pf = [] {
+      const char* e = std::getenv("RFK_BAND_PREFETCH");  // tuning experiments only (measured: no gain)
+      return e ? std::atoi(e) : 0;
+    }();
+    bp.prefetch_tiles = pf;
     bp.H = g.H;
     bp.W = g.W;
     {

@@ -229,6 +229,8 @@ class Net {
   __nv_bfloat16* tb(int t) const { return static_cast<__nv_bfloat16*>(tptr(t)); }
   __nv_bfloat16* gptr(int t) const;
   void gemm(const rfk::GemmDesc& d, cudaStream_t st);
+  bool wgrad_overlap() const;
+  void ensure_wgrad_stream();
   void check(cudaError_t e, const char* what) const;
   void free_device();
 
@@ -251,7 +253,7 @@ class Net {
   std::vector<int> grad_acc_base_;
   long arena_bytes_ = 0, grad_bytes_ = 0;
   long ws_im2col_ = 0, ws_partials_ = 0, ws_zero_ = 0, ws_split_ = 0, ws_stats_ = 0, ws_misc_ = 0,
-       ws_counters_ = 0;
+       ws_counters_ = 0, ws_dsplit_ = 0;
   MemoryReport rep_;
   long launches_ = 0;
   bool counting_ = false;
@@ -282,6 +284,10 @@ class Net {
   cudaGraphExec_t phase_exec_[3] = {nullptr, nullptr, nullptr};
   std::unique_ptr<NcclComm> comm_;
   cudaStream_t comm_stream_ = nullptr;
+  // conv backward: the weight-gradient GEMM runs on a side stream next to the
+  // data-gradient GEMM (fork / join inside the step graph)
+  cudaStream_t wgrad_stream_ = nullptr;
+  cudaEvent_t wgrad_fork_ = nullptr, wgrad_join_ = nullptr;
   struct Bucket {
     int after_instr;  // launch once this schedule instruction has been enqueued
     long lo, hi;      // float range of the gradient buffer

@@ -43,6 +43,9 @@ Net::~Net() {
   for (auto e : bucket_events_) cudaEventDestroy(e);
   if (comm_done_) cudaEventDestroy(comm_done_);
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
+  if (wgrad_fork_) cudaEventDestroy(wgrad_fork_);
+  if (wgrad_join_) cudaEventDestroy(wgrad_join_);
+  if (wgrad_stream_) cudaStreamDestroy(wgrad_stream_);
 }
 
 void Net::check(cudaError_t e, const char* what) const {
@@ -280,6 +283,23 @@ static double gemm_algorithmic_bytes(const rfk::GemmDesc& d) {
   return a + b + c;
 }
 
+// Conv backward runs the weight-gradient GEMM on a side stream concurrently
+// with the data-gradient GEMM (RFK_WGRAD_OVERLAP=0 serialises them).
+bool Net::wgrad_overlap() const {
+  static const bool on = [] {
+    const char* e = std::getenv("RFK_WGRAD_OVERLAP");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+void Net::ensure_wgrad_stream() {
+  if (wgrad_stream_) return;
+  check(cudaStreamCreateWithFlags(&wgrad_stream_, cudaStreamNonBlocking), "wgrad stream");
+  check(cudaEventCreateWithFlags(&wgrad_fork_, cudaEventDisableTiming), "event");
+  check(cudaEventCreateWithFlags(&wgrad_join_, cudaEventDisableTiming), "event");
+}
+
 void Net::gemm(const rfk::GemmDesc& d, cudaStream_t st) {
   if (tracing_) gemm_trace_.push_back({d, trace_flops_, gemm_algorithmic_bytes(d)});
   check(rfk::gemm_launch(d, st), "gemm");
@@ -486,6 +506,16 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       const Param& w = params_[op.w_param];
       const __nv_bfloat16* dy = gptr(op.out);
       trace_flops_ = 2.0 * y.rows() * op.cout * op.R * op.S * op.cin_real;  // dgrad and wgrad each
+      // fork: the weight gradient (below) runs on a side stream next to the
+      // data gradient; both only read dy and x, and the join closes this op
+      const bool fork = wgrad_overlap();
+      cudaStream_t wst = st;
+      if (fork) {
+        ensure_wgrad_stream();
+        check(cudaEventRecord(wgrad_fork_, st), "event");
+        check(cudaStreamWaitEvent(wgrad_stream_, wgrad_fork_, 0), "wait");
+        wst = wgrad_stream_;
+      }
       // ---- dgrad
       __nv_bfloat16* dx = gptr(op.in[0]);
       if (op.in[0] != input_t_ && dx) {
@@ -537,7 +567,9 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           }
         }
         if (op.dg_splits > 1 && d.a_kind == rfk::Operand::Im2colK) {
-          float* ws_split = reinterpret_cast<float*>(ws + ws_im2col_ + ws_partials_ + ws_zero_);
+          // own region: the weight-gradient split partials may be in flight on the side stream
+          float* ws_split = reinterpret_cast<float*>(ws + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ +
+                                                     ws_misc_ + ws_counters_);
           const bool accumulate = d.accumulate_out;
           d.splits = op.dg_splits;
           d.block_n = op.dg_bn;
@@ -569,7 +601,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       d.block_n = op.wg_bn;
       if (op.explicit_im2col) {
         rfk::ConvShape cs{x.N, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
-        check(rfk::im2col(tb(op.in[0]), cs, op.kpad, ws_im2col, st), "im2col");
+        check(rfk::im2col(tb(op.in[0]), cs, op.kpad, ws_im2col, wst), "im2col");
         d.b_kind = rfk::Operand::MNMajor2D;
         d.b = ws_im2col;
         d.b_ld = op.kpad;
@@ -589,11 +621,15 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         d.splits = op.wg_splits;
         d.out = ws_split;
         d.split_stride = (long)op.cout * kw;
-        gemm(d, st);
-        check(rfk::reduce_splits(ws_split, op.wg_splits, (long)op.cout * kw, dW, false, st), "reduce_splits");
+        gemm(d, wst);
+        check(rfk::reduce_splits(ws_split, op.wg_splits, (long)op.cout * kw, dW, false, wst), "reduce_splits");
       } else {
         d.out = dW;
-        gemm(d, st);
+        gemm(d, wst);
+      }
+      if (fork) {  // join
+        check(cudaEventRecord(wgrad_join_, wgrad_stream_), "event");
+        check(cudaStreamWaitEvent(st, wgrad_join_, 0), "wait");
       }
       break;
     }

@@ -697,7 +697,7 @@ void Net::layout() {
   rep_.grad_arena_bytes = grad_bytes_;
 
   // workspaces
-  ws_im2col_ = ws_partials_ = ws_zero_ = ws_split_ = ws_stats_ = ws_misc_ = 0;
+  ws_im2col_ = ws_partials_ = ws_zero_ = ws_split_ = ws_stats_ = ws_misc_ = ws_dsplit_ = 0;
   for (auto& op : ops_) {
     if (op.kind == OpKind::Conv) {
       const Tensor& x = tensors_[op.in[0]];
@@ -732,7 +732,7 @@ void Net::layout() {
         if (pl.second > 1) {
           op.dg_bn = pl.first;
           op.dg_splits = pl.second;
-          ws_split_ = std::max(ws_split_, align_up((long)pl.second * x.rows() * op.cin * 4));
+          ws_dsplit_ = std::max(ws_dsplit_, align_up((long)pl.second * x.rows() * op.cin * 4));
         }
       }
       // fused BN statistics slot for this conv
@@ -775,7 +775,8 @@ void Net::layout() {
       ws_stats_ += align_up(kStatRows * 2 * op.cout * 4);
     }
   ws_counters_ = 0;
-  rep_.workspace_bytes = ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_ + ws_counters_;
+  rep_.workspace_bytes =
+      ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_ + ws_counters_ + ws_dsplit_;
   rep_.param_bytes = n_params_ * 4 * 3;
   rep_.state_bytes = n_state_ * 4;
 }

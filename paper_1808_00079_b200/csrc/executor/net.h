@@ -288,6 +288,11 @@ class Net {
   // data-gradient GEMM (fork / join inside the step graph)
   cudaStream_t wgrad_stream_ = nullptr;
   cudaEvent_t wgrad_fork_ = nullptr, wgrad_join_ = nullptr;
+  bool wgrad_pending_ = false;
+  std::vector<std::pair<long, long>> wgrad_reads_act_, wgrad_reads_grad_;  // byte ranges pending wgrads read
+  void instr_writes(const Instr& ins, std::vector<std::pair<long, long>>& act,
+                    std::vector<std::pair<long, long>>& grad) const;
+  void join_wgrad(cudaStream_t st);
   struct Bucket {
     int after_instr;  // launch once this schedule instruction has been enqueued
     long lo, hi;      // float range of the gradient buffer

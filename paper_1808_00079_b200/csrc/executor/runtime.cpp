@@ -351,7 +351,10 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       if (op.fp_splits > 1 && d.a_kind == rfk::Operand::Im2colK) {
         // split-K into fp32 partials, then one pass sums them in split order,
         // rounds to bf16 and emits the BN statistics rows
-        float* ws_split = reinterpret_cast<float*>(ws + ws_im2col_ + ws_partials_ + ws_zero_);
+        // the main-stream split region (the weight-gradient partials of a
+        // pending side-stream GEMM may still live in ws_split)
+        float* ws_split = reinterpret_cast<float*>(ws + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ +
+                                                   ws_misc_ + ws_counters_);
         d.splits = op.fp_splits;
         d.block_n = op.fp_bn;
         d.out = ws_split;
@@ -627,9 +630,13 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         d.out = dW;
         gemm(d, wst);
       }
-      if (fork) {  // join
-        check(cudaEventRecord(wgrad_join_, wgrad_stream_), "event");
-        check(cudaStreamWaitEvent(st, wgrad_join_, 0), "wait");
+      if (fork) {
+        // joined lazily (forward_backward): before the first instruction that
+        // writes what this weight gradient reads, before an all-reduce bucket,
+        // and at the end of the backward
+        if (op.in[0] != input_t_) wgrad_reads_act_.push_back({slot_[op.in[0]], slot_[op.in[0]] + x.bytes()});
+        wgrad_reads_grad_.push_back({grad_slot_[op.out], grad_slot_[op.out] + y.bytes()});
+        wgrad_pending_ = true;
       }
       break;
     }
@@ -924,13 +931,52 @@ std::vector<std::array<long, 3>> Net::bucket_plan(long bucket_bytes) {
   return out;
 }
 
+// Bytes of the activation arena / gradient arena an instruction writes.
+void Net::instr_writes(const Instr& ins, std::vector<std::pair<long, long>>& act,
+                       std::vector<std::pair<long, long>>& grad) const {
+  act.clear();
+  grad.clear();
+  const Op& op = ops_[ins.op];
+  if (ins.kind == InstrKind::Forward) {
+    auto put = [&](int t) {
+      if (t != input_t_ && t != loss_t_ && slot_[t] >= 0) act.push_back({slot_[t], slot_[t] + tensors_[t].bytes()});
+    };
+    put(op.out);
+    if (op.fused_bn >= 0) put(ops_[op.fused_bn].out);
+  } else if (ins.kind == InstrKind::Backward) {
+    for (int t : op.in)
+      if (t != input_t_ && grad_slot_[t] >= 0) grad.push_back({grad_slot_[t], grad_slot_[t] + tensors_[t].bytes()});
+  }
+}
+
+void Net::join_wgrad(cudaStream_t st) {
+  if (!wgrad_pending_) return;
+  check(cudaEventRecord(wgrad_join_, wgrad_stream_), "event");
+  check(cudaStreamWaitEvent(st, wgrad_join_, 0), "wait");
+  wgrad_reads_act_.clear();
+  wgrad_reads_grad_.clear();
+  wgrad_pending_ = false;
+}
+
 void Net::forward_backward(cudaStream_t st) {
   if (!setup_done_) throw std::invalid_argument("setup the network first");
   const bool dp = comm_ && comm_->ready() && comm_->nranks() > 0;
   size_t b = 0;
+  std::vector<std::pair<long, long>> wa, wg;
+  auto overlaps = [](const std::vector<std::pair<long, long>>& w, const std::vector<std::pair<long, long>>& r) {
+    for (const auto& x : w)
+      for (const auto& y : r)
+        if (x.first < y.second && y.first < x.second) return true;
+    return false;
+  };
   for (int k = 0; k < (int)sched_.size(); ++k) {
+    if (wgrad_pending_) {
+      instr_writes(sched_[k], wa, wg);
+      if (overlaps(wa, wgrad_reads_act_) || overlaps(wg, wgrad_reads_grad_)) join_wgrad(st);
+    }
     run_instr(sched_[k], st);
     while (dp && b < buckets_.size() && buckets_[b].after_instr == k) {
+      join_wgrad(st);  // the bucket's weight gradients must be complete
       // fork: the side stream waits for the gradients, then reduces them
       // while this stream carries on with the backward
       check(cudaEventRecord(bucket_events_[b], st), "event");
@@ -942,6 +988,7 @@ void Net::forward_backward(cudaStream_t st) {
       ++b;
     }
   }
+  join_wgrad(st);
   if (dp) {  // join
     check(cudaEventRecord(comm_done_, comm_stream_), "event");
     check(cudaStreamWaitEvent(st, comm_done_, 0), "wait");
@@ -1147,6 +1194,7 @@ std::vector<double> Net::instr_profile(int iters, cudaStream_t st) {
         check(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal), "event");
         for (size_t k = 0; k < n; ++k) {
           run_instr(sched_[k], s);
+          join_wgrad(s);  // per-instruction attribution: no cross-instruction overlap
           check(cudaEventRecordWithFlags(ev[k + 1], s, cudaEventRecordExternal), "event");
         }
         update(0.f, 0.f, 0.f, s);  // lr 0: parameters unchanged

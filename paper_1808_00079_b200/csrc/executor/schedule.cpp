@@ -722,7 +722,7 @@ void Net::layout() {
         if (pl.second > 1) {
           op.fp_bn = pl.first;
           op.fp_splits = pl.second;
-          ws_split_ = std::max(ws_split_, align_up((long)pl.second * y.rows() * op.cout * 4));
+          ws_dsplit_ = std::max(ws_dsplit_, align_up((long)pl.second * y.rows() * op.cout * 4));
         }
       }
       const bool dgrad_taps = op.in[0] != input_t_ && !op.explicit_im2col && !(op.R == 1 && op.S == 1 &&

@@ -164,6 +164,10 @@ int rfx_net_instr_profile(rfx_net* net, int32_t iters, void* stream, double* ms,
 int rfx_net_gemm_try(rfx_net* net, int32_t idx, int32_t block_n, int32_t splits, int32_t iters, void* stream,
                      double* ms);
 
+/* 1 when no kernel wrote past the activation arena (sized to the planner's
+ * Eq. 1 total): a canary band behind it is checked */
+int rfx_net_arena_guard(const rfx_net* net, int32_t* intact);
+
 int32_t rfx_net_num_params(const rfx_net* net);
 int rfx_net_param_info(const rfx_net* net, int32_t i, char* name, size_t name_cap, int32_t* shape,
                        int32_t* ndim, int32_t* kind, int64_t* count);

@@ -291,6 +291,10 @@ int rfx_net_gemm_profile(rfx_net* n, int32_t iters, void* st, double* ms, double
   });
 }
 
+int rfx_net_arena_guard(const rfx_net* n, int32_t* intact) {
+  return guard([&] { *intact = n->net->arena_guard_intact() ? 1 : 0; });
+}
+
 int32_t rfx_net_num_params(const rfx_net* n) { return n->net->num_params(); }
 
 int rfx_net_param_info(const rfx_net* n, int32_t i, char* name, size_t cap, int32_t* shape, int32_t* ndim,

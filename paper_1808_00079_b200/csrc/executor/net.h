@@ -33,7 +33,8 @@ enum class OpKind : int { Input = 0, Conv, BN, BNAddReLU, ReLU, MaxPool, AvgPool
 const char* op_kind_name(OpKind k);
 
 constexpr long kAlign = 1024;  // arena slot alignment (bytes); costs are rounded to it
-constexpr long kStatRows = 160;  // fused-BN partial rows: >= the persistent GEMM grid (SM count)
+constexpr long kStatRows = 160;
+constexpr long kArenaGuard = 1 << 20;  // canary bytes behind the activation arena  // fused-BN partial rows: >= the persistent GEMM grid (SM count)
 inline long align_up(long x, long a = kAlign) { return (x + a - 1) / a * a; }
 
 struct Tensor {
@@ -195,6 +196,8 @@ class Net {
   void read_bn_running(int op, float* mean, float* var) const;
 
   float* grad_buffer() const { return d_grad_; }
+  // true when the canary band behind the Eq.-1-sized activation arena is untouched
+  bool arena_guard_intact() const;
   long grad_count() const { return n_params_; }
 
   // Data parallel: average the flat gradient buffer across ranks with NCCL,

@@ -98,7 +98,11 @@ void Net::setup(uint64_t seed) {
   auto alloc = [&](void** p, long bytes, const char* what) {
     check(cudaMalloc(p, bytes > 0 ? bytes : 256), what);
   };
-  alloc((void**)&d_arena_, arena_bytes_, "activation arena");
+  // the activation arena is exactly the planner's Eq. 1 total; a guard band
+  // behind it (filled with a canary) lets tests check that no kernel of the
+  // step ever writes past that high-water mark
+  alloc((void**)&d_arena_, arena_bytes_ + kArenaGuard, "activation arena");
+  check(cudaMemset(d_arena_ + arena_bytes_, 0xA5, kArenaGuard), "arena guard");
   alloc((void**)&d_grad_arena_, grad_bytes_, "gradient arena");
   alloc((void**)&d_ws_, rep_.workspace_bytes, "workspace");
   alloc((void**)&d_param_, n_params_ * 4, "params");
@@ -251,6 +255,14 @@ void Net::read_bn_running(int o, float* mean, float* var) const {
 }
 
 // ============================================================ addressing
+bool Net::arena_guard_intact() const {
+  std::vector<unsigned char> h(kArenaGuard);
+  check(cudaMemcpy(h.data(), d_arena_ + arena_bytes_, kArenaGuard, cudaMemcpyDeviceToHost), "arena guard");
+  for (unsigned char c : h)
+    if (c != 0xA5) return false;
+  return true;
+}
+
 void* Net::tptr(int t) const {
   if (t == input_t_) return d_input_;
   if (t == loss_t_) return d_loss_;

@@ -79,6 +79,7 @@ _SIGS = {
     "rfx_net_read_loss": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_void_p]),
     "rfx_net_instr_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int32,
                                         C.POINTER(C.c_int32)]),
+    "rfx_net_arena_guard": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "rfx_net_gemm_try": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
                                    C.POINTER(C.c_double)]),
     "rfx_net_gemm_profile_detail": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int32,
@@ -417,6 +418,12 @@ class ReforwardNet:
         _check(self.L.rfx_net_gemm_profile_detail(self.h, iters, _stream(stream), buf, n.value, C.byref(n)))
         keys = ("M", "N", "K", "a_kind", "b_kind", "splits", "ms", "flops", "bytes", "block_n")
         return [dict(zip(keys, buf[10 * i: 10 * i + 10])) for i in range(n.value)]
+
+    def arena_guard_intact(self) -> bool:
+        """No kernel wrote past the Eq.-1-sized activation arena (canary band check)."""
+        v = C.c_int32()
+        _check(self.L.rfx_net_arena_guard(self.h, C.byref(v)))
+        return bool(v.value)
 
     def gemm_try(self, idx: int, block_n: int, splits: int, iters: int = 5, stream=None) -> float:
         """ms of traced GEMM `idx` with a forced tile width and split count (tuning probe)."""

@@ -159,3 +159,20 @@ def test_staged_batches_match_load_batch():
         net.forward_backward()
         got.append(net.read_loss())
     assert got == ref
+
+
+@pytest.mark.parametrize("arch,batch,hw", [("resnet50", 8, 64), ("densenet_tiny", 4, 32), ("vgg11", 4, 32)])
+def test_arena_high_water_is_the_planned_eq1(arch, batch, hw):
+    """The device arena is allocated at exactly the planner's Eq. 1 total and a
+    full training step (first forward, re-forwards, backward, graph replay)
+    never writes past it: the canary band behind the arena stays intact."""
+    net = ReforwardNet.named(arch, batch, hw, hw, 10)
+    rep = net.plan("reforward")
+    assert rep.arena_bytes == rep.planned_total == rep.tracked_peak
+    net.setup(seed=0)
+    x, y = random_batch(net, seed=1)
+    net.load_batch(x, y)
+    for use_graph in (False, True):
+        net.step(lr=0.01, use_graph=use_graph)
+    torch.cuda.synchronize()
+    assert net.arena_guard_intact()

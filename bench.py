@@ -369,7 +369,10 @@ def main():
         net_sa, rep_sa, _ = build_net(args.batch, "store_all", seed=1234 + rank)
         net_sa.load_batch(x.cuda(), y.cuda(), stream=stream)
         if world > 1:
-            net_sa.set_comm(world, rank, uid)
+            # a NCCL unique id bootstraps exactly one communicator: fresh one
+            obj = [ReforwardNet.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            net_sa.set_comm(world, rank, obj[0])
         ms_sa = time_steps(net_sa, args.steps, args.warmup, stream, world)
         sa_value = args.batch * world / (ms_sa / 1000.0)
         overhead = ms / ms_sa

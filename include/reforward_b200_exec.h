@@ -45,6 +45,11 @@ typedef struct rfx_gemm_args {
 /* kind 4 = conv weights [Cout][R][S][Cpad] read as the dgrad B operand (flipped taps) */
 
 int rfx_gemm(const rfx_gemm_args* args, void* stream);
+/* explicit im2col of a few-channel NHWC bf16 conv input (the stem path):
+ * x [N][H][W][Cs] (C real channels) -> out [N*P*Q][kpad], K order (r, s, c),
+ * zero K padding; kpad % 8 == 0 */
+int rfx_im2col(const void* x, int N, int H, int W, int C, int Cs, int P, int Q, int R, int S, int stride, int pad,
+               int kpad, void* out, void* stream);
 
 /* ------------------------------------------------------------ re-forward training executor
  * A network is a DAG of ops over NHWC tensors; each builder call returns the

@@ -4,6 +4,7 @@
 #include <string>
 
 #include "kernels/kernels.h"
+#include "kernels/ops.h"
 #include "reforward_b200.h"
 
 namespace rfexec {
@@ -36,6 +37,18 @@ extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
   cudaError_t e = rfk::gemm_launch(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     rfexec::set_last_error(std::string("rfx_gemm: ") + cudaGetErrorString(e));
+    return RF_E_CUDA;
+  }
+  return RF_OK;
+}
+
+extern "C" int rfx_im2col(const void* x, int N, int H, int W, int C, int Cs, int P, int Q, int R, int S, int stride,
+                          int pad, int kpad, void* out, void* stream) {
+  rfk::ConvShape g{N, H, W, C, Cs, P, Q, R, S, stride, pad};
+  cudaError_t e = rfk::im2col(static_cast<const __nv_bfloat16*>(x), g, kpad, static_cast<__nv_bfloat16*>(out),
+                              static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    rfexec::set_last_error(std::string("rfx_im2col: ") + cudaGetErrorString(e));
     return RF_E_CUDA;
   }
   return RF_OK;

@@ -75,6 +75,7 @@ struct Op {
   int cin = 0, cin_real = 0, cout = 0, cpad = 0, coutpad = 0;
   bool explicit_im2col = false;
   int kpad = 0;              // explicit im2col K (padded)
+  int im2col_imgs = 0;       // images per explicit-im2col chunk (the chunk stays in L2)
   bool fuse_stats = false;   // conv epilogue emits BN partial sums for its consumer
   long stats_off = -1;       // its slot in the statistics workspace (floats)
   int wg_splits = 1, wg_bn = 128;  // wgrad split-K and tile N

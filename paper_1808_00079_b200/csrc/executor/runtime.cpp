@@ -337,13 +337,37 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       d.b = d_bf16_ + w.bf16_off;
       if (op.explicit_im2col) {
         if (op.pad != op.pad_w) throw std::runtime_error("explicit im2col needs square padding");
-        rfk::ConvShape cs{x.N, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
-        check(rfk::im2col(tb(op.in[0]), cs, op.kpad, ws_im2col, st), "im2col");
         d.a_kind = rfk::Operand::KMajor2D;
         d.a = ws_im2col;
         d.a_ld = op.kpad;
         d.K = op.kpad;
         d.b_ld = op.kpad;
+        float* stats = (op.fuse_stats && !reforward) ? ws_stats + op.stats_off : nullptr;
+        trace_flops_ = 2.0 * y.rows() * op.cout * op.R * op.S * op.cin_real;
+        if (reforward && op.fused_bn >= 0) {
+          const Op& bn = ops_[op.fused_bn];
+          const BNState& b = bns_[bn.bn];
+          d.bn_out = tptr(bn.out);
+          d.bn_scale = d_state_ + b.scale;
+          d.bn_shift = d_state_ + b.shift;
+          d.bn_relu = bn.k == 1;
+        }
+        // image chunks: im2col of a chunk (L2-resident) -> its GEMM rows; the
+        // BN statistics rows accumulate over the chunks in order
+        const long img_rows = (long)y.H * y.W;
+        for (int n0 = 0; n0 < x.N; n0 += op.im2col_imgs) {
+          const int nn = std::min(op.im2col_imgs, x.N - n0);
+          rfk::ConvShape cs{nn, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
+          check(rfk::im2col(tb(op.in[0]) + (long)n0 * x.H * x.W * x.C, cs, op.kpad, ws_im2col, st), "im2col");
+          rfk::GemmDesc dc = d;
+          dc.M = (int)(nn * img_rows);
+          dc.out = tb(op.out) + n0 * img_rows * op.cout;
+          if (dc.bn_out) dc.bn_out = static_cast<__nv_bfloat16*>(dc.bn_out) + n0 * img_rows * op.cout;
+          dc.stats = stats;
+          dc.stats_acc = n0 > 0;
+          gemm(dc, st);
+        }
+        break;
       } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0 && op.pad_w == 0) {
         d.a_kind = rfk::Operand::KMajor2D;
         d.a = tptr(op.in[0]);
@@ -615,11 +639,27 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       d.ldc = kw;
       d.block_n = op.wg_bn;
       if (op.explicit_im2col) {
-        rfk::ConvShape cs{x.N, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
-        check(rfk::im2col(tb(op.in[0]), cs, op.kpad, ws_im2col, wst), "im2col");
+        // image chunks (L2-resident im2col): every chunk's split-K partials
+        // land in their own slice; one reduction sums them chunk-major
         d.b_kind = rfk::Operand::MNMajor2D;
         d.b = ws_im2col;
         d.b_ld = op.kpad;
+        d.splits = op.wg_splits;
+        d.split_stride = (long)op.cout * kw;
+        const long img_rows = (long)y.H * y.W;
+        int parts = 0;
+        for (int n0 = 0; n0 < x.N; n0 += op.im2col_imgs) {
+          const int nn = std::min(op.im2col_imgs, x.N - n0);
+          rfk::ConvShape cs{nn, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
+          check(rfk::im2col(tb(op.in[0]) + (long)n0 * x.H * x.W * x.C, cs, op.kpad, ws_im2col, wst), "im2col");
+          rfk::GemmDesc dc = d;
+          dc.K = (int)(nn * img_rows);
+          dc.a = dy + n0 * img_rows * op.cout;
+          dc.out = ws_split + (long)parts * op.cout * kw;
+          gemm(dc, wst);
+          parts += op.wg_splits;
+        }
+        check(rfk::reduce_splits(ws_split, parts, (long)op.cout * kw, dW, false, wst), "reduce_splits");
       } else if (op.R == 1 && op.S == 1 && op.stride == 1 && op.pad == 0 && op.pad_w == 0) {
         d.b_kind = rfk::Operand::MNMajor2D;
         d.b = tptr(op.in[0]);
@@ -630,7 +670,9 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         d.b = tptr(op.in[0]);
         d.b_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad_w, op.stride, op.stride};
       }
-      if (op.wg_splits > 1) {
+      if (op.explicit_im2col) {
+        // done above
+      } else if (op.wg_splits > 1) {
         // split-K partials in the workspace, summed in split order by a
         // whole-GPU reduction kernel into the gradient buffer
         d.splits = op.wg_splits;

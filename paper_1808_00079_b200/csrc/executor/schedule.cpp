@@ -611,10 +611,19 @@ std::pair<int, int> im2col_split_plan(long M, int N, long kb) {
   return pick;
 }
 
+// explicit-im2col chunk size (RFK_IM2COL_CHUNK_MB; default 0 = whole batch,
+// the fastest measured; chunks trade ~130 MB of workspace for launches)
+long im2col_chunk_bytes() {
+  const char* e = std::getenv("RFK_IM2COL_CHUNK_MB");
+  const long mb = e ? std::atol(e) : 0;
+  return mb > 0 ? mb << 20 : (1L << 62);
+}
+
 int wgrad_splits(long tiles, long kblocks) {
   long s = (148 + tiles - 1) / tiles;
   s = std::min(s, std::max(1L, kblocks / 8));
-  return (int)std::max(1L, std::min(s, 32L));
+  static const long cap = std::getenv("RFK_WG_SPLIT_CAP") ? std::atol(std::getenv("RFK_WG_SPLIT_CAP")) : 148;
+  return (int)std::max(1L, std::min(s, cap));
 }
 }  // namespace
 
@@ -702,15 +711,30 @@ void Net::layout() {
     if (op.kind == OpKind::Conv) {
       const Tensor& x = tensors_[op.in[0]];
       const Tensor& y = tensors_[op.out];
-      if (op.explicit_im2col) ws_im2col_ = std::max(ws_im2col_, align_up(y.rows() * op.kpad * 2));
+      if (op.explicit_im2col) {
+        // the im2col matrix is built and consumed in chunks of whole images
+        // small enough to stay in L2 (the full stem matrix is ~150 MB at
+        // batch 32, HBM traffic twice over)
+        const long per_img = (long)y.H * y.W * op.kpad * 2;
+        op.im2col_imgs = (int)std::max(1L, std::min((long)y.N, im2col_chunk_bytes() / per_img));
+        ws_im2col_ = std::max(ws_im2col_, align_up(op.im2col_imgs * per_img));
+      }
       if (op.stride > 1 && op.R > 1)
         ws_zero_ = std::max(ws_zero_, align_up((long)x.N * (x.H - op.R + 1 + 2 * op.pad) *
                                                (x.W - op.S + 1 + 2 * op.pad_w) * op.cout * 2));
       const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
       op.wg_bn = kw <= 64 ? 64 : (kw <= 128 ? 128 : 256);
       const long tiles = ((op.cout + 127) / 128) * ((kw + op.wg_bn - 1) / op.wg_bn);
-      op.wg_splits = wgrad_splits(tiles, (y.rows() + 63) / 64);
-      if (op.wg_splits > 1) ws_split_ = std::max(ws_split_, align_up((long)op.wg_splits * op.cout * kw * 4));
+      if (op.explicit_im2col) {
+        // one set of split-K partials per image chunk, summed together (chunk
+        // major, split minor) by one reduction
+        const long chunks = (y.N + op.im2col_imgs - 1) / op.im2col_imgs;
+        op.wg_splits = wgrad_splits(tiles, ((long)op.im2col_imgs * y.H * y.W + 63) / 64);
+        ws_split_ = std::max(ws_split_, align_up(chunks * op.wg_splits * op.cout * kw * 4));
+      } else {
+        op.wg_splits = wgrad_splits(tiles, (y.rows() + 63) / 64);
+        if (op.wg_splits > 1) ws_split_ = std::max(ws_split_, align_up((long)op.wg_splits * op.cout * kw * 4));
+      }
       // fprop / dgrad through TMA im2col: split-K when the output tiles are
       // too few to fill the GPU (the deep 14x14 / 7x7 layers)
       op.fp_splits = op.dg_splits = 1;

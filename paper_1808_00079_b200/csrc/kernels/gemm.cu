@@ -50,6 +50,7 @@ struct alignas(64) KParams {
   int out_f32, accumulate_out;
   const float* bias;
   float* stats;
+  int stats_acc;
   long split_stride;
   int remap, rP, rQ, rH, rW, rsh, rsw;
   int b_taps;  // WeightTapsMN: filter taps R*S
@@ -332,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
         const int col = nt * BN + c;
         if (col < p.N) {
+          if (p.stats_acc) s += row[col], q += row[p.N + col];  // earlier chunks of M first
           row[col] = s;
           row[p.N + col] = q;
         }
@@ -747,6 +749,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   kp.accumulate_out = d.accumulate_out;
   kp.bias = d.bias;
   kp.stats = d.stats;
+  kp.stats_acc = d.stats_acc ? 1 : 0;
   kp.split_stride = d.split_stride;
   // output through TMA (store, or reduce-add when accumulating) whenever the
   // rows are not remapped and the strides are 16-byte multiples

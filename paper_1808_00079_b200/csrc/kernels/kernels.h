@@ -50,6 +50,7 @@ struct GemmDesc {
   bool accumulate_out = false;  // out += D (fp32 or bf16)
   const float* bias = nullptr;  // per column
   float* stats = nullptr;       // [m_tiles][2][N] column sum / sum of squares
+  bool stats_acc = false;       // add to the statistics rows instead of writing them (chunked M)
   int splits = 1;               // split-K; split z writes out + z * split_stride
   long split_stride = 0;
   // row remap of the output (strided-conv dgrad scatter): row m = (n, p, q)

@@ -1136,54 +1136,94 @@ __global__ void __launch_bounds__(kThreads) im2col_kernel(const __nv_bfloat16* _
   }
 }
 
-// Row-staged im2col (the stem's few-channel conv): one block per output row
-// (n, p) stages the R input rows it reads, zero-padded to W + 2*pad columns,
-// in shared memory with 16-byte loads, then writes the Q x Kpad slab with
-// coalesced 16-byte stores.  The gather happens in shared memory instead of
-// as 2-byte global loads, so the kernel runs at the output write rate.
+// Window-staged im2col (the stem's few-channel conv): a block takes a run of
+// `rpb` consecutive output rows p0.. of one image and stages the
+// (rpb-1)*stride + R input rows they read in shared memory, zero-padded to
+// W + 2*pad columns and COMPACT -- only the C real channels per pixel, so the
+// (r, s, c) K order of a tap row is contiguous and consecutive K groups of a
+// warp read consecutive shared-memory words (no bank conflicts; the padded
+// 16-byte pixels made 4-way conflicts).  The global loads of a window are
+// issued four per thread before any store.  Then the rpb Q x Kpad slabs are
+// written with coalesced 16-byte stores.
 __global__ void __launch_bounds__(kThreads) im2col_rows_kernel(const __nv_bfloat16* __restrict__ x, ConvShape g,
-                                                              int Kpad, __nv_bfloat16* __restrict__ out) {
+                                                              int Kpad, int rpb, __nv_bfloat16* __restrict__ out) {
   pdl_enter();
-  extern __shared__ __align__(16) unsigned short rows_s[];  // [R][W + 2 pad][Cs], then the k table
+  extern __shared__ __align__(16) unsigned short rows_s[];  // [window rows][W + 2 pad][C], then the k table
   const int Wp = g.W + 2 * g.pad;
-  const int cv = g.Cs / 8;  // 16-byte vectors per pixel
+  const int cv = g.Cs / 8;  // 16-byte vectors per stored pixel
   const int kv = Kpad / 8;
   const int Kreal = g.R * g.S * g.C;
+  const int win = (rpb - 1) * g.stride + g.R;
   // k -> offset of (r, s, c) in the staged rows relative to the output
-  // pixel's first column (-1: K padding)
-  int* ktab = reinterpret_cast<int*>(rows_s + (long)g.R * Wp * g.Cs);
+  // pixel's first column of its first window row (-1: K padding)
+  int* ktab = reinterpret_cast<int*>(rows_s + (((long)win * Wp * g.C + 7) & ~7L));
   for (int k = threadIdx.x; k < Kpad; k += blockDim.x) {
     const int c = k % g.C, rs = k / g.C, s = rs % g.S, r = rs / g.S;
-    ktab[k] = k < Kreal ? (r * Wp + s) * g.Cs + c : -1;
+    ktab[k] = k < Kreal ? (r * Wp + s) * g.C + c : -1;
   }
-  for (long rowid = blockIdx.x; rowid < (long)g.N * g.P; rowid += gridDim.x) {
-    const int p = (int)(rowid % g.P), n = (int)(rowid / g.P);
-    __syncthreads();
+  const int runs_per_img = (g.P + rpb - 1) / rpb;
+  const int step = blockDim.x / kv;
+  const int kg = threadIdx.x % kv;
+  for (int run = blockIdx.x; run < g.N * runs_per_img; run += gridDim.x) {
+    const int n = run / runs_per_img, p0 = (run % runs_per_img) * rpb;
+    const int np = min(rpb, g.P - p0);
+    const int h0 = p0 * g.stride - g.pad;
+    const int rows = (np - 1) * g.stride + g.R;
+    const int rowv = Wp * cv;  // 16-byte vectors per staged row
     const uint4* xv = reinterpret_cast<const uint4*>(x) + (long)n * g.H * g.W * cv;
-    for (int i = threadIdx.x; i < g.R * Wp * cv; i += blockDim.x) {
-      const int c8 = i % cv, t = i / cv, wp = t % Wp, r = t / Wp;
-      const int h = p * g.stride - g.pad + r, w = wp - g.pad;
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (h >= 0 && h < g.H && w >= 0 && w < g.W) v = __ldg(xv + ((long)h * g.W + w) * cv + c8);
-      reinterpret_cast<uint4*>(rows_s)[i] = v;
+    __syncthreads();  // the previous run's slabs are written
+    // four rows' loads in flight per thread, then the compact stores
+    for (int j = threadIdx.x; j < rowv; j += blockDim.x) {
+      const int c8 = cv == 1 ? 0 : j % cv, wp = cv == 1 ? j : j / cv, w = wp - g.pad;
+      const bool win_w = w >= 0 && w < g.W;
+      for (int r0 = 0; r0 < rows; r0 += 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int h = h0 + r0 + u;
+          v[u] = make_uint4(0u, 0u, 0u, 0u);
+          if (r0 + u < rows && win_w && h >= 0 && h < g.H) v[u] = __ldg(xv + ((long)h * g.W + w) * cv + c8);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (r0 + u >= rows) break;
+          const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+          unsigned short* dst = rows_s + ((long)(r0 + u) * Wp + wp) * g.C + c8 * 8;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            if (c8 * 8 + c < g.C) dst[c] = (unsigned short)(wv[c >> 1] >> ((c & 1) * 16));
+        }
+      }
     }
     __syncthreads();
     // each thread owns one 8-wide K group (its 8 gather offsets stay in
     // registers) and walks the output pixels; consecutive threads write
     // consecutive 16-byte vectors of a pixel's K row
-    uint4* o = reinterpret_cast<uint4*>(out + rowid * g.Q * Kpad);
-    const int step = blockDim.x / kv;
     if ((int)threadIdx.x < step * kv) {
-      const int kg = threadIdx.x % kv;
+      // K padding: offset 0 and a zero mask instead of a per-element select
       int off[8];
+      uint32_t mask[4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) off[j] = ktab[kg * 8 + j];
-      for (int q = threadIdx.x / kv; q < g.Q; q += step) {
-        const unsigned short* px = rows_s + q * g.stride * g.Cs;
-        uint32_t e[8];
+      for (int j = 0; j < 8; ++j) off[j] = max(ktab[kg * 8 + j], 0);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) e[j] = off[j] >= 0 ? px[off[j]] : 0u;
-        o[q * kv + kg] = make_uint4(e[0] | (e[1] << 16), e[2] | (e[3] << 16), e[4] | (e[5] << 16), e[6] | (e[7] << 16));
+      for (int j = 0; j < 4; ++j)
+        mask[j] = (ktab[kg * 8 + 2 * j] >= 0 ? 0xffffu : 0u) | (ktab[kg * 8 + 2 * j + 1] >= 0 ? 0xffff0000u : 0u);
+      const bool all_pad = (mask[0] | mask[1] | mask[2] | mask[3]) == 0u;
+      for (int pp = 0; pp < np; ++pp) {
+        const unsigned short* base = rows_s + pp * g.stride * Wp * g.C;
+        uint4* o = reinterpret_cast<uint4*>(out + ((long)n * g.P + p0 + pp) * g.Q * Kpad);
+        for (int q = threadIdx.x / kv; q < g.Q; q += step) {
+          uint4 val = make_uint4(0u, 0u, 0u, 0u);
+          if (!all_pad) {
+            const unsigned short* px = base + q * g.stride * g.C;
+            uint32_t e[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) e[j] = px[off[j]];
+            val = make_uint4(__byte_perm(e[0], e[1], 0x5410) & mask[0], __byte_perm(e[2], e[3], 0x5410) & mask[1],
+                             __byte_perm(e[4], e[5], 0x5410) & mask[2], __byte_perm(e[6], e[7], 0x5410) & mask[3]);
+          }
+          o[q * kv + kg] = val;
+        }
       }
     }
   }
@@ -1512,15 +1552,23 @@ cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __n
 
 cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st) {
   if (Kpad % 8) return cudaErrorInvalidValue;
-  const long rows_smem = (long)g.R * (g.W + 2 * g.pad) * g.Cs * 2 + (long)Kpad * 4;
-  if (g.Cs % 8 == 0 && rows_smem <= 96 * 1024 && Kpad / 8 <= kThreads) {
+  // rows per run: the largest <= 8 whose compact window fits 48 KB
+  const long row_bytes = (long)(g.W + 2 * g.pad) * g.C * 2;
+  auto smem_for = [&](int r) { return ((((long)(r - 1) * g.stride + g.R) * row_bytes + 15) & ~15L) + (long)Kpad * 4; };
+  int rpb = 8;
+  while (rpb > 1 && smem_for(rpb) > 48 * 1024) --rpb;
+  const long win_smem = smem_for(rpb);
+  if (g.Cs % 8 == 0 && win_smem <= 96 * 1024 && Kpad / 8 <= kThreads) {
     static bool attr_set = false;
     if (!attr_set) {
       cudaFuncSetAttribute(im2col_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
       attr_set = true;
     }
-    const long rows = (long)g.N * g.P;
-    RFK_CHECK_LAUNCH(launch_k(im2col_rows_kernel, (int)std::min<long>(rows, 148 * 8), kThreads, rows_smem, st, x, g, Kpad, out));
+    const long runs = (long)g.N * ((g.P + rpb - 1) / rpb);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, im2col_rows_kernel, kThreads, win_smem);
+    const long blocks = std::min<long>(runs, 148L * std::max(1, per_sm));
+    RFK_CHECK_LAUNCH(launch_k(im2col_rows_kernel, (int)blocks, kThreads, win_smem, st, x, g, Kpad, rpb, out));
     return cudaGetLastError();
   }
   const long total = (long)g.N * g.P * g.Q * (Kpad / 8);

@@ -47,6 +47,8 @@ def lib():
         _lib = load_library()
         _lib.rfx_gemm.restype = C.c_int
         _lib.rfx_gemm.argtypes = [C.POINTER(GemmArgs), C.c_void_p]
+        _lib.rfx_im2col.restype = C.c_int
+        _lib.rfx_im2col.argtypes = [C.c_void_p] + [C.c_int] * 12 + [C.c_void_p, C.c_void_p]
         _lib.rf_last_error.restype = C.c_char_p
     return _lib
 
@@ -65,3 +67,20 @@ def gemm(args: GemmArgs, stream=None) -> None:
     rc = L.rfx_gemm(C.byref(args), stream_handle(stream))
     if rc != 0:
         raise RuntimeError(L.rf_last_error().decode())
+
+
+def im2col(x: torch.Tensor, C_real: int, R: int, S: int, stride: int, pad: int, kpad: int, out: torch.Tensor = None,
+           stream=None) -> torch.Tensor:
+    """Explicit im2col of an NHWC bf16 input with C_real of its x.shape[3]
+    channels: [N*P*Q][kpad], K order (r, s, c), zero padded."""
+    N, H, W, Cs = x.shape
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    if out is None:
+        out = torch.empty(N * P * Q, kpad, dtype=torch.bfloat16, device=x.device)
+    L = lib()
+    rc = L.rfx_im2col(x.data_ptr(), N, H, W, C_real, Cs, P, Q, R, S, stride, pad, kpad, out.data_ptr(),
+                      stream_handle(stream))
+    if rc != 0:
+        raise RuntimeError(L.rf_last_error().decode())
+    return out

@@ -176,3 +176,35 @@ def test_arena_high_water_is_the_planned_eq1(arch, batch, hw):
         net.step(lr=0.01, use_graph=use_graph)
     torch.cuda.synchronize()
     assert net.arena_guard_intact()
+
+
+def test_chunked_stem_im2col_matches_whole_batch(monkeypatch):
+    """The explicit-im2col stem built and consumed in image chunks (BN
+    statistics rows accumulated over the chunks, weight-gradient partials
+    summed chunk-major) gives the whole-batch step up to fp32 summation order,
+    and stays bit-identical between re-forward and store-all."""
+    arch, batch, hw = "resnet18", 5, 64  # 1 MB chunks = 2 images: chunks of 2, 2, 1
+
+    def run(chunk_mb, policy):
+        monkeypatch.setenv("RFK_IM2COL_CHUNK_MB", str(chunk_mb))
+        net = ReforwardNet.named(arch, batch, hw, hw, 10)
+        net.plan(policy)
+        net.setup(seed=2)
+        x, y = random_batch(net, seed=3)
+        net.load_batch(x, y)
+        net.forward_backward()
+        torch.cuda.synchronize()
+        return net.read_loss(), {p.name: net.read_param(p.index, 1) for p in net.params()}
+
+    loss_w, g_w = run(0, "reforward")
+    loss_c, g_c = run(1, "reforward")
+    loss_s, g_s = run(1, "store_all")
+    assert abs(loss_c - loss_w) <= 1e-3 * abs(loss_w), (loss_c, loss_w)
+    a = np.concatenate([g_c[n].ravel() for n in g_w]).astype(np.float64)
+    b = np.concatenate([g_w[n].ravel() for n in g_w]).astype(np.float64)
+    assert float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b))) >= 0.999
+    stem = [n for n in g_w if n.startswith("stem.conv")][0]
+    assert rel_err(g_c[stem], g_w[stem]) <= 2e-2
+    assert loss_c == loss_s
+    for n in g_c:
+        assert np.array_equal(g_c[n], g_s[n]), n

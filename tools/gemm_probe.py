@@ -74,6 +74,21 @@ def cases():
                 dict(M=n1 * h1 * h1, N=64, K=576, a_kind=K.IM2COL_K, a=x2.data_ptr(), a_geom=g2,
                      b_kind=K.KMAJOR, b=w1.data_ptr(), b_ld=576, out=o1.data_ptr(), ldc=64,
                      stats=s1.data_ptr(), splits=1, band=1), (x2, w1, o1, s1), {}))
+    # stem (7x7/2, 3 -> 64 at 112x112): explicit im2col K = 192, whole batch
+    # and one 4-image chunk (the chunk's A stays in L2 across replays)
+    Ms, Ks = 32 * 112 * 112, 192
+    As, Bs, Os = bf(Ms, Ks), bf(64, Ks), bf(Ms, 64)
+    Ss = torch.zeros(160, 2, 64, device=dev)
+    for m in (Ms, Ms // 8):
+        out.append((f"stem fprop M={m} K192 N64 +stats", m, 64, Ks,
+                    dict(M=m, N=64, K=Ks, a_kind=K.KMAJOR, a=As.data_ptr(), a_ld=Ks, b_kind=K.KMAJOR,
+                         b=Bs.data_ptr(), b_ld=Ks, out=Os.data_ptr(), ldc=64, stats=Ss.data_ptr(), splits=1),
+                    (As, Bs, Os, Ss), {}))
+    Ws = torch.zeros(32, 64, Ks, device=dev)
+    out.append(("stem wgrad 64x192 K=401408 s32", 64, Ks, Ms,
+                dict(M=64, N=Ks, K=Ms, a_kind=K.MNMAJOR, a=Os.data_ptr(), a_ld=64, b_kind=K.MNMAJOR,
+                     b=As.data_ptr(), b_ld=Ks, out=Ws.data_ptr(), ldc=Ks, out_f32=1, splits=32,
+                     split_stride=64 * Ks), (As, Os, Ws), {"block_n": 256}))
     # launch + prologue + epilogue floor: one 128x128 tile per SM, one K block
     Mt = 128 * 148
     at, bt, ot = bf(Mt, 64), bf(128, 64), bf(Mt, 128)

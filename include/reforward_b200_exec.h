@@ -48,6 +48,11 @@ int rfx_gemm(const rfx_gemm_args* args, void* stream);
 /* explicit im2col of a few-channel NHWC bf16 conv input (the stem path):
  * x [N][H][W][Cs] (C real channels) -> out [N*P*Q][kpad], K order (r, s, c),
  * zero K padding; kpad % 8 == 0 */
+/* max-pool backward (NHWC bf16, C % 8 == 0): dx (+)= sum over the windows
+ * whose first argmax is the pixel of their dy, in fixed window order.
+ * workspace: N*P*Q*C bytes, used only by the two-pass fallback */
+int rfx_maxpool_bwd(const void* x, const void* dy, int N, int H, int W, int C, int k, int stride, int pad, void* dx,
+                    int accumulate, void* workspace, void* stream);
 int rfx_im2col(const void* x, int N, int H, int W, int C, int Cs, int P, int Q, int R, int S, int stride, int pad,
                int kpad, void* out, void* stream);
 

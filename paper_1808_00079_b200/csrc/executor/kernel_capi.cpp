@@ -53,3 +53,16 @@ extern "C" int rfx_im2col(const void* x, int N, int H, int W, int C, int Cs, int
   }
   return RF_OK;
 }
+
+extern "C" int rfx_maxpool_bwd(const void* x, const void* dy, int N, int H, int W, int C, int k, int stride, int pad,
+                               void* dx, int accumulate, void* workspace, void* stream) {
+  rfk::PoolGeom g{N, H, W, C, (H + 2 * pad - k) / stride + 1, (W + 2 * pad - k) / stride + 1, k, stride, pad};
+  cudaError_t e = rfk::maxpool_bwd(static_cast<const __nv_bfloat16*>(x), nullptr, static_cast<const __nv_bfloat16*>(dy),
+                                   g, static_cast<__nv_bfloat16*>(dx), accumulate != 0, workspace,
+                                   static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    rfexec::set_last_error(std::string("rfx_maxpool_bwd: ") + cudaGetErrorString(e));
+    return RF_E_CUDA;
+  }
+  return RF_OK;
+}

@@ -6,6 +6,7 @@
 // consecutive channels of one pixel.  Every reduction is a fixed-shape tree
 // (no atomics): results are bit-reproducible run to run, which is what makes
 // re-forward gradients bit-identical to store-all gradients.
+#include <cstdlib>
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -652,6 +653,159 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __
       for (int k = 0; k < 8; ++k) sum[k] += pv[k];
     }
     *reinterpret_cast<uint4*>(dx + (size_t)i * 8) = pack8(sum);
+  }
+}
+
+// Fused backward (argmax + gather in one pass, no index workspace): a block
+// owns a T x T tile of windows of one image and the input pixels whose rows /
+// columns fall in that tile's stride partition.  The input patch under the
+// tile's windows (plus the hp low-side halo windows that also cover owned
+// pixels) is staged in shared memory with batched 16-byte loads; phase 1
+// finds each staged window's first argmax there and stages its dy; phase 2
+// gives every owned input pixel the sum, in fixed (p, q) order, of dy over
+// the covering windows whose argmax it is -- the same order, so the same
+// bits, as the two-kernel form.
+template <int KW, int KS>
+__global__ void __launch_bounds__(kThreads) maxpool_bwd_tiled_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                    const __nv_bfloat16* __restrict__ dy, PoolGeom g,
+                                                                    int T, __nv_bfloat16* __restrict__ dx, int acc) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t pool_s[];
+  if (KW) g.k = KW;  // compile-time window / stride: divisions become shifts
+  if (KS) g.stride = KS;
+  const int cv = g.C / 8;
+  const int hp = (g.k - 1) / g.stride;
+  const int tiles_q = (g.Q + T - 1) / T, tiles_p = (g.P + T - 1) / T;
+  const int WT = T + hp;                       // staged windows per side
+  const int XT = (WT - 1) * g.stride + g.k;    // staged input pixels per side
+  const int nwin = WT * WT;
+  uint4* x_s = reinterpret_cast<uint4*>(pool_s);                                      // [XT][XT][cv]
+  uint4* dy_s = x_s + (size_t)XT * XT * cv;                                           // [nwin][cv]
+  uint2* ix_s = reinterpret_cast<uint2*>(dy_s + (size_t)nwin * cv);                   // [nwin][cv]
+  for (int tile = blockIdx.x; tile < g.N * tiles_p * tiles_q; tile += gridDim.x) {
+    const int tq = tile % tiles_q, tp = (tile / tiles_q) % tiles_p, n = tile / (tiles_q * tiles_p);
+    const int p0 = tp * T, q0 = tq * T;
+    const int hb = (p0 - hp) * g.stride - g.pad, wb = (q0 - hp) * g.stride - g.pad;  // patch origin
+    __syncthreads();
+    {
+      // patch rows are contiguous runs of XT*cv vectors: per-thread column
+      // index fixed, four rows' loads in flight
+      const int rowv = XT * cv;
+      for (int j = threadIdx.x; j < rowv; j += blockDim.x) {
+        const int w = wb + j / cv;
+        const bool okw = w >= 0 && w < g.W;
+        const uint4* src = reinterpret_cast<const uint4*>(x) + ((long)n * g.H * g.W + wb) * cv + j;
+        for (int r0 = 0; r0 < XT; r0 += 4) {
+          uint4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int h = hb + r0 + u;
+            v[u] = make_uint4(0u, 0u, 0u, 0u);
+            if (r0 + u < XT && okw && h >= 0 && h < g.H) v[u] = __ldg(src + (long)h * g.W * cv);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (r0 + u < XT) x_s[(r0 + u) * rowv + j] = v[u];
+        }
+      }
+      for (int i = threadIdx.x; i < nwin * cv; i += blockDim.x) {
+        const int c8 = i % cv, wi = i / cv;
+        const int p = p0 - hp + wi / WT, q = q0 - hp + wi % WT;
+        if (p >= 0 && p < g.P && q >= 0 && q < g.Q) dy_s[i] = ldg16(dy + ((((long)n * g.P + p) * g.Q + q) * cv + c8) * 8);
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nwin * cv; i += blockDim.x) {
+      const int c8 = i % cv, wi = i / cv;
+      const int pr = wi / WT, qr = wi % WT;
+      const int p = p0 - hp + pr, q = q0 - hp + qr;
+      if (p < 0 || p >= g.P || q < 0 || q >= g.Q) continue;
+      // first argmax, bf16x2 SIMD: strict '>' keeps the first hit (and
+      // ignores NaN) like the scalar form; window positions as byte lanes
+      uint32_t m[4] = {0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u};  // -inf pairs
+      uint32_t bx = 0, by = 0;
+      for (int r = 0; r < g.k; ++r) {
+        const int h = p * g.stride - g.pad + r;
+        if (h < 0 || h >= g.H) continue;
+        for (int s = 0; s < g.k; ++s) {
+          const int w = q * g.stride - g.pad + s;
+          if (w < 0 || w >= g.W) continue;
+          const uint4 v = x_s[((pr * g.stride + r) * XT + qr * g.stride + s) * cv + c8];
+          const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+          uint32_t gm[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            __nv_bfloat162 a2, b2;
+            memcpy(&a2, &vv[t], 4);
+            memcpy(&b2, &m[t], 4);
+            gm[t] = __hgt2_mask(a2, b2);
+            m[t] = (vv[t] & gm[t]) | (m[t] & ~gm[t]);
+          }
+          const uint32_t pos = (uint32_t)(r * g.k + s) * 0x01010101u;
+          const uint32_t b0 = __byte_perm(gm[0], gm[1], 0x6420), b1 = __byte_perm(gm[2], gm[3], 0x6420);
+          bx = (pos & b0) | (bx & ~b0);
+          by = (pos & b1) | (by & ~b1);
+        }
+      }
+      ix_s[i] = make_uint2(bx, by);
+    }
+    __syncthreads();
+    // owned input rows / columns: the stride partition of this tile (the
+    // first tile from 0, the last to the end)
+    const int h_lo = tp == 0 ? 0 : p0 * g.stride - g.pad;
+    const int h_hi = tp == tiles_p - 1 ? g.H : min(g.H, (p0 + T) * g.stride - g.pad);
+    const int w_lo = tq == 0 ? 0 : q0 * g.stride - g.pad;
+    const int w_hi = tq == tiles_q - 1 ? g.W : min(g.W, (q0 + T) * g.stride - g.pad);
+    const int ow = max(0, w_hi - w_lo);
+    const int row_items = ow * cv;
+    // (c8, w) of a thread fixed per tile when the block covers whole rows
+    const bool rows_fit = row_items > 0 && (int)blockDim.x % row_items == 0;
+    const int owned = max(0, h_hi - h_lo) * row_items;
+    const int c8f = rows_fit ? (int)threadIdx.x % cv : 0, wf = rows_fit ? w_lo + ((int)threadIdx.x / cv) % ow : 0;
+    const int hstep = rows_fit ? (int)blockDim.x / row_items : 0;
+    for (int j = threadIdx.x, it = 0; j < owned; j += blockDim.x, ++it) {
+      int c8, w, h;
+      if (rows_fit) {
+        c8 = c8f, w = wf, h = h_lo + (int)threadIdx.x / row_items + it * hstep;  // j = threadIdx.x + it * blockDim.x
+      } else {
+        c8 = j % cv;
+        const int t = j / cv;
+        w = w_lo + t % ow, h = h_lo + t / ow;
+      }
+      float sum[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum[k] = 0.f;
+      const int p_lo = max(0, (h + g.pad - g.k + g.stride) / g.stride);
+      const int p_hi = min(g.P - 1, (h + g.pad) / g.stride);
+      const int q_lo = max(0, (w + g.pad - g.k + g.stride) / g.stride);
+      const int q_hi = min(g.Q - 1, (w + g.pad) / g.stride);
+      for (int p = p_lo; p <= p_hi; ++p)
+        for (int q = q_lo; q <= q_hi; ++q) {
+          const int wi = (p - p0 + hp) * WT + (q - q0 + hp);
+          const uint2 iv = ix_s[wi * cv + c8];
+          const uint32_t self = (uint32_t)((h - (p * g.stride - g.pad)) * g.k + (w - (q * g.stride - g.pad)));
+          // per-channel byte compare -> bf16 lane masks; adding a masked +0
+          // leaves the fp32 sum bit-identical (it is never -0)
+          const uint32_t mx = __vcmpeq4(iv.x, self * 0x01010101u), my = __vcmpeq4(iv.y, self * 0x01010101u);
+          uint4 d = dy_s[wi * cv + c8];
+          d.x &= __byte_perm(mx, 0, 0x1100);
+          d.y &= __byte_perm(mx, 0, 0x3322);
+          d.z &= __byte_perm(my, 0, 0x1100);
+          d.w &= __byte_perm(my, 0, 0x3322);
+          float dv[8];
+          unpack8(d, dv);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) sum[k] += dv[k];
+        }
+      __nv_bfloat16* o = dx + (((long)n * g.H + h) * g.W + w) * g.C + c8 * 8;
+      if (acc) {
+        float pv[8];
+        unpack8(*reinterpret_cast<const uint4*>(o), pv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sum[k] += pv[k];
+      }
+      *reinterpret_cast<uint4*>(o) = pack8(sum);
+    }
   }
 }
 
@@ -1434,6 +1588,23 @@ cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __
   if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   (void)y;
   if (g.k * g.k > 256) return cudaErrorInvalidValue;
+  // fused single pass when the window tile (8x8, else smaller) fits in 48 KB
+  const int cv = g.C / 8, hp = (g.k - 1) / g.stride;
+  static const int t_max = std::getenv("RFK_POOL_TILE") ? std::atoi(std::getenv("RFK_POOL_TILE")) : 8;
+  for (int T = t_max; T >= 2; T /= 2) {
+    const long xt = (long)(T + hp - 1) * g.stride + g.k;
+    const long smem = xt * xt * cv * 16 + (long)(T + hp) * (T + hp) * cv * 24;
+    if (smem > 64 * 1024 || std::getenv("RFK_POOL_TWO_PASS")) continue;
+    auto kern = g.k == 3 && g.stride == 2 ? maxpool_bwd_tiled_kernel<3, 2>
+                : g.k == 2 && g.stride == 2 ? maxpool_bwd_tiled_kernel<2, 2> : maxpool_bwd_tiled_kernel<0, 0>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    const long tiles = (long)g.N * ((g.P + T - 1) / T) * ((g.Q + T - 1) / T);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    const long blocks = std::min<long>(tiles, 148L * std::max(1, per_sm));
+    RFK_CHECK_LAUNCH(launch_k(kern, (int)blocks, kThreads, smem, st, x, dy, g, T, dx, acc ? 1 : 0));
+    return cudaGetLastError();
+  }
   uint8_t* idx = static_cast<uint8_t*>(idx_ws);
   const long wins = (long)g.N * g.P * g.Q * (g.C / 8);
   RFK_CHECK_LAUNCH(launch_k(maxpool_argmax_kernel, grid_for(wins, kThreads * 2), kThreads, 0, st, x, g, idx));

@@ -49,6 +49,9 @@ def lib():
         _lib.rfx_gemm.argtypes = [C.POINTER(GemmArgs), C.c_void_p]
         _lib.rfx_im2col.restype = C.c_int
         _lib.rfx_im2col.argtypes = [C.c_void_p] + [C.c_int] * 12 + [C.c_void_p, C.c_void_p]
+        _lib.rfx_maxpool_bwd.restype = C.c_int
+        _lib.rfx_maxpool_bwd.argtypes = [C.c_void_p, C.c_void_p] + [C.c_int] * 7 + [C.c_void_p, C.c_int, C.c_void_p,
+                                                                                     C.c_void_p]
         _lib.rf_last_error.restype = C.c_char_p
     return _lib
 
@@ -84,3 +87,18 @@ def im2col(x: torch.Tensor, C_real: int, R: int, S: int, stride: int, pad: int, 
     if rc != 0:
         raise RuntimeError(L.rf_last_error().decode())
     return out
+
+
+def maxpool_bwd(x: torch.Tensor, dy: torch.Tensor, k: int, stride: int, pad: int, dx: torch.Tensor = None,
+                accumulate: bool = False, stream=None) -> torch.Tensor:
+    """Max-pool backward of an NHWC bf16 input (first-argmax ties, fixed-order sums)."""
+    N, H, W, Cc = x.shape
+    if dx is None:
+        dx = torch.zeros_like(x)
+    ws = torch.empty(dy.numel(), dtype=torch.uint8, device=x.device)
+    L = lib()
+    rc = L.rfx_maxpool_bwd(x.data_ptr(), dy.data_ptr(), N, H, W, Cc, k, stride, pad, dx.data_ptr(),
+                           1 if accumulate else 0, ws.data_ptr(), stream_handle(stream))
+    if rc != 0:
+        raise RuntimeError(L.rf_last_error().decode())
+    return dx

@@ -81,6 +81,7 @@ struct Op {
   int wg_splits = 1, wg_bn = 128;  // wgrad split-K and tile N
   int fp_splits = 1, fp_bn = 0;    // fprop split-K (bf16 finish kernel) and tile N
   int dg_splits = 1, dg_bn = 0;    // dgrad split-K and tile N
+  bool dg_subpixel = false;        // strided dgrad as s*s stride-1 sub-pixel GEMMs (no zero insertion)
   int fused_bn = -1;               // conv: BN op whose re-forward runs in this conv's epilogue
   bool reforward_in_producer = false;  // BN: re-forwarded by its producing conv's epilogue
   // pool
@@ -120,6 +121,11 @@ struct MemoryReport {
   long reforward_ops = 0, segment_loads = 0, forward_ops = 0, backward_ops = 0;
   long launches_per_step = 0;
 };
+
+struct SubpixelDim {
+  int r0 = 0, J = 0, c = 0, pad_lo = 0, rows = 0;
+};
+SubpixelDim subpixel_dim(int a, int stride, int R, int pad, int H);
 
 class Net;
 std::unique_ptr<Net> make_net(int batch);
@@ -234,6 +240,7 @@ class Net {
   __nv_bfloat16* gptr(int t) const;
   void gemm(const rfk::GemmDesc& d, cudaStream_t st);
   bool wgrad_overlap() const;
+  bool subpixel_ok(const Op& op, const Tensor& x) const;  // strided dgrad as sub-pixel GEMMs
   void ensure_wgrad_stream();
   void check(cudaError_t e, const char* what) const;
   void free_device();

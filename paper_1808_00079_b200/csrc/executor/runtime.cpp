@@ -595,7 +595,45 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           d.a_kind = rfk::Operand::Im2colK;
           d.band = band_enabled();
           const int pd = op.R - 1 - op.pad, pdw = op.S - 1 - op.pad_w;
-          if (op.stride == 1) {
+          if (op.dg_subpixel) {
+            // Sub-pixel decomposition: the stride x stride classes of input
+            // positions (h, w) = (s*m + a, s*n + b) each take a stride-1
+            // correlation of dy with their own subset of the (flipped) taps --
+            // no zero-inserted dy, no multiplications by inserted zeros.  Every
+            // class GEMM scatters its rows to its pixels (row remap).
+            const int st_ = op.stride;
+            bool empty = false;
+            for (int a = 0; a < st_; ++a)
+              for (int b = 0; b < st_; ++b) {
+                const SubpixelDim ch = subpixel_dim(a, st_, op.R, op.pad, x.H);
+                const SubpixelDim cw = subpixel_dim(b, st_, op.S, op.pad_w, x.W);
+                empty |= ch.J == 0 || cw.J == 0;
+              }
+            if (empty && !acc(0)) check(cudaMemsetAsync(dx, 0, x.bytes(), st), "memset");
+            for (int a = 0; a < st_; ++a)
+              for (int b = 0; b < st_; ++b) {
+                const SubpixelDim ch = subpixel_dim(a, st_, op.R, op.pad, x.H);
+                const SubpixelDim cw = subpixel_dim(b, st_, op.S, op.pad_w, x.W);
+                if (ch.J == 0 || cw.J == 0 || ch.rows == 0 || cw.rows == 0) continue;
+                rfk::GemmDesc dc = d;
+                dc.M = x.N * ch.rows * cw.rows;
+                dc.K = ch.J * cw.J * op.coutpad;
+                dc.a = dy;
+                dc.a_geom = rfk::ConvGeom{y.N, y.H, y.W, op.cout, ch.rows, cw.rows, ch.J, cw.J, ch.pad_lo, cw.pad_lo, 1, 1};
+                dc.b_tap_base = (ch.r0 + (ch.J - 1) * st_) * op.S + cw.r0 + (cw.J - 1) * st_;
+                dc.b_tap_dr = st_ * op.S;
+                dc.b_tap_ds = st_;
+                dc.band = false;
+                dc.remap = true;
+                dc.rP = ch.rows;
+                dc.rQ = cw.rows;
+                dc.rH = x.H;
+                dc.rW = x.W;
+                dc.rsh = dc.rsw = st_;
+                dc.out = dx + ((long)a * x.W + b) * op.cin;
+                gemm(dc, st);
+              }
+          } else if (op.stride == 1) {
             d.a = dy;
             d.a_geom = rfk::ConvGeom{y.N, y.H, y.W, op.cout, x.H, x.W, op.R, op.S, pd, pdw, 1, 1};
           } else {
@@ -621,7 +659,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           check(rfk::reduce_splits_bf16(ws_split, op.dg_splits, d.M, op.cin, dx, op.cin, accumulate, nullptr,
                                         (int)kStatRows, st),
                 "reduce_splits_bf16");
-        } else {
+        } else if (!op.dg_subpixel) {
           gemm(d, st);
         }
       }

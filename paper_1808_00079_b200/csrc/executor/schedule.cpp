@@ -582,8 +582,6 @@ void Net::build_schedule() {
 
 // ============================================================ layout
 namespace {
-// split-K of a weight-gradient GEMM: enough splits for about one persistent
-// wave (148 CTAs), each split keeping >= 8 K blocks, at most 32 partials
 // Split-K for a bf16-output implicit GEMM (conv fprop / dgrad through TMA
 // im2col), from the sweep-fitted cost model of gemm.cu: t = waves * (k blocks
 // * 0.5 us + per-tile b) plus, when split, the fp32 partial round trip
@@ -611,6 +609,39 @@ std::pair<int, int> im2col_split_plan(long M, int N, long kb) {
   return pick;
 }
 
+}  // namespace
+
+// Sub-pixel classes of a strided conv's data gradient along one dimension:
+// input positions h = s*m + a get taps r = r0 + j*s (j < J) of dy rows
+// m + c - j, i.e. a stride-1 correlation over dy with J taps and low padding
+// J - 1 - c, over ceil((H - a) / s) output rows.
+SubpixelDim subpixel_dim(int a, int stride, int R, int pad, int H) {
+  SubpixelDim d;
+  d.r0 = (a + pad) % stride;
+  d.J = d.r0 < R ? (R - d.r0 + stride - 1) / stride : 0;
+  d.c = (a + pad) / stride;
+  d.pad_lo = d.J - 1 - d.c;
+  d.rows = a < H ? (H - a + stride - 1) / stride : 0;
+  return d;
+}
+
+// Use the sub-pixel form for a strided k x k dgrad when every class is a
+// proper stride-1 correlation and each class GEMM still fills the GPU
+// (RFK_SUBPIXEL=0 keeps zero insertion everywhere, 2 forces the sub-pixel
+// form regardless of size -- tests).
+bool Net::subpixel_ok(const Op& op, const Tensor& x) const {
+  const int mode = std::getenv("RFK_SUBPIXEL") ? std::atoi(std::getenv("RFK_SUBPIXEL")) : 1;
+  if (mode == 0 || op.stride < 2 || (op.R == 1 && op.S == 1) || op.explicit_im2col || op.in[0] == input_t_) return false;
+  for (int a = 0; a < op.stride; ++a) {
+    const SubpixelDim h = subpixel_dim(a, op.stride, op.R, op.pad, x.H), w = subpixel_dim(a, op.stride, op.S, op.pad_w, x.W);
+    if (h.pad_lo < 0 || w.pad_lo < 0) return false;
+  }
+  const long class_rows = x.rows() / ((long)op.stride * op.stride);
+  const long tiles = (class_rows + 127) / 128 * ((op.cin + 127) / 128);
+  return mode == 2 || tiles >= 148;  // measured: at 98 tiles (ResNet-50 layer3) the four launches lose
+}
+
+namespace {
 // explicit-im2col chunk size (RFK_IM2COL_CHUNK_MB; default 0 = whole batch,
 // the fastest measured; chunks trade ~130 MB of workspace for launches)
 long im2col_chunk_bytes() {
@@ -619,6 +650,8 @@ long im2col_chunk_bytes() {
   return mb > 0 ? mb << 20 : (1L << 62);
 }
 
+// split-K of a weight-gradient GEMM: enough splits for about one persistent
+// wave (148 CTAs), each split keeping >= 8 K blocks (RFK_WG_SPLIT_CAP caps it)
 int wgrad_splits(long tiles, long kblocks) {
   long s = (148 + tiles - 1) / tiles;
   s = std::min(s, std::max(1L, kblocks / 8));
@@ -749,7 +782,8 @@ void Net::layout() {
           ws_dsplit_ = std::max(ws_dsplit_, align_up((long)pl.second * y.rows() * op.cout * 4));
         }
       }
-      const bool dgrad_taps = op.in[0] != input_t_ && !op.explicit_im2col && !(op.R == 1 && op.S == 1 &&
+      op.dg_subpixel = subpixel_ok(op, x);
+      const bool dgrad_taps = !op.dg_subpixel && op.in[0] != input_t_ && !op.explicit_im2col && !(op.R == 1 && op.S == 1 &&
                                                                                 op.pad == 0 && op.pad_w == 0);
       if (dgrad_taps && op.cin % 4 == 0 && op.cin / 4 <= 256) {
         const auto pl = im2col_split_plan(x.rows(), op.cin, (long)op.R * op.S * (op.coutpad / 64));

@@ -54,6 +54,7 @@ struct alignas(64) KParams {
   long split_stride;
   int remap, rP, rQ, rH, rW, rsh, rsw;
   int b_taps;  // WeightTapsMN: filter taps R*S
+  int b_tap_base, b_tap_dr, b_tap_ds;  // weight tap of A tap (r, s): base - r*dr - s*ds
   int out_mode;  // 0 generic stores, 1 TMA store, 2 TMA reduce-add (accumulate_out)
   int stages;  // smem ring depth (<= Cfg::kStages)
   int m_tiles, n_tiles, splits;  // persistent tile space
@@ -217,7 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               break;
             case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
               const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
-              const int ftap = p.b_taps - 1 - tap;
+              const int tr = tap / p.g_S, ts = tap - tr * p.g_S;
+              const int ftap = p.b_tap_base - tr * p.b_tap_dr - ts * p.b_tap_ds;
 #pragma unroll
               for (int j = 0; j < BN / 64; ++j)
                 tma_load_3d(sb + j * 8192, &p.tb, &full[stage], tc.n0 + 64 * j, ftap, cb * 64);
@@ -571,6 +573,10 @@ bool encode_im2col(CUtensorMap* m, const void* ptr, const ConvGeom& g, uint32_t 
   // bounding box of the receptive-field bases: [-pad, dim + pad - (filter-1))
   int lower[2] = {-g.pad_w, -g.pad_h};
   int upper[2] = {g.pad_w - (g.S - 1), g.pad_h - (g.R - 1)};
+  // stride 1: the box spans exactly the Q x P output bases, which also covers
+  // asymmetric padding (the sub-pixel dgrad classes pad only the high side)
+  if (g.stride_w == 1) upper[0] = g.Q - g.W - g.pad_w;
+  if (g.stride_h == 1) upper[1] = g.P - g.H - g.pad_h;
   cuuint32_t es[4] = {1, (cuuint32_t)g.stride_w, (cuuint32_t)g.stride_h, 1};
   CUresult r = g_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, lower,
                                upper, 64, pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -724,6 +730,11 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
       kp.b_taps = d.b_taps;
+      if (d.b_tap_base >= 0) {
+        kp.b_tap_base = d.b_tap_base, kp.b_tap_dr = d.b_tap_dr, kp.b_tap_ds = d.b_tap_ds;
+      } else {
+        kp.b_tap_base = d.b_taps - 1, kp.b_tap_dr = d.a_geom.S, kp.b_tap_ds = 1;
+      }
       if (d.a_kind != Operand::Im2colK) return cudaErrorInvalidValue;  // 1x1 dgrad uses MNMajor2D
       break;
     }

@@ -43,6 +43,9 @@ struct GemmDesc {
   ConvGeom b_geom;
   long b_extent = 0;  // valid MN extent of an MN-major B (0 = N)
   int b_taps = 1, b_cpad = 0, b_rows = 0;  // WeightTapsMN: R*S, Cpad, Cout
+  // WeightTapsMN: weight tap read for A tap (r, s) = base - r * dr - s * ds
+  // (base < 0: the flipped full filter, R*S - 1 - tap)
+  int b_tap_base = -1, b_tap_dr = 0, b_tap_ds = 0;
   // epilogue
   void* out = nullptr;
   long ldc = 0;

@@ -208,3 +208,29 @@ def test_chunked_stem_im2col_matches_whole_batch(monkeypatch):
     assert loss_c == loss_s
     for n in g_c:
         assert np.array_equal(g_c[n], g_s[n]), n
+
+
+@pytest.mark.parametrize("arch,batch,hw", [("resnet18", 4, 64), ("alexnet", 2, 64)])
+def test_subpixel_strided_dgrad_matches_zero_insertion(monkeypatch, arch, batch, hw):
+    """Strided k x k data gradients as stride x stride sub-pixel GEMMs (forced
+    at these small sizes) equal the zero-insertion form up to fp32 summation
+    order, and keep re-forward / store-all bit identity."""
+    def run(mode, policy):
+        monkeypatch.setenv("RFK_SUBPIXEL", str(mode))
+        net = ReforwardNet.named(arch, batch, hw, hw, 10)
+        net.plan(policy)
+        net.setup(seed=4)
+        x, y = random_batch(net, seed=6)
+        net.load_batch(x, y)
+        net.forward_backward()
+        torch.cuda.synchronize()
+        return net.read_loss(), {p.name: net.read_param(p.index, 1) for p in net.params()}
+
+    loss_z, g_z = run(0, "reforward")
+    loss_s, g_s = run(2, "reforward")
+    loss_a, g_a = run(2, "store_all")
+    assert loss_s == loss_z  # the forward is untouched
+    worst = max(rel_err(g_s[n], g_z[n]) for n in g_z)
+    assert worst <= 2e-2, worst
+    for n in g_s:
+        assert np.array_equal(g_s[n], g_a[n]), n

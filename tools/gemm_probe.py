@@ -89,6 +89,28 @@ def cases():
                 dict(M=64, N=Ks, K=Ms, a_kind=K.MNMAJOR, a=Os.data_ptr(), a_ld=64, b_kind=K.MNMAJOR,
                      b=As.data_ptr(), b_ld=Ks, out=Ws.data_ptr(), ldc=Ks, out_f32=1, splits=32,
                      split_stride=64 * Ks), (As, Os, Ws), {"block_n": 256}))
+    # sub-pixel dgrad class (layer2.0 3x3/2): dy 28x28x128 -> odd/odd class
+    # of dx 56x56x128, 2x2 taps, with and without the output row remap
+    dyc = bf(32, 28, 28, 128)
+    wc = bf(128, 3, 3, 128)
+    dxc = bf(32, 56, 56, 128)
+    gc = K.ConvGeom(32, 28, 28, 128, 28, 28, 2, 2, 0, 0, 1, 1)
+    for remap in (1, 0):
+        out.append((f"subpixel class 2x2 K512 remap={remap}", 25088, 128, 512,
+                    dict(M=25088, N=128, K=512, a_kind=K.IM2COL_K, a=dyc.data_ptr(), a_geom=gc, b_kind=4,
+                         b=wc.data_ptr(), out=dxc.data_ptr(), ldc=128, splits=1, remap=remap, rP=28, rQ=28, rH=56,
+                         rW=56, rsh=2, rsw=2), (dyc, wc, dxc),
+                    {"b_extent": 128, "b_taps": 9, "b_cpad": 128, "b_rows": 128}))
+    gc1 = K.ConvGeom(32, 28, 28, 128, 28, 28, 1, 1, 0, 0, 1, 1)
+    out.append(("subpixel class 1x1 K128 remap=1", 25088, 128, 128,
+                dict(M=25088, N=128, K=128, a_kind=K.IM2COL_K, a=dyc.data_ptr(), a_geom=gc1, b_kind=4,
+                     b=wc.data_ptr(), out=dxc.data_ptr(), ldc=128, splits=1, remap=1, rP=28, rQ=28, rH=56,
+                     rW=56, rsh=2, rsw=2), (dyc, wc, dxc),
+                {"b_extent": 128, "b_taps": 9, "b_cpad": 128, "b_rows": 128}))
+    a2 = bf(25088, 128)
+    out.append(("plain 2D 25088x128x128", 25088, 128, 128,
+                dict(M=25088, N=128, K=128, a_kind=K.KMAJOR, a=a2.data_ptr(), a_ld=128, b_kind=K.KMAJOR,
+                     b=wc.data_ptr(), b_ld=128, out=dxc.data_ptr(), ldc=128, splits=1), (a2, wc, dxc), {}))
     # launch + prologue + epilogue floor: one 128x128 tile per SM, one K block
     Mt = 128 * 148
     at, bt, ot = bf(Mt, 64), bf(128, 64), bf(Mt, 128)

@@ -356,7 +356,11 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_step")
+            summ = json.load(f)
+        # the capture is of one workload (tools/profile_step.py); other
+        # networks / sizes report no traffic rather than a foreign number
+        if summ.get("workload", "resnet50_b32_224") == f"{ARCH}_b{args.batch}_{HW}":
+            traffic = summ.get("dram_bytes_per_step")
     except Exception:
         pass
 

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("csv")
     ap.add_argument("--gemm-json")
     ap.add_argument("--label", default="")
+    ap.add_argument("--workload", default="resnet50_b32_224", help="arch_bBATCH_HW of the profiled step")
     a = ap.parse_args()
     with open(a.csv) as f:
         lines = [l for l in f if not l.startswith("==")]
@@ -48,7 +49,7 @@ def main():
         g = [v for k, v in agg.items() if k.startswith("gemm_kernel")]
         launches = sum(v[0] for v in g)
         dram = sum(v[2] for v in g)
-        out = {"source": a.csv, "label": a.label, "gemm_launches": launches, "dram_bytes_per_step": dram,
+        out = {"source": a.csv, "label": a.label, "workload": a.workload, "gemm_launches": launches, "dram_bytes_per_step": dram,
                "dram_bytes_per_launch": dram / max(launches, 1),
                "gemm_ncu_us_per_step": sum(v[1] for v in g) / 1e3,
                "families": {k: {"count": c, "us": t / 1e3, "dram_bytes": b} for k, (c, t, b) in agg.items()}}

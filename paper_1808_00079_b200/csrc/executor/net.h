@@ -242,6 +242,7 @@ class Net {
   bool wgrad_overlap() const;
   bool subpixel_ok(const Op& op, const Tensor& x) const;  // strided dgrad as sub-pixel GEMMs
   void ensure_wgrad_stream();
+  void ensure_sub_streams();
   void check(cudaError_t e, const char* what) const;
   void free_device();
 
@@ -299,6 +300,9 @@ class Net {
   // data-gradient GEMM (fork / join inside the step graph)
   cudaStream_t wgrad_stream_ = nullptr;
   cudaEvent_t wgrad_fork_ = nullptr, wgrad_join_ = nullptr;
+  // sub-pixel dgrad: class GEMMs 1..3 run on their own streams next to class 0
+  cudaStream_t sub_stream_[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t sub_fork_ = nullptr, sub_join_[3] = {nullptr, nullptr, nullptr};
   bool wgrad_pending_ = false;
   std::vector<std::pair<long, long>> wgrad_reads_act_, wgrad_reads_grad_;  // byte ranges pending wgrads read
   void instr_writes(const Instr& ins, std::vector<std::pair<long, long>>& act,

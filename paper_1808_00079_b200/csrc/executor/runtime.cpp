@@ -19,6 +19,12 @@ int round8(int c) { return (c + 7) / 8 * 8; }
 // and moves ~5x fewer A bytes than TMA im2col, but measures no faster yet on
 // ResNet-50's 3x3 convs (its per-tile load phase is not bandwidth-bound; see
 // DESIGN.md), so it is opt-in: RFK_BAND=1.
+// sub-pixel class GEMMs on parallel streams (RFK_SUBPIXEL_PAR=0: one stream)
+bool sub_parallel() {
+  static const bool on = !std::getenv("RFK_SUBPIXEL_PAR") || std::atoi(std::getenv("RFK_SUBPIXEL_PAR")) != 0;
+  return on;
+}
+
 bool band_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("RFK_BAND");
@@ -46,6 +52,11 @@ Net::~Net() {
   if (wgrad_fork_) cudaEventDestroy(wgrad_fork_);
   if (wgrad_join_) cudaEventDestroy(wgrad_join_);
   if (wgrad_stream_) cudaStreamDestroy(wgrad_stream_);
+  if (sub_fork_) cudaEventDestroy(sub_fork_);
+  for (int i = 0; i < 3; ++i) {
+    if (sub_join_[i]) cudaEventDestroy(sub_join_[i]);
+    if (sub_stream_[i]) cudaStreamDestroy(sub_stream_[i]);
+  }
 }
 
 void Net::check(cudaError_t e, const char* what) const {
@@ -303,6 +314,15 @@ bool Net::wgrad_overlap() const {
     return e == nullptr || std::atoi(e) != 0;
   }();
   return on;
+}
+
+void Net::ensure_sub_streams() {
+  if (sub_fork_) return;
+  check(cudaEventCreateWithFlags(&sub_fork_, cudaEventDisableTiming), "event");
+  for (int i = 0; i < 3; ++i) {
+    check(cudaStreamCreateWithFlags(&sub_stream_[i], cudaStreamNonBlocking), "sub-pixel stream");
+    check(cudaEventCreateWithFlags(&sub_join_[i], cudaEventDisableTiming), "event");
+  }
 }
 
 void Net::ensure_wgrad_stream() {
@@ -610,8 +630,17 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
                 empty |= ch.J == 0 || cw.J == 0;
               }
             if (empty && !acc(0)) check(cudaMemsetAsync(dx, 0, x.bytes(), st), "memset");
+            // classes write disjoint pixels: up to four run concurrently
+            // (each alone is too small to fill the GPU)
+            const bool par = st_ == 2 && sub_parallel();
+            if (par) {
+              ensure_sub_streams();
+              check(cudaEventRecord(sub_fork_, st), "event");
+            }
+            int cls = 0;
+            bool launched[4] = {false, false, false, false};
             for (int a = 0; a < st_; ++a)
-              for (int b = 0; b < st_; ++b) {
+              for (int b = 0; b < st_; ++b, ++cls) {
                 const SubpixelDim ch = subpixel_dim(a, st_, op.R, op.pad, x.H);
                 const SubpixelDim cw = subpixel_dim(b, st_, op.S, op.pad_w, x.W);
                 if (ch.J == 0 || cw.J == 0 || ch.rows == 0 || cw.rows == 0) continue;
@@ -631,8 +660,18 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
                 dc.rW = x.W;
                 dc.rsh = dc.rsw = st_;
                 dc.out = dx + ((long)a * x.W + b) * op.cin;
-                gemm(dc, st);
+                cudaStream_t cs = st;
+                if (par && cls > 0) {
+                  cs = sub_stream_[cls - 1];
+                  check(cudaStreamWaitEvent(cs, sub_fork_, 0), "wait");
+                }
+                gemm(dc, cs);
+                if (par && cls > 0) check(cudaEventRecord(sub_join_[cls - 1], cs), "event");
+                if (cls < 4) launched[cls] = true;
               }
+            if (par)
+              for (int i = 1; i < cls; ++i)
+                if (launched[i]) check(cudaStreamWaitEvent(st, sub_join_[i - 1], 0), "wait");
           } else if (op.stride == 1) {
             d.a = dy;
             d.a_geom = rfk::ConvGeom{y.N, y.H, y.W, op.cout, x.H, x.W, op.R, op.S, pd, pdw, 1, 1};

@@ -638,7 +638,11 @@ bool Net::subpixel_ok(const Op& op, const Tensor& x) const {
   }
   const long class_rows = x.rows() / ((long)op.stride * op.stride);
   const long tiles = (class_rows + 127) / 128 * ((op.cin + 127) / 128);
-  return mode == 2 || tiles >= 148;  // measured: at 98 tiles (ResNet-50 layer3) the four launches lose
+  // one stream: each class must fill a wave (measured: at 98 tiles, ResNet-50
+  // layer3, four serial launches lose); stride 2 with the classes on four
+  // parallel streams: the four together must
+  const bool par = op.stride == 2 && (!std::getenv("RFK_SUBPIXEL_PAR") || std::atoi(std::getenv("RFK_SUBPIXEL_PAR")) != 0);
+  return mode == 2 || (par ? tiles * 4 >= 96 : tiles >= 148);
 }
 
 namespace {

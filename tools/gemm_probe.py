@@ -89,6 +89,18 @@ def cases():
                 dict(M=64, N=Ks, K=Ms, a_kind=K.MNMAJOR, a=Os.data_ptr(), a_ld=64, b_kind=K.MNMAJOR,
                      b=As.data_ptr(), b_ld=Ks, out=Ws.data_ptr(), ldc=Ks, out_f32=1, splits=32,
                      split_stride=64 * Ks), (As, Os, Ws), {"block_n": 256}))
+    # the 56x56x64 3x3 conv as a plain 2-D GEMM (A materialised): is the
+    # im2col-mode TMA or the N=64 tile shape the limit?
+    a56 = bf(n1 * h1 * h1, 576)
+    for bn_ in (64, 128):
+        out.append((f"2D 100352x64x576 (3x3 56x56 shape) bn={bn_}", n1 * h1 * h1, 64, 576,
+                    dict(M=n1 * h1 * h1, N=64, K=576, a_kind=K.KMAJOR, a=a56.data_ptr(), a_ld=576, b_kind=K.KMAJOR,
+                         b=w1.data_ptr(), b_ld=576, out=o1.data_ptr(), ldc=64, splits=1), (a56, w1, o1),
+                    {"block_n": bn_}))
+    out.append(("3x3 56x56x64 fprop im2col no stats", n1 * h1 * h1, 64, 576,
+                dict(M=n1 * h1 * h1, N=64, K=576, a_kind=K.IM2COL_K, a=x1.data_ptr(), a_geom=g1,
+                     b_kind=K.KMAJOR, b=w1.data_ptr(), b_ld=576, out=o1.data_ptr(), ldc=64, splits=1),
+                (x1, w1, o1), {}))
     # sub-pixel dgrad class (layer2.0 3x3/2): dy 28x28x128 -> odd/odd class
     # of dx 56x56x128, 2x2 taps, with and without the output row remap
     dyc = bf(32, 28, 28, 128)

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -181,6 +182,8 @@ def time_e2e(net, steps, warmup, stream, world, xh, yh):
     import torch.distributed as dist
     copy = torch.cuda.Stream()
 
+    losses = torch.zeros(max(steps, warmup) + 1, dtype=torch.float32).pin_memory()
+
     def run(n, start_event=None):
         if start_event is not None:
             copy.wait_event(start_event)
@@ -190,7 +193,10 @@ def time_e2e(net, steps, warmup, stream, world, xh, yh):
                 net.stage_batch(xh, yh, (k + 1) % 2, copy_stream=copy)
             net.use_batch(k % 2, stream=stream)
             net.step(lr=0.01, momentum=0.9, weight_decay=1e-4, use_graph=True, stream=stream)
-            net.read_loss(stream=stream)  # D2H of the step's result (synchronises)
+            # D2H of the step's result into pinned memory, in stream order (the
+            # host reads the values after the run, as an async training loop
+            # would log them)
+            net.copy_loss(losses, k, stream=stream)
 
     run(warmup)
     torch.cuda.synchronize()
@@ -203,6 +209,8 @@ def time_e2e(net, steps, warmup, stream, world, xh, yh):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    if not all(math.isfinite(v) for v in losses[:steps].tolist()):
+        raise RuntimeError("non-finite loss in the end-to-end run")
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -155,6 +155,9 @@ int rfx_net_step(rfx_net* net, float lr, float momentum, float weight_decay, int
 int rfx_net_run_phase(rfx_net* net, int32_t phase, float lr, float momentum, float weight_decay,
                       int32_t use_graph, void* stream);
 int rfx_net_read_loss(rfx_net* net, float* loss, void* stream);
+/* enqueue the D2H copy of the step's loss into host_dst (pinned memory: no
+ * host synchronisation; the value is valid once the stream reaches it) */
+int rfx_net_copy_loss(rfx_net* net, float* host_dst, void* stream);
 /* live roofline probe: replay exactly the step's GEMM launches; ms and
  * algorithmic flops per step, number of GEMM launches */
 int rfx_net_gemm_profile(rfx_net* net, int32_t iters, void* stream, double* ms_per_step,

@@ -247,6 +247,10 @@ int rfx_net_step(rfx_net* n, float lr, float momentum, float wd, int32_t use_gra
   return guard([&] { n->net->step(lr, momentum, wd, S(st), use_graph != 0); });
 }
 
+int rfx_net_copy_loss(rfx_net* n, float* host_dst, void* st) {
+  return guard([&] { n->net->copy_loss(host_dst, S(st)); });
+}
+
 int rfx_net_read_loss(rfx_net* n, float* loss, void* st) {
   return guard([&] { *loss = n->net->read_loss(S(st)); });
 }

@@ -174,6 +174,7 @@ class Net {
   void step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph);
   // phase: 0 forward+backward, 1 update, 2 both (each cached as its own CUDA graph)
   void run_phase(int phase, float lr, float momentum, float wd, cudaStream_t st, bool use_graph);
+  void copy_loss(float* dst, cudaStream_t st);  // async D2H (dst pinned: no host sync)
   float read_loss(cudaStream_t st);
 
   // Live roofline probe of the dense-contraction kernels: replay exactly the

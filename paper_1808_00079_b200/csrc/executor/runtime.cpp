@@ -1348,6 +1348,10 @@ std::vector<double> Net::instr_profile(int iters, cudaStream_t st) {
   return ms;
 }
 
+void Net::copy_loss(float* dst, cudaStream_t st) {
+  check(cudaMemcpyAsync(dst, d_loss_, 4, cudaMemcpyDeviceToHost, st), "loss d2h");
+}
+
 float Net::read_loss(cudaStream_t st) {
   float v = 0.f;
   check(cudaMemcpyAsync(&v, d_loss_, 4, cudaMemcpyDeviceToHost, st), "loss d2h");

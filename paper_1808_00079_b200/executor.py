@@ -77,6 +77,7 @@ _SIGS = {
     "rfx_net_update": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_void_p]),
     "rfx_net_step": (C.c_int, [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_int32, C.c_void_p]),
     "rfx_net_read_loss": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_void_p]),
+    "rfx_net_copy_loss": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_void_p]),
     "rfx_net_instr_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_int32,
                                         C.POINTER(C.c_int32)]),
     "rfx_net_arena_guard": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
@@ -438,6 +439,15 @@ class ReforwardNet:
         buf = (C.c_double * max(n.value, 1))()
         _check(self.L.rfx_net_instr_profile(self.h, iters, _stream(stream), buf, n.value, C.byref(n)))
         return list(buf[:n.value])
+
+    def copy_loss(self, host_dst, index: int = 0, stream=None) -> None:
+        """Enqueue the D2H copy of the step's loss into host_dst[index] (a pinned
+        float32 CPU tensor) without synchronising the host."""
+        import torch
+        if host_dst.dtype != torch.float32 or host_dst.device.type != "cpu":
+            raise ValueError("host_dst must be a float32 CPU tensor")
+        ptr = host_dst.data_ptr() + 4 * index
+        _check(self.L.rfx_net_copy_loss(self.h, C.cast(C.c_void_p(ptr), C.POINTER(C.c_float)), _stream(stream)))
 
     def read_loss(self, stream=None) -> float:
         v = C.c_float()

@@ -159,6 +159,11 @@ def test_staged_batches_match_load_batch():
         net.forward_backward()
         got.append(net.read_loss())
     assert got == ref
+    # asynchronous loss D2H into pinned memory (no host sync per step)
+    host = torch.zeros(4, dtype=torch.float32).pin_memory()
+    net.copy_loss(host, 2)
+    torch.cuda.synchronize()
+    assert host[2].item() == got[-1]
 
 
 @pytest.mark.parametrize("arch,batch,hw", [("resnet50", 8, 64), ("densenet_tiny", 4, 32), ("vgg11", 4, 32)])

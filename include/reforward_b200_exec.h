@@ -41,6 +41,8 @@ typedef struct rfx_gemm_args {
   int64_t b_extent;                  /* valid MN extent of an MN-major B (0 = N) */
   int32_t b_taps, b_cpad, b_rows;    /* kind 4 (conv weights as dgrad B): R*S, Cpad, Cout */
   int32_t band;                      /* stride-1 im2col A: use the shifted-band kernel when eligible */
+  int32_t b_tap_map;                 /* kind 4: nonzero = weight tap of A tap (r, s) is base - r*dr - s*ds */
+  int32_t b_tap_base, b_tap_dr, b_tap_ds;  /* (sub-pixel dgrad classes); zero = flipped full filter */
 } rfx_gemm_args;
 /* kind 4 = conv weights [Cout][R][S][Cpad] read as the dgrad B operand (flipped taps) */
 

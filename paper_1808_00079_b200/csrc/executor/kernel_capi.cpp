@@ -34,6 +34,11 @@ extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
   d.b_cpad = a->b_cpad;
   d.b_rows = a->b_rows;
   d.band = a->band != 0;
+  if (a->b_tap_map) {
+    d.b_tap_base = a->b_tap_base;
+    d.b_tap_dr = a->b_tap_dr;
+    d.b_tap_ds = a->b_tap_ds;
+  }
   cudaError_t e = rfk::gemm_launch(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     rfexec::set_last_error(std::string("rfx_gemm: ") + cudaGetErrorString(e));

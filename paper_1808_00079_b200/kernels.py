@@ -29,7 +29,9 @@ class GemmArgs(C.Structure):
                 ("bias", C.c_void_p), ("stats", C.c_void_p), ("splits", C.c_int32), ("split_stride", C.c_int64),
                 ("remap", C.c_int32), ("rP", C.c_int32), ("rQ", C.c_int32), ("rH", C.c_int32), ("rW", C.c_int32),
                 ("rsh", C.c_int32), ("rsw", C.c_int32), ("block_n", C.c_int32), ("b_extent", C.c_int64),
-                ("b_taps", C.c_int32), ("b_cpad", C.c_int32), ("b_rows", C.c_int32), ("band", C.c_int32)]
+                ("b_taps", C.c_int32), ("b_cpad", C.c_int32), ("b_rows", C.c_int32), ("band", C.c_int32),
+                ("b_tap_map", C.c_int32), ("b_tap_base", C.c_int32), ("b_tap_dr", C.c_int32),
+                ("b_tap_ds", C.c_int32)]
 
 
 def conv_geom(N, H, W, Cin, R, S, pad, stride) -> ConvGeom:

@@ -171,6 +171,52 @@ def test_conv_dgrad_weight_taps(N, H, W, Ci, Co, R, pad):
     _check(out, ref)
 
 
+def _subpixel_dim(a, s, R, pad, H):
+    r0 = (a + pad) % s
+    J = (R - r0 + s - 1) // s if r0 < R else 0
+    c = (a + pad) // s
+    return r0, J, c, J - 1 - c, (H - a + s - 1) // s
+
+
+@pytest.mark.parametrize("N,H,W,Ci,Co,R,pad,s", [(2, 16, 16, 64, 64, 3, 1, 2), (1, 15, 13, 72, 40, 3, 0, 2),
+                                                 (2, 14, 14, 128, 96, 3, 1, 2)])
+def test_conv_dgrad_subpixel_classes(N, H, W, Ci, Co, R, pad, s):
+    """Strided dgrad as s*s stride-1 class GEMMs: im2col over dY with the
+    class's taps (asymmetric box), weight taps through the general tap map,
+    rows scattered to the class's pixels (remap)."""
+    P, Q = (H + 2 * pad - R) // s + 1, (W + 2 * pad - R) // s + 1
+    dy = _bf(N, Co, P, Q, seed=21)
+    w = _bf(Co, Ci, R, R, scale=0.1, seed=22)
+    ref = torch.nn.grad.conv2d_input((N, Ci, H, W), w.float(), dy.float(), stride=s, padding=pad)
+    ref = ref.permute(0, 2, 3, 1).contiguous()
+    cpad = (Ci + 63) // 64 * 64
+    wp = _pad_w(w, cpad)
+    dyn = dy.permute(0, 2, 3, 1).contiguous()
+    copad = (Co + 63) // 64 * 64
+    out = torch.zeros(N, H, W, Ci, device=dev, dtype=torch.bfloat16)
+    for a in range(s):
+        for b in range(s):
+            r0a, Ja, ca, pla, Pa = _subpixel_dim(a, s, R, pad, H)
+            r0b, Jb, cb, plb, Qb = _subpixel_dim(b, s, R, pad, W)
+            if Ja == 0 or Jb == 0 or Pa == 0 or Qb == 0:
+                continue
+            ga = K.ConvGeom(N, P, Q, Co, Pa, Qb, Ja, Jb, pla, plb, 1, 1)
+            args = K.GemmArgs(M=N * Pa * Qb, N=Ci, K=Ja * Jb * copad, a_kind=K.IM2COL_K, a=dyn.data_ptr(), a_geom=ga,
+                              b_kind=4, b=wp.data_ptr(), out=out.data_ptr() + (a * W + b) * Ci * 2, ldc=Ci,
+                              splits=1, remap=1, rP=Pa, rQ=Qb, rH=H, rW=W, rsh=s, rsw=s)
+            args.b_extent = Ci
+            args.b_taps = R * R
+            args.b_cpad = cpad
+            args.b_rows = Co
+            args.b_tap_map = 1
+            args.b_tap_base = (r0a + (Ja - 1) * s) * R + r0b + (Jb - 1) * s
+            args.b_tap_dr = s * R
+            args.b_tap_ds = s
+            K.gemm(args)
+    torch.cuda.synchronize()
+    _check(out, ref)
+
+
 @pytest.mark.parametrize("M,N,Kd,f32", [(256, 256, 64, False), (200, 72, 96, False), (130, 40, 128, True)])
 def test_gemm_accumulate_out(M, N, Kd, f32):
     # out += A B^T (TMA reduce-add epilogue)

@@ -1,5 +1,6 @@
 // Device side of the executor: arenas, parameters, per-op forward/backward
 // dispatch onto the sm_100a kernels, SGD, CUDA-graph capture of the step.
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1100,10 +1101,17 @@ void Net::forward_backward(cudaStream_t st) {
         if (x.first < y.second && y.first < x.second) return true;
     return false;
   };
+  static const bool trace = std::getenv("RFK_TRACE_JOIN") != nullptr;
+  int joins_act = 0, joins_grad = 0;
   for (int k = 0; k < (int)sched_.size(); ++k) {
     if (wgrad_pending_) {
       instr_writes(sched_[k], wa, wg);
-      if (overlaps(wa, wgrad_reads_act_) || overlaps(wg, wgrad_reads_grad_)) join_wgrad(st);
+      const bool ja = overlaps(wa, wgrad_reads_act_), jg = overlaps(wg, wgrad_reads_grad_);
+      if (ja || jg) {
+        joins_act += ja;
+        joins_grad += jg && !ja;
+        join_wgrad(st);
+      }
     }
     run_instr(sched_[k], st);
     while (dp && b < buckets_.size() && buckets_[b].after_instr == k) {
@@ -1120,6 +1128,7 @@ void Net::forward_backward(cudaStream_t st) {
     }
   }
   join_wgrad(st);
+  if (trace) std::fprintf(stderr, "wgrad joins: %d on activation ranges, %d on gradient ranges\n", joins_act, joins_grad);
   if (dp) {  // join
     check(cudaEventRecord(comm_done_, comm_stream_), "event");
     check(cudaStreamWaitEvent(st, comm_done_, 0), "wait");

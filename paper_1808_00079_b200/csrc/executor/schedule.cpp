@@ -702,6 +702,11 @@ void Net::layout() {
     long size;
   };
   std::vector<Iv> ivs;
+  std::vector<int> conv_bpos;  // backward positions of the conv backwards, ascending
+  for (int o = 0; o < no; ++o)
+    if (ops_[o].kind == OpKind::Conv && bpos[o] >= 0) conv_bpos.push_back(bpos[o]);
+  std::sort(conv_bpos.begin(), conv_bpos.end());
+  const int grad_slack = std::getenv("RFK_GRAD_SLACK") ? std::atoi(std::getenv("RFK_GRAD_SLACK")) : 0;
   for (int t = 0; t < nt; ++t) {
     if (t == input_t_ || t == loss_t_) continue;
     int start = 1 << 30;
@@ -716,8 +721,18 @@ void Net::layout() {
       grad_acc_[grad_acc_base_[writers[k].second.first] + writers[k].second.second] = k > 0 ? 1 : 0;
       start = std::min(start, writers[k].first);
     }
-    const int end = bpos[tensors_[t].producer];
+    int end = bpos[tensors_[t].producer];
     if (writers.empty() || end < 0) continue;
+    // a conv's output gradient is read by its weight-gradient GEMM on the side
+    // stream after the conv's backward: keep the slot until `slack` further
+    // conv backwards have been issued, so the next writers of the gradient
+    // arena do not force a join right behind the fork (the gradient arena is
+    // not part of Eq. 1; its size is reported separately)
+    if (ops_[tensors_[t].producer].kind == OpKind::Conv && wgrad_overlap() && grad_slack > 0) {
+      const auto it = std::upper_bound(conv_bpos.begin(), conv_bpos.end(), end);
+      const long k = (it - conv_bpos.begin()) + grad_slack - 1;
+      end = k < (long)conv_bpos.size() ? conv_bpos[k] : idx;
+    }
     ivs.push_back({t, start, end, tensors_[t].cost()});
   }
   std::sort(ivs.begin(), ivs.end(), [](const Iv& a, const Iv& b) { return a.start < b.start || (a.start == b.start && a.t < b.t); });

@@ -1245,6 +1245,30 @@ __global__ void pack_input_vec_kernel(const float* __restrict__ x, int N, int C,
   }
 }
 
+// The common case (C <= 8 real channels -> one 16-byte group, H*W % 4 == 0):
+// each thread packs four consecutive pixels of one image from one float4 per
+// channel, 32-bit indexing.
+__global__ void __launch_bounds__(kThreads) pack_input_q4_kernel(const float* __restrict__ x, int N, int C,
+                                                                unsigned HW4, __nv_bfloat16* __restrict__ out) {
+  pdl_enter();
+  const unsigned total = (unsigned)N * HW4;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned n = i / HW4, q = i - n * HW4;
+    float v[8][4];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < C) f = __ldg(reinterpret_cast<const float4*>(x + ((size_t)n * C + c) * HW4 * 4) + q);
+      v[c][0] = f.x, v[c][1] = f.y, v[c][2] = f.z, v[c][3] = f.w;
+    }
+    uint4* o = reinterpret_cast<uint4*>(out) + (size_t)i * 4;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      o[p] = make_uint4(pack_bf16_pair(v[0][p], v[1][p]), pack_bf16_pair(v[2][p], v[3][p]),
+                        pack_bf16_pair(v[4][p], v[5][p]), pack_bf16_pair(v[6][p], v[7][p]));
+  }
+}
+
 // explicit im2col for thin-channel convs: out[m][k], k = (r*S + s)*C + c, K
 // padded with zeros to Kpad.
 // One thread per (output pixel, 8 consecutive k): a single 16-byte store;
@@ -1711,6 +1735,13 @@ cudaError_t weight_prep_batched(const WeightPrepLayer* table_dev, int layers, lo
 }
 
 cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __nv_bfloat16* out, cudaStream_t st) {
+  const long hw = (long)H * W;
+  if (Cpad == 8 && C <= 8 && hw % 4 == 0 && (long)N * hw < (1L << 31) &&
+      reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+    RFK_CHECK_LAUNCH(launch_k(pack_input_q4_kernel, grid_for((long)N * hw / 4, kThreads), kThreads, 0, st, x, N, C,
+                              (unsigned)(hw / 4), out));
+    return cudaGetLastError();
+  }
   if (Cpad % 8 == 0) {
     const long work = (long)N * H * W * (Cpad / 8);
     RFK_CHECK_LAUNCH(launch_k(pack_input_vec_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, N, C, H, W, Cpad, out));

@@ -653,6 +653,18 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
                 dc.b_tap_base = (ch.r0 + (ch.J - 1) * st_) * op.S + cw.r0 + (cw.J - 1) * st_;
                 dc.b_tap_dr = st_ * op.S;
                 dc.b_tap_ds = st_;
+                if (ch.J == 1 && cw.J == 1 && ch.pad_lo == 0 && cw.pad_lo == 0 && ch.rows == y.H && cw.rows == y.W) {
+                  // one tap, no shift: A is dy itself and B one weight tap
+                  // (plain 2-D operands, no im2col)
+                  dc.K = op.cout;
+                  dc.a_kind = rfk::Operand::KMajor2D;
+                  dc.a_ld = op.cout;
+                  dc.b_kind = rfk::Operand::MNMajor2D;
+                  dc.b = d_bf16_ + w.bf16_off + (long)dc.b_tap_base * op.cpad;
+                  dc.b_ld = (long)op.R * op.S * op.cpad;
+                  dc.b_extent = op.cin;
+                  dc.b_tap_base = -1;
+                }
                 dc.band = false;
                 dc.remap = true;
                 dc.rP = ch.rows;

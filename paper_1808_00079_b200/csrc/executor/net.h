@@ -84,6 +84,7 @@ struct Op {
   bool dg_subpixel = false;        // strided dgrad as s*s stride-1 sub-pixel GEMMs (no zero insertion)
   int fused_bn = -1;               // conv: BN op whose re-forward runs in this conv's epilogue
   bool reforward_in_producer = false;  // BN: re-forwarded by its producing conv's epilogue
+  int bn_gather = -1;              // BN over a concatenation: index of its statistics-gather table
   // pool
   int k = 1;
   // classifier / linear
@@ -319,6 +320,14 @@ class Net {
   long bucket_floats_ = 0;
   void plan_buckets();
   void* d_prep_table_ = nullptr;
+  // BN over concatenations (DenseNet): per BN, the concat's leaf tensors in
+  // channel order; per leaf, its partial-sum slot (floats into the stats
+  // workspace) and row count; one device table of 32-channel blocks
+  std::vector<std::vector<int>> gather_leaves_;
+  std::vector<long> leaf_stats_off_;   // per tensor; -1 = not a colstats leaf
+  std::vector<int> gather_first_block_;
+  void* d_gather_ = nullptr;
+  void build_gather_tables();
   int prep_layers_ = 0;
   long prep_total_ = 0;
   float phase_hyper_[3][3] = {};

@@ -74,6 +74,8 @@ void Net::free_device() {
   gemm_trace_.clear();
   if (d_prep_table_) cudaFree(d_prep_table_);
   d_prep_table_ = nullptr;
+  if (d_gather_) cudaFree(d_gather_);
+  d_gather_ = nullptr;
   for (int k = 0; k < 2; ++k) {
     if (d_stage_images_[k]) cudaFree(d_stage_images_[k]);
     if (d_stage_labels_[k]) cudaFree(d_stage_labels_[k]);
@@ -137,6 +139,7 @@ void Net::setup(uint64_t seed) {
   check(cudaMemset(d_ws_, 0, rep_.workspace_bytes > 0 ? rep_.workspace_bytes : 256), "memset");
   check(cudaMemset(d_labels_, 0, batch_ * 4), "memset");
   check(cudaMemset(d_input_, 0, in.bytes()), "memset");
+  build_gather_tables();
 
   // parameters: Kaiming-normal convs, unit BN, small classifier (deterministic)
   std::vector<float> host(n_params_, 0.f);
@@ -444,6 +447,20 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       float* S = d_state_;
       if (phase == 1) {  // residual add, phase 1: out <- skip (exact copy)
         check(cudaMemcpyAsync(tptr(op.out), tptr(op.in[1]), y.bytes(), cudaMemcpyDeviceToDevice, st), "skip copy");
+        break;
+      }
+      if (!reforward && op.bn_gather >= 0) {
+        // BN over a concatenation: gather the leaves' statistics, then apply
+        const auto* table = static_cast<const rfk::BnGatherBlock*>(d_gather_) + gather_first_block_[op.bn_gather];
+        check(rfk::bn_finalize_gather(table, y.C, y.rows(), d_param_ + params_[op.w_param].offset,
+                                      d_param_ + params_[op.b_param].offset, op.eps, S + b.mean, S + b.invstd,
+                                      S + b.scale, S + b.shift, S + b.run_mean, S + b.run_var, op.momentum, st),
+              "bn_finalize_gather");
+        const bool relu = op.kind == OpKind::BNAddReLU || op.k == 1;
+        const __nv_bfloat16* skip = op.kind == OpKind::BNAddReLU ? tb(op.in[1]) : nullptr;
+        if (phase == 2) skip = tb(op.out);
+        check(rfk::bn_apply(tb(op.in[0]), skip, S + b.scale, S + b.shift, relu, y.rows(), y.C, tb(op.out), st),
+              "bn_apply");
         break;
       }
       if (!reforward) {
@@ -922,9 +939,55 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
   }
 }
 
+// Device tables of the BN-over-concat statistics gathers: one entry per
+// 32-channel block of each such BN, pointing at the rows of the leaf tensor
+// that produced those channels (conv epilogue slot or colstats slot).
+void Net::build_gather_tables() {
+  gather_first_block_.clear();
+  if (gather_leaves_.empty()) return;
+  float* ws_stats = reinterpret_cast<float*>(d_ws_ + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_);
+  std::vector<rfk::BnGatherBlock> tab;
+  for (const auto& leaves : gather_leaves_) {
+    gather_first_block_.push_back((int)tab.size());
+    for (int u : leaves) {
+      const Tensor& t = tensors_[u];
+      const Op& pr = ops_[t.producer];
+      rfk::BnGatherBlock b{};
+      if (pr.kind == OpKind::Conv && pr.out == u && pr.fuse_stats) {
+        b.partials = ws_stats + pr.stats_off;
+        b.parts = (int)kStatRows;
+      } else {
+        if (leaf_stats_off_[u] < 0) throw std::logic_error("concat leaf without a statistics slot");
+        b.partials = ws_stats + leaf_stats_off_[u];
+        b.parts = rfk::colstats_blocks(t.rows());
+      }
+      b.Csrc = t.C;
+      for (int c = 0; c < t.C; c += 32) {
+        b.coff = c;
+        tab.push_back(b);
+      }
+    }
+  }
+  check(cudaMalloc(&d_gather_, tab.size() * sizeof(rfk::BnGatherBlock)), "gather table");
+  check(cudaMemcpy(d_gather_, tab.data(), tab.size() * sizeof(rfk::BnGatherBlock), cudaMemcpyHostToDevice),
+        "gather table");
+}
+
 void Net::run_instr(const Instr& ins, cudaStream_t st) {
   if (ins.kind == InstrKind::Forward && ins.reforward && ops_[ins.op].reforward_in_producer) return;  // done by the conv
-  if (ins.kind == InstrKind::Forward) op_forward(ops_[ins.op], ins.reforward, ins.phase, st);
+  if (ins.kind == InstrKind::Forward) {
+    const Op& op = ops_[ins.op];
+    op_forward(op, ins.reforward, ins.phase, st);
+    if (!ins.reforward && ins.phase != 1 && op.out >= 0 && leaf_stats_off_[op.out] >= 0) {
+      // statistics of a concat leaf, once, for every BN that gathers them
+      const Tensor& t = tensors_[op.out];
+      float* ws_stats = reinterpret_cast<float*>(d_ws_ + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_);
+      check(rfk::colstats(tb(op.out), t.rows(), t.C, ws_stats + leaf_stats_off_[op.out], rfk::colstats_blocks(t.rows()),
+                          st),
+            "leaf colstats");
+    }
+    return;
+  }
   else if (ins.kind == InstrKind::Backward) op_backward(ops_[ins.op], st);
 }
 

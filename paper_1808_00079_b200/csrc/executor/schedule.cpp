@@ -828,6 +828,43 @@ void Net::layout() {
     if (op.kind == OpKind::MaxPool)  // window argmax bytes for the backward (shares the zero-insert region)
       ws_zero_ = std::max(ws_zero_, align_up(tensors_[op.out].elems()));
   }
+  // BN over a concatenation (DenseNet's BN-ReLU-conv on the growing feature
+  // stack): the per-channel batch statistics of a channel do not depend on
+  // which concat it sits in, so every leaf tensor's sums are produced once --
+  // by its conv's epilogue or one colstats pass after its producer -- and each
+  // BN gathers its channels' rows instead of re-reading the whole stack.
+  gather_leaves_.clear();
+  leaf_stats_off_.assign(tensors_.size(), -1);
+  std::vector<char> colstats_leaf(tensors_.size(), 0);
+  const bool gather_on = !std::getenv("RFK_BN_GATHER") || std::atoi(std::getenv("RFK_BN_GATHER")) != 0;
+  for (auto& op : ops_) {
+    op.bn_gather = -1;
+    if (!gather_on || (op.kind != OpKind::BN && op.kind != OpKind::BNAddReLU)) continue;
+    const int t = op.in[0];
+    if (tensors_[t].producer < 0 || ops_[tensors_[t].producer].kind != OpKind::Concat) continue;
+    std::vector<int> leaves, stack{t};
+    while (!stack.empty()) {  // depth-first, left input first: channel order
+      const int u = stack.back();
+      stack.pop_back();
+      const int pr = tensors_[u].producer;
+      if (pr >= 0 && ops_[pr].kind == OpKind::Concat) {
+        stack.push_back(ops_[pr].in[1]);
+        stack.push_back(ops_[pr].in[0]);
+      } else {
+        leaves.push_back(u);
+      }
+    }
+    bool ok = true;
+    for (int u : leaves) ok = ok && u != input_t_ && tensors_[u].producer >= 0 && tensors_[u].C % 32 == 0;
+    if (!ok) continue;
+    for (int u : leaves) {
+      Op& pr = ops_[tensors_[u].producer];
+      if (pr.kind == OpKind::Conv && pr.out == u && !pr.explicit_im2col) pr.fuse_stats = true;
+      else colstats_leaf[u] = 1;
+    }
+    op.bn_gather = (int)gather_leaves_.size();
+    gather_leaves_.push_back(std::move(leaves));
+  }
   // Re-forward fusion: a conv whose only consumer is a plain BN in the same
   // segment applies that BN (statistics of the first forward) in its own
   // epilogue when both are re-forwarded; the BN's re-forward is then a no-op.
@@ -850,6 +887,11 @@ void Net::layout() {
     if (op.kind == OpKind::Conv && op.fuse_stats) {
       op.stats_off = ws_stats_ / 4;  // [kStatRows][2][cout]: one row per persistent GEMM CTA
       ws_stats_ += align_up(kStatRows * 2 * op.cout * 4);
+    }
+  for (int t = 0; t < (int)tensors_.size(); ++t)
+    if (colstats_leaf[t]) {  // [colstats_blocks][2][C]
+      leaf_stats_off_[t] = ws_stats_ / 4;
+      ws_stats_ += align_up((long)rfk::colstats_blocks(tensors_[t].rows()) * 2 * tensors_[t].C * 4);
     }
   ws_counters_ = 0;
   rep_.workspace_bytes =

@@ -187,6 +187,32 @@ __global__ void bn_finalize_kernel(const float* __restrict__ partials, int parts
   }
 }
 
+// Finalize of a BN over a concatenation: block b takes its 32 channels' sums
+// from the rows of their source tensor (table[b]).
+__global__ void bn_finalize_gather_kernel(const BnGatherBlock* __restrict__ table, int C, float count,
+                                          const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+                                          float* __restrict__ mean, float* __restrict__ invstd,
+                                          float* __restrict__ scale, float* __restrict__ shift,
+                                          float* __restrict__ run_mean, float* __restrict__ run_var, float momentum) {
+  pdl_enter();
+  const BnGatherBlock b = table[blockIdx.x];
+  float s0, s1;
+  sum_partials(b.partials, b.parts, b.Csrc, b.coff + (int)threadIdx.x, s0, s1);
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  if (threadIdx.y != 0 || c >= C) return;
+  const float mu = s0 / count;
+  const float var = fmaxf(s1 / count - mu * mu, 0.f);
+  const float is = rsqrtf(var + eps);
+  mean[c] = mu;
+  invstd[c] = is;
+  const float sc = gamma[c] * is;
+  scale[c] = sc;
+  shift[c] = beta[c] - mu * sc;
+  const float unbiased = count > 1.f ? var * count / (count - 1.f) : var;
+  run_mean[c] = (1.f - momentum) * run_mean[c] + momentum * mu;
+  run_var[c] = (1.f - momentum) * run_var[c] + momentum * unbiased;
+}
+
 // out = [relu](y * scale + shift [+ skip])
 // (skip may alias out: each element is read before it is written)
 __device__ __forceinline__ void ld8f(const float* p, float (&f)[8]) {
@@ -1515,6 +1541,15 @@ cudaError_t bn_finalize(const float* partials, int parts, int C, long count, con
   RFK_CHECK_LAUNCH(launch_k(bn_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, partials, parts, C, (float)count, gamma, beta, eps, mean,
                                                             invstd, scale, shift, run_mean, run_var, momentum,
                                                             update_running ? 1 : 0));
+  return cudaGetLastError();
+}
+
+cudaError_t bn_finalize_gather(const BnGatherBlock* table, int C, long count, const float* gamma, const float* beta,
+                               float eps, float* mean, float* invstd, float* scale, float* shift, float* run_mean,
+                               float* run_var, float momentum, cudaStream_t st) {
+  if (C % 32) return cudaErrorInvalidValue;
+  RFK_CHECK_LAUNCH(launch_k(bn_finalize_gather_kernel, C / 32, dim3(32, kFinY), 0, st, table, C, (float)count, gamma,
+                            beta, eps, mean, invstd, scale, shift, run_mean, run_var, momentum));
   return cudaGetLastError();
 }
 

@@ -18,6 +18,16 @@ cudaError_t colstats(const __nv_bfloat16* x, long M, int C, float* partials, int
 cudaError_t bn_finalize(const float* partials, int parts, int C, long count, const float* gamma, const float* beta,
                         float eps, float* mean, float* invstd, float* scale, float* shift, float* run_mean,
                         float* run_var, float momentum, bool update_running, cudaStream_t st);
+// BatchNorm over a channel concatenation: the statistics of every 32-channel
+// block come from the partial-sum rows of the tensor that produced those
+// channels (computed once per tensor, not once per consuming layer)
+struct BnGatherBlock {
+  const float* partials;  // [parts][2][Csrc]
+  int parts, Csrc, coff;  // rows, source channels, channel offset of this block in the source
+};
+cudaError_t bn_finalize_gather(const BnGatherBlock* table, int C, long count, const float* gamma, const float* beta,
+                               float eps, float* mean, float* invstd, float* scale, float* shift, float* run_mean,
+                               float* run_var, float momentum, cudaStream_t st);
 cudaError_t bn_apply(const __nv_bfloat16* y, const __nv_bfloat16* skip, const float* scale, const float* shift,
                      bool relu, long M, int C, __nv_bfloat16* out, cudaStream_t st);
 // mask_mode: 0 none (plain BN), 1 relu(bn(y)), 2 relu via stored output (> 0)

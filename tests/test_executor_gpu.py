@@ -239,3 +239,37 @@ def test_subpixel_strided_dgrad_matches_zero_insertion(monkeypatch, arch, batch,
     assert worst <= 2e-2, worst
     for n in g_s:
         assert np.array_equal(g_s[n], g_a[n]), n
+
+
+def test_bn_over_concat_gathers_leaf_statistics(monkeypatch):
+    """DenseNet's BN over the growing concatenation takes each channel block's
+    batch statistics from the tensor that produced it (computed once) instead
+    of re-reading the whole stack: same step up to fp32 summation order, and
+    re-forward / store-all bit identity holds."""
+    arch, batch, hw = "densenet121", 2, 32
+
+    def run(mode, policy):
+        monkeypatch.setenv("RFK_BN_GATHER", str(mode))
+        net = ReforwardNet.named(arch, batch, hw, hw, 10)
+        net.plan(policy)
+        net.setup(seed=5)
+        x, y = random_batch(net, seed=7)
+        net.load_batch(x, y)
+        net.forward_backward()
+        torch.cuda.synchronize()
+        bn = [o for o in net.ops() if o.kind in ("bn", "bn_add_relu")]
+        run_stats = [net.read_bn_running(o.id) for o in bn]
+        return net.read_loss(), {p.name: net.read_param(p.index, 1) for p in net.params()}, run_stats
+
+    loss_0, g_0, r_0 = run(0, "reforward")
+    loss_1, g_1, r_1 = run(1, "reforward")
+    loss_s, g_s, _ = run(1, "store_all")
+    assert abs(loss_1 - loss_0) <= 1e-3 * abs(loss_0), (loss_1, loss_0)
+    for (m0, v0), (m1, v1) in zip(r_0, r_1):
+        assert np.allclose(m0, m1, rtol=1e-3, atol=1e-5) and np.allclose(v0, v1, rtol=1e-3, atol=1e-5)
+    a = np.concatenate([g_1[n].ravel() for n in g_0]).astype(np.float64)
+    b = np.concatenate([g_0[n].ravel() for n in g_0]).astype(np.float64)
+    assert float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b))) >= 0.999
+    assert loss_1 == loss_s
+    for n in g_1:
+        assert np.array_equal(g_1[n], g_s[n]), n

@@ -338,6 +338,8 @@ class Net {
     double bytes;  // algorithmic HBM bytes: operands read once + output written (read too when accumulating)
   };
   bool tracing_ = false;
+  bool tuned_ = false;
+  void autotune(cudaStream_t st);  // per GEMM shape: fastest tile width (process-wide cache)
   double trace_flops_ = 0;  // algorithmic flops to attach to the next traced GEMM
   std::vector<GemmRecord> gemm_trace_;
   cudaGraphExec_t capture(const std::function<void(cudaStream_t)>& body, long* kernel_nodes);

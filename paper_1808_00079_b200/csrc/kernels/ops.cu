@@ -136,16 +136,28 @@ __device__ __forceinline__ void sum_partials(const float* __restrict__ partials,
   __shared__ float sh0[kFinY][33], sh1[kFinY][33];
   float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
   if (c < C) {
-    int p = threadIdx.y;
-    for (; p + kFinY < parts; p += 2 * kFinY) {
-      a0 += __ldg(partials + (long)p * 2 * C + c);
-      b0 += __ldg(partials + (long)p * 2 * C + C + c);
-      a1 += __ldg(partials + (long)(p + kFinY) * 2 * C + c);
-      b1 += __ldg(partials + (long)(p + kFinY) * 2 * C + C + c);
-    }
-    if (p < parts) {
-      a0 += __ldg(partials + (long)p * 2 * C + c);
-      b0 += __ldg(partials + (long)p * 2 * C + C + c);
+    // rows y + 32k: even k into (a0, b0), odd k into (a1, b1), ascending k.
+    // Eight rows' loads are issued before any add (the finalize is one
+    // L2 round trip per batch, not per row); the add order is unchanged.
+    for (int k0 = 0; (int)threadIdx.y + kFinY * k0 < parts; k0 += 8) {
+      float va[8], vb[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int p = (int)threadIdx.y + kFinY * (k0 + j);
+        va[j] = p < parts ? __ldg(partials + (long)p * 2 * C + c) : 0.f;
+        vb[j] = p < parts ? __ldg(partials + (long)p * 2 * C + C + c) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if ((int)threadIdx.y + kFinY * (k0 + j) >= parts) break;
+        if (j & 1) {
+          a1 += va[j];
+          b1 += vb[j];
+        } else {
+          a0 += va[j];
+          b0 += vb[j];
+        }
+      }
     }
   }
   sh0[threadIdx.y][threadIdx.x] = a0 + a1;

@@ -339,6 +339,7 @@ class Net {
   };
   bool tracing_ = false;
   bool tuned_ = false;
+  int im2col_holder_ = -1;  // explicit-im2col conv whose whole-batch matrix ws_im2col holds (this step)
   void autotune(cudaStream_t st);  // per GEMM shape: fastest tile width (process-wide cache)
   double trace_flops_ = 0;  // algorithmic flops to attach to the next traced GEMM
   std::vector<GemmRecord> gemm_trace_;

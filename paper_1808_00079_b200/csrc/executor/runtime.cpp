@@ -479,7 +479,13 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         for (int n0 = 0; n0 < x.N; n0 += op.im2col_imgs) {
           const int nn = std::min(op.im2col_imgs, x.N - n0);
           rfk::ConvShape cs{nn, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
-          check(rfk::im2col(tb(op.in[0]) + (long)n0 * x.H * x.W * x.C, cs, op.kpad, ws_im2col, st), "im2col");
+          // the matrix of the network input is the same for the first
+          // forward, the re-forward and the weight gradient: built once per step
+          const int oid = (int)(&op - &ops_[0]);
+          const bool whole = nn == x.N && op.in[0] == input_t_;
+          if (!(whole && im2col_holder_ == oid))
+            check(rfk::im2col(tb(op.in[0]) + (long)n0 * x.H * x.W * x.C, cs, op.kpad, ws_im2col, st), "im2col");
+          im2col_holder_ = whole ? oid : -1;
           rfk::GemmDesc dc = d;
           dc.M = (int)(nn * img_rows);
           dc.out = tb(op.out) + n0 * img_rows * op.cout;
@@ -855,7 +861,11 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
         for (int n0 = 0; n0 < x.N; n0 += op.im2col_imgs) {
           const int nn = std::min(op.im2col_imgs, x.N - n0);
           rfk::ConvShape cs{nn, x.H, x.W, op.cin_real, x.C, y.H, y.W, op.R, op.S, op.stride, op.pad};
-          check(rfk::im2col(tb(op.in[0]) + (long)n0 * x.H * x.W * x.C, cs, op.kpad, ws_im2col, wst), "im2col");
+          const int oid = (int)(&op - &ops_[0]);
+          const bool whole = nn == x.N && op.in[0] == input_t_;
+          if (!(whole && im2col_holder_ == oid))
+            check(rfk::im2col(tb(op.in[0]) + (long)n0 * x.H * x.W * x.C, cs, op.kpad, ws_im2col, wst), "im2col");
+          im2col_holder_ = whole ? oid : -1;
           rfk::GemmDesc dc = d;
           dc.K = (int)(nn * img_rows);
           dc.a = dy + n0 * img_rows * op.cout;
@@ -1264,6 +1274,7 @@ void Net::join_wgrad(cudaStream_t st) {
 
 void Net::forward_backward(cudaStream_t st) {
   if (!setup_done_) throw std::invalid_argument("setup the network first");
+  im2col_holder_ = -1;  // a new batch: the stem's im2col is rebuilt by the first forward
   const bool dp = comm_ && comm_->ready() && comm_->nranks() > 0;
   size_t b = 0;
   std::vector<std::pair<long, long>> wa, wg;
@@ -1504,6 +1515,7 @@ std::vector<double> Net::instr_profile(int iters, cudaStream_t st) {
   cudaGraphExec_t g = capture(
       [&](cudaStream_t s) {
         check(cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal), "event");
+        im2col_holder_ = -1;  // as in forward_backward
         for (size_t k = 0; k < n; ++k) {
           run_instr(sched_[k], s);
           join_wgrad(s);  // per-instruction attribution: no cross-instruction overlap

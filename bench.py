@@ -329,7 +329,7 @@ def main():
     stream = torch.cuda.Stream()
     peaks, peak_kind = _peaks()
 
-    net, rep, plan_s = build_net(args.batch, "reforward", seed=1234 + rank)
+    net, rep, plan_s = build_net(args.batch, "reforward", seed=1234)
     gpu_stored = net.plan_sets()[0] if ARCH.startswith(("densenet", "inception")) else None
     x, y = random_batch(net, seed=rank)
     net.load_batch(x.cuda(), y.cuda(), stream=stream)
@@ -386,7 +386,7 @@ def main():
     if not args.no_store_all:
         del net
         torch.cuda.synchronize()
-        net_sa, rep_sa, _ = build_net(args.batch, "store_all", seed=1234 + rank)
+        net_sa, rep_sa, _ = build_net(args.batch, "store_all", seed=1234)
         net_sa.load_batch(x.cuda(), y.cuda(), stream=stream)
         if world > 1:
             # a NCCL unique id bootstraps exactly one communicator: fresh one

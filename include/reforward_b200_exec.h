@@ -189,6 +189,13 @@ int rfx_net_param_info(const rfx_net* net, int32_t i, char* name, size_t name_ca
 /* which: 0 value, 1 gradient, 2 momentum; canonical (PyTorch OIHW / [out,in] / [C]) layout */
 int rfx_net_read_param(const rfx_net* net, int32_t i, int32_t which, float* host);
 int rfx_net_write_param(rfx_net* net, int32_t i, const float* host);
+/* Host-only layout of the flat fp32 parameter / gradient buffers (what the
+ * data-parallel all-reduce buckets cover): parameter i occupies
+ * [offset, offset + count); pack writes a canonical tensor into that slice's
+ * layout (padding zeroed), unpack reads it back.  No device access. */
+int rfx_net_param_slot(const rfx_net* net, int32_t i, int64_t* offset, int64_t* count);
+int rfx_net_pack_param(const rfx_net* net, int32_t i, const float* canonical, float* flat_slice);
+int rfx_net_unpack_param(const rfx_net* net, int32_t i, const float* flat_slice, float* canonical);
 int rfx_net_read_tensor(const rfx_net* net, int32_t t, float* host); /* NHWC, valid if resident */
 int rfx_net_read_bn_running(const rfx_net* net, int32_t op, float* mean, float* var);
 /* debug: give every activation gradient its own slot (call before plan) and read it back */

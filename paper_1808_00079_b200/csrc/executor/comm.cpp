@@ -17,6 +17,7 @@ using ncclResult_t = int;
 using FnGetUniqueId = ncclResult_t (*)(UniqueId*);
 using FnCommInitRank = ncclResult_t (*)(void**, int, UniqueId, int);
 using FnAllReduce = ncclResult_t (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+using FnBroadcast = ncclResult_t (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 using FnCommDestroy = ncclResult_t (*)(void*);
 using FnGetErrorString = const char* (*)(ncclResult_t);
 
@@ -27,6 +28,7 @@ struct Api {
   FnGetUniqueId get_unique_id = nullptr;
   FnCommInitRank comm_init_rank = nullptr;
   FnAllReduce all_reduce = nullptr;
+  FnBroadcast broadcast = nullptr;
   FnCommDestroy comm_destroy = nullptr;
   FnGetErrorString error_string = nullptr;
   bool ok = false;
@@ -43,9 +45,10 @@ Api& api() {
     a.get_unique_id = reinterpret_cast<FnGetUniqueId>(dlsym(h, "ncclGetUniqueId"));
     a.comm_init_rank = reinterpret_cast<FnCommInitRank>(dlsym(h, "ncclCommInitRank"));
     a.all_reduce = reinterpret_cast<FnAllReduce>(dlsym(h, "ncclAllReduce"));
+    a.broadcast = reinterpret_cast<FnBroadcast>(dlsym(h, "ncclBroadcast"));
     a.comm_destroy = reinterpret_cast<FnCommDestroy>(dlsym(h, "ncclCommDestroy"));
     a.error_string = reinterpret_cast<FnGetErrorString>(dlsym(h, "ncclGetErrorString"));
-    a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy;
+    a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.broadcast && a.comm_destroy;
   });
   return a;
 }
@@ -89,6 +92,12 @@ NcclComm::~NcclComm() {
 bool NcclComm::allreduce_avg(float* buf, size_t count, cudaStream_t st, std::string* err) {
   const int rc = api().all_reduce(buf, buf, count, kNcclFloat32, kNcclAvg, comm_, st);
   if (rc != 0) return fail(err, "ncclAllReduce", rc);
+  return true;
+}
+
+bool NcclComm::broadcast(float* buf, size_t count, int root, cudaStream_t st, std::string* err) {
+  const int rc = api().broadcast(buf, buf, count, kNcclFloat32, root, comm_, st);
+  if (rc != 0) return fail(err, "ncclBroadcast", rc);
   return true;
 }
 

@@ -18,6 +18,8 @@ class NcclComm {
   int nranks() const { return nranks_; }
   // in-place average of `count` floats
   bool allreduce_avg(float* buf, size_t count, cudaStream_t st, std::string* err);
+  // in-place broadcast of `count` floats from `root`
+  bool broadcast(float* buf, size_t count, int root, cudaStream_t st, std::string* err);
 
  private:
   void* comm_ = nullptr;

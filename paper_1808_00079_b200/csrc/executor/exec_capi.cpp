@@ -326,6 +326,21 @@ int rfx_net_write_param(rfx_net* n, int32_t i, const float* host) {
   return guard([&] { n->net->write_param(i, host); });
 }
 
+int rfx_net_param_slot(const rfx_net* n, int32_t i, int64_t* offset, int64_t* count) {
+  return guard([&] {
+    *offset = n->net->param_offset(i);
+    *count = n->net->param_count(i);
+  });
+}
+
+int rfx_net_pack_param(const rfx_net* n, int32_t i, const float* canonical, float* flat_slice) {
+  return guard([&] { n->net->pack_param(i, canonical, flat_slice); });
+}
+
+int rfx_net_unpack_param(const rfx_net* n, int32_t i, const float* flat_slice, float* canonical) {
+  return guard([&] { n->net->unpack_param(i, flat_slice, canonical); });
+}
+
 int rfx_net_read_tensor(const rfx_net* n, int32_t t, float* host) {
   return guard([&] { n->net->read_tensor(t, host); });
 }

@@ -171,7 +171,12 @@ class Net {
   void stage_batch(const float* images_host, const int* labels_host, int slot, cudaStream_t copy_st);
   void use_batch(int slot, cudaStream_t st);
   void forward_backward(cudaStream_t st);  // loss + gradients (no update)
-  void update(float lr, float momentum, float wd, cudaStream_t st);  // SGD + weight prep
+  void update(float lr, float momentum, float wd, cudaStream_t st) {  // SGD + weight prep
+    set_hyper(lr, momentum, wd, st);
+    update(st);
+  }
+  void set_hyper(float lr, float momentum, float wd, cudaStream_t st);
+  void update(cudaStream_t st);  // SGD with the device-resident hyperparameters
   void step(float lr, float momentum, float wd, cudaStream_t st, bool use_graph);
   // phase: 0 forward+backward, 1 update, 2 both (each cached as its own CUDA graph)
   void run_phase(int phase, float lr, float momentum, float wd, cudaStream_t st, bool use_graph);
@@ -199,6 +204,12 @@ class Net {
   const Param& param(int i) const { return params_[i]; }
   void read_param(int i, int which, float* host) const;  // which: 0 value, 1 grad, 2 momentum
   void write_param(int i, const float* host);
+  // host-only layout conversion: canonical <-> the slice [param_offset(i),
+  // + param_count(i)) of the flat fp32 parameter / gradient buffers
+  void pack_param(int i, const float* canonical, float* flat_slice) const;
+  void unpack_param(int i, const float* flat_slice, float* canonical) const;
+  long param_offset(int i) const { return params_.at(i).offset; }
+  long param_count(int i) const { return params_.at(i).count; }
   void read_tensor(int t, float* host) const;
   void read_grad_tensor(int t, float* host) const;  // valid for every tensor with keep_grads
   void set_keep_grads(bool on) { keep_grads_ = on; }
@@ -330,7 +341,6 @@ class Net {
   void build_gather_tables();
   int prep_layers_ = 0;
   long prep_total_ = 0;
-  float phase_hyper_[3][3] = {};
 
   struct GemmRecord {
     rfk::GemmDesc desc;
@@ -338,6 +348,10 @@ class Net {
     double bytes;  // algorithmic HBM bytes: operands read once + output written (read too when accumulating)
   };
   bool tracing_ = false;
+  // a gradient bucket's all-reduce may be running on comm_stream_: persistent
+  // GEMMs leave comm_sm_reserve_ SMs to the NCCL kernels (RFK_COMM_SMS)
+  bool comm_inflight_ = false;
+  int comm_sm_reserve_ = 0;
   bool tuned_ = false;
   int im2col_holder_ = -1;  // explicit-im2col conv whose whole-batch matrix ws_im2col holds (this step)
   void autotune(cudaStream_t st);  // per GEMM shape: fastest tile width (process-wide cache)

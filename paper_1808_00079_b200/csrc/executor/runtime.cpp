@@ -179,10 +179,13 @@ void Net::setup(uint64_t seed) {
 }
 
 // Canonical (PyTorch) layout <-> GEMM layout conversions.
-void Net::write_param(int i, const float* host) {
+// Canonical (PyTorch) layout <-> the parameter's slice of the flat fp32
+// buffers (GEMM layout: conv [Cout][R][S][Cpad] or [Cout][Kpad] for explicit
+// im2col, hidden linear [out][h][w][c]); padding stays zero.  Host-only.
+void Net::pack_param(int i, const float* host, float* buf) const {
   const Param& p = params_.at(i);
   const Op& op = ops_[p.op];
-  std::vector<float> buf(p.count, 0.f);
+  std::fill(buf, buf + p.count, 0.f);
   if (p.kind == 0) {
     const int co = op.cout, ci = op.cin_real, R = op.R, S = op.S;
     for (int a = 0; a < co; ++a)
@@ -203,21 +206,13 @@ void Net::write_param(int i, const float* host) {
         for (int hw = 0; hw < HW; ++hw)
           buf[(long)o * op.cin + (long)hw * Cc + c] = host[(long)o * op.cin + (long)c * HW + hw];
   } else {
-    std::memcpy(buf.data(), host, p.count * 4);
-  }
-  check(cudaMemcpy(d_param_ + p.offset, buf.data(), p.count * 4, cudaMemcpyHostToDevice), "write_param");
-  if (setup_done_) {
-    prep_weights(0);
-    check(cudaDeviceSynchronize(), "write_param");
+    std::memcpy(buf, host, p.count * 4);
   }
 }
 
-void Net::read_param(int i, int which, float* host) const {
+void Net::unpack_param(int i, const float* buf, float* host) const {
   const Param& p = params_.at(i);
   const Op& op = ops_[p.op];
-  const float* src = which == 0 ? d_param_ : (which == 1 ? d_grad_ : d_mom_);
-  std::vector<float> buf(p.count);
-  check(cudaMemcpy(buf.data(), src + p.offset, p.count * 4, cudaMemcpyDeviceToHost), "read_param");
   if (p.kind == 0) {
     const int co = op.cout, ci = op.cin_real, R = op.R, S = op.S;
     for (int a = 0; a < co; ++a)
@@ -236,8 +231,27 @@ void Net::read_param(int i, int which, float* host) const {
         for (int hw = 0; hw < HW; ++hw)
           host[(long)o * op.cin + (long)c * HW + hw] = buf[(long)o * op.cin + (long)hw * Cc + c];
   } else {
-    std::memcpy(host, buf.data(), p.count * 4);
+    std::memcpy(host, buf, p.count * 4);
   }
+}
+
+void Net::write_param(int i, const float* host) {
+  const Param& p = params_.at(i);
+  std::vector<float> buf(p.count, 0.f);
+  pack_param(i, host, buf.data());
+  check(cudaMemcpy(d_param_ + p.offset, buf.data(), p.count * 4, cudaMemcpyHostToDevice), "write_param");
+  if (setup_done_) {
+    prep_weights(0);
+    check(cudaDeviceSynchronize(), "write_param");
+  }
+}
+
+void Net::read_param(int i, int which, float* host) const {
+  const Param& p = params_.at(i);
+  const float* src = which == 0 ? d_param_ : (which == 1 ? d_grad_ : d_mom_);
+  std::vector<float> buf(p.count);
+  check(cudaMemcpy(buf.data(), src + p.offset, p.count * 4, cudaMemcpyDeviceToHost), "read_param");
+  unpack_param(i, buf.data(), host);
 }
 
 void Net::read_tensor(int t, float* host) const {
@@ -312,6 +326,19 @@ static double gemm_algorithmic_bytes(const rfk::GemmDesc& d) {
   }
   const double c = (d.out_f32 ? 4.0 : 2.0) * d.M * d.N * (d.accumulate_out ? 2 : 1);
   return a + b + c;
+}
+
+// Algorithmic flops of one GEMM launch: 2 M N K from its own descriptor (an
+// im2col operand's K is its taps x channels), capped by the layer's
+// algorithmic flops set by the op (trace_flops_) -- the cap removes padded
+// channels (stem K = 7*7*3 padded to 64-multiples) and the zeros of a
+// zero-insertion dgrad, while a layer split over several launches (sub-pixel
+// dgrad classes, image chunks) counts each launch's own share once.
+static double gemm_launch_flops(const rfk::GemmDesc& d, double layer_flops) {
+  double k = d.K;
+  if (d.a_kind == rfk::Operand::Im2colK) k = (double)d.a_geom.R * d.a_geom.S * d.a_geom.C;
+  const double f = 2.0 * d.M * d.N * k;
+  return layer_flops > 0 ? std::min(f, layer_flops) : f;
 }
 
 // Conv backward runs the weight-gradient GEMM on a side stream concurrently
@@ -399,6 +426,10 @@ void Net::autotune(cudaStream_t st) {
       if (bn > 64 && r.desc.N <= bn / 2) continue;
       rfk::GemmDesc dc = r.desc;
       dc.block_n = bn;
+      // the probe must not leave partial sums in the conv's BN statistics
+      // slot: each width maps tiles to different CTA rows, and the finalize
+      // sums every row (rows a CTA never touches are assumed zero)
+      dc.stats = nullptr;
       cudaGraphExec_t g = capture(
           [&](cudaStream_t s) {
             for (int i = 0; i < 3; ++i) check(rfk::gemm_launch(dc, s), "gemm");
@@ -420,21 +451,47 @@ void Net::autotune(cudaStream_t st) {
   cudaEventDestroy(e1);
   gemm_trace_.clear();  // re-traced with the tuned widths when needed
   check(cudaStreamSynchronize(st), "autotune");
+  // the probes wrote real output buffers (some accumulating): restore the
+  // zeroed state setup() left, so a tuned net starts exactly like an untuned one
+  check(cudaMemset(d_ws_, 0, rep_.workspace_bytes > 0 ? rep_.workspace_bytes : 256), "memset");
+  check(cudaMemset(d_grad_, 0, n_params_ * 4), "memset");
+  check(cudaMemset(d_arena_, 0, arena_bytes_ > 0 ? arena_bytes_ : 256), "memset");
+  check(cudaDeviceSynchronize(), "autotune");
 }
 
-void Net::gemm(const rfk::GemmDesc& d, cudaStream_t st) {
+static int num_sms() {
+  static const int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+void Net::gemm(const rfk::GemmDesc& d0, cudaStream_t st) {
+  rfk::GemmDesc dcap;
+  const rfk::GemmDesc* dp = &d0;
+  if (comm_inflight_ && comm_sm_reserve_ > 0 && !d0.stats) {
+    // statistics GEMMs (first forward only) keep the full grid: their
+    // per-CTA statistics rows must not depend on whether a bucket is in flight
+    dcap = d0;
+    dcap.max_ctas = std::max(1, num_sms() - comm_sm_reserve_);
+    dp = &dcap;
+  }
+  const rfk::GemmDesc& d = *dp;
   if (d.block_n == 0 && tuned_) {
     std::lock_guard<std::mutex> lock(g_tune_mu);
     const auto it = g_tune.find(tune_key(d));
     if (it != g_tune.end()) {
       rfk::GemmDesc dt = d;
       dt.block_n = it->second;
-      if (tracing_) gemm_trace_.push_back({dt, trace_flops_, gemm_algorithmic_bytes(dt)});
+      if (tracing_) gemm_trace_.push_back({dt, gemm_launch_flops(dt, trace_flops_), gemm_algorithmic_bytes(dt)});
       check(rfk::gemm_launch(dt, st), "gemm");
       return;
     }
   }
-  if (tracing_) gemm_trace_.push_back({d, trace_flops_, gemm_algorithmic_bytes(d)});
+  if (tracing_) gemm_trace_.push_back({d, gemm_launch_flops(d, trace_flops_), gemm_algorithmic_bytes(d)});
   check(rfk::gemm_launch(d, st), "gemm");
 }
 
@@ -492,6 +549,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
           if (dc.bn_out) dc.bn_out = static_cast<__nv_bfloat16*>(dc.bn_out) + n0 * img_rows * op.cout;
           dc.stats = stats;
           dc.stats_acc = n0 > 0;
+          trace_flops_ = 2.0 * dc.M * op.cout * op.R * op.S * op.cin_real;  // this chunk's share
           gemm(dc, st);
         }
         break;
@@ -870,7 +928,10 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           dc.K = (int)(nn * img_rows);
           dc.a = dy + n0 * img_rows * op.cout;
           dc.out = ws_split + (long)parts * op.cout * kw;
+          const double layer = trace_flops_;
+          trace_flops_ = 2.0 * dc.K * op.cout * op.R * op.S * op.cin_real;  // this chunk's share
           gemm(dc, wst);
+          trace_flops_ = layer;
           parts += op.wg_splits;
         }
         check(rfk::reduce_splits(ws_split, parts, (long)op.cout * kw, dW, false, wst), "reduce_splits");
@@ -1189,6 +1250,18 @@ void Net::set_comm(int nranks, int rank, const char id[128], long bucket_bytes) 
   if (!comm_done_) check(cudaEventCreateWithFlags(&comm_done_, cudaEventDisableTiming), "event");
   bucket_floats_ = std::max(1L, bucket_bytes / 4);
   plan_buckets();
+  {
+    const char* e = std::getenv("RFK_COMM_SMS");
+    comm_sm_reserve_ = e ? std::max(0, std::atoi(e)) : (nranks > 1 ? 16 : 0);
+  }
+  // every replica starts from rank 0's parameters and BN state (data-parallel
+  // SGD: same model, averaged gradients), then refreshes its bf16 GEMM copies
+  if (!comm_->broadcast(d_param_, (size_t)n_params_, 0, comm_stream_, &err) ||
+      !comm_->broadcast(d_state_, (size_t)n_state_, 0, comm_stream_, &err))
+    throw std::runtime_error(err);
+  check(cudaMemsetAsync(d_mom_, 0, n_params_ * 4, comm_stream_), "memset");
+  prep_weights(comm_stream_);
+  check(cudaStreamSynchronize(comm_stream_), "parameter broadcast");
   for (auto& p : phase_exec_)
     if (p) {
       cudaGraphExecDestroy(p);
@@ -1298,11 +1371,19 @@ void Net::forward_backward(cudaStream_t st) {
     }
     run_instr(sched_[k], st);
     while (dp && b < buckets_.size() && buckets_[b].after_instr == k) {
-      join_wgrad(st);  // the bucket's weight gradients must be complete
+      // the bucket's weight gradients must be complete: the comm stream (not
+      // this one) waits for the pending side-stream weight-gradient GEMMs, so
+      // the backward keeps going; the wgrad read sets stay pending for the
+      // main stream's own lazy join
+      if (wgrad_pending_) {
+        check(cudaEventRecord(wgrad_join_, wgrad_stream_), "event");
+        check(cudaStreamWaitEvent(comm_stream_, wgrad_join_, 0), "wait");
+      }
       // fork: the side stream waits for the gradients, then reduces them
       // while this stream carries on with the backward
       check(cudaEventRecord(bucket_events_[b], st), "event");
       check(cudaStreamWaitEvent(comm_stream_, bucket_events_[b], 0), "wait");
+      comm_inflight_ = true;
       std::string err;
       if (!comm_->allreduce_avg(d_grad_ + buckets_[b].lo, (size_t)(buckets_[b].hi - buckets_[b].lo), comm_stream_,
                                 &err))
@@ -1311,6 +1392,7 @@ void Net::forward_backward(cudaStream_t st) {
     }
   }
   join_wgrad(st);
+  comm_inflight_ = false;
   if (trace) std::fprintf(stderr, "wgrad joins: %d on activation ranges, %d on gradient ranges\n", joins_act, joins_grad);
   if (dp) {  // join
     check(cudaEventRecord(comm_done_, comm_stream_), "event");
@@ -1318,9 +1400,18 @@ void Net::forward_backward(cudaStream_t st) {
   }
 }
 
-void Net::update(float lr, float momentum, float wd, cudaStream_t st) {
+// SGD hyperparameters live in device memory (d_hyper_ = {lr, momentum, wd}),
+// written in stream order before each step, so one captured step graph
+// serves any learning-rate schedule.  The source is pageable: cudaMemcpyAsync
+// stages it before returning, so the stack buffer may go away.
+void Net::set_hyper(float lr, float momentum, float wd, cudaStream_t st) {
+  const float h[3] = {lr, momentum, wd};
+  check(cudaMemcpyAsync(d_hyper_, h, sizeof h, cudaMemcpyHostToDevice, st), "hyper h2d");
+}
+
+void Net::update(cudaStream_t st) {
   // one pass: momentum SGD on the fp32 masters + refresh of their bf16 copy
-  check(rfk::sgd_update(d_param_, d_grad_, d_mom_, n_params_, lr, momentum, wd, d_bf16_, st), "sgd");
+  check(rfk::sgd_update(d_param_, d_grad_, d_mom_, n_params_, d_hyper_, d_bf16_, st), "sgd");
 }
 
 cudaGraphExec_t Net::capture(const std::function<void(cudaStream_t)>& body, long* kernel_nodes) {
@@ -1359,22 +1450,17 @@ cudaGraphExec_t Net::capture(const std::function<void(cudaStream_t)>& body, long
 void Net::run_phase(int phase, float lr, float momentum, float wd, cudaStream_t st, bool use_graph) {
   auto body = [&](cudaStream_t s) {
     if (phase == 0 || phase == 2) forward_backward(s);
-    if (phase == 1 || phase == 2) update(lr, momentum, wd, s);
+    if (phase == 1 || phase == 2) update(s);
   };
+  if (phase == 1 || phase == 2) set_hyper(lr, momentum, wd, st);
   if (!use_graph) {
     body(st);
     return;
   }
-  float* hp = phase_hyper_[phase];
-  if (!phase_exec_[phase] || hp[0] != lr || hp[1] != momentum || hp[2] != wd) {
-    if (phase_exec_[phase]) cudaGraphExecDestroy(phase_exec_[phase]);
-    phase_exec_[phase] = nullptr;
+  if (!phase_exec_[phase]) {
     long k = 0;
     phase_exec_[phase] = capture(body, &k);
     if (phase == 2) rep_.launches_per_step = k;
-    hp[0] = lr;
-    hp[1] = momentum;
-    hp[2] = wd;
   }
   check(cudaGraphLaunch(phase_exec_[phase], st), "graph launch");
 }
@@ -1521,11 +1607,12 @@ std::vector<double> Net::instr_profile(int iters, cudaStream_t st) {
           join_wgrad(s);  // per-instruction attribution: no cross-instruction overlap
           check(cudaEventRecordWithFlags(ev[k + 1], s, cudaEventRecordExternal), "event");
         }
-        update(0.f, 0.f, 0.f, s);  // lr 0: parameters unchanged
+        update(s);  // hyperparameters zeroed below: parameters unchanged
         check(cudaEventRecordWithFlags(ev[n + 1], s, cudaEventRecordExternal), "event");
       },
       nullptr);
   std::vector<double> ms(n + 1, 0.0);
+  set_hyper(0.f, 0.f, 0.f, st);  // lr 0
   for (int it = 0; it < iters + 1; ++it) {
     check(cudaGraphLaunch(g, st), "graph");
     check(cudaStreamSynchronize(st), "sync");

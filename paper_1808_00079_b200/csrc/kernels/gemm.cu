@@ -590,7 +590,7 @@ bool encode_im2col(CUtensorMap* m, const void* ptr, const ConvGeom& g, uint32_t 
 }
 
 template <int BN>
-cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, cudaStream_t st) {
+cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max_ctas, cudaStream_t st) {
   using C = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
@@ -607,7 +607,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, cudaStr
     if (sms <= 0) sms = 148;
   }
   const long total = (long)m_tiles * n_tiles * splits;
-  const int grid = (int)std::min<long>(total, sms);
+  const int grid = (int)std::min<long>(total, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
   kp.m_tiles = m_tiles;
   kp.n_tiles = n_tiles;
   kp.splits = splits;
@@ -809,9 +809,9 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   const int m_tiles = gemm_m_tiles(d);
   const int n_tiles = (d.N + bn - 1) / bn;
   switch (bn) {
-    case 64: return launch_bn<64>(kp, m_tiles, n_tiles, splits, stream);
-    case 128: return launch_bn<128>(kp, m_tiles, n_tiles, splits, stream);
-    default: return launch_bn<256>(kp, m_tiles, n_tiles, splits, stream);
+    case 64: return launch_bn<64>(kp, m_tiles, n_tiles, splits, d.max_ctas, stream);
+    case 128: return launch_bn<128>(kp, m_tiles, n_tiles, splits, d.max_ctas, stream);
+    default: return launch_bn<256>(kp, m_tiles, n_tiles, splits, d.max_ctas, stream);
   }
 }
 

@@ -70,6 +70,9 @@ struct GemmDesc {
   const float* bn_scale = nullptr;
   const float* bn_shift = nullptr;
   bool bn_relu = false;
+  // persistent grid cap (0 = one CTA per SM): leaves SMs free for NCCL kernels
+  // on a side stream while gradient buckets are in flight
+  int max_ctas = 0;
 };
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream);

@@ -1166,9 +1166,13 @@ __global__ void __launch_bounds__(kThreads) reduce_splits_kernel(const float* __
 // wb is given it also refreshes the bf16 GEMM copy of the weights in the same
 // pass (n % 4 == 0, 16-byte aligned buffers).
 __global__ void __launch_bounds__(kThreads) sgd_kernel(float* __restrict__ w, const float* __restrict__ g,
-                                                      float* __restrict__ m, long n4, float lr, float momentum,
-                                                      float wd, __nv_bfloat16* __restrict__ wb) {
+                                                      float* __restrict__ m, long n4,
+                                                      const float* __restrict__ hyper,
+                                                      __nv_bfloat16* __restrict__ wb) {
   pdl_enter();
+  // lr, momentum, weight decay from device memory: a captured step graph
+  // stays valid under a learning-rate schedule
+  const float lr = __ldg(hyper), momentum = __ldg(hyper + 1), wd = __ldg(hyper + 2);
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) {
     float4 wv = reinterpret_cast<float4*>(w)[i];
     const float4 gv = __ldg(reinterpret_cast<const float4*>(g) + i);
@@ -1760,10 +1764,10 @@ cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bo
   return cudaGetLastError();
 }
 
-cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, float momentum, float wd,
-                       __nv_bfloat16* wb, cudaStream_t st) {
+cudaError_t sgd_update(float* w, const float* g, float* m, long n, const float* hyper, __nv_bfloat16* wb,
+                       cudaStream_t st) {
   if (n % 4) return cudaErrorInvalidValue;
-  RFK_CHECK_LAUNCH(launch_k(sgd_kernel, grid_for(n / 4, kThreads * 2), kThreads, 0, st, w, g, m, n / 4, lr, momentum, wd, wb));
+  RFK_CHECK_LAUNCH(launch_k(sgd_kernel, grid_for(n / 4, kThreads * 2), kThreads, 0, st, w, g, m, n / 4, hyper, wb));
   return cudaGetLastError();
 }
 

@@ -64,9 +64,10 @@ cudaError_t colsum_f32(const float* x, int R, int C, float* out, bool acc, cudaS
 cudaError_t reduce_splits_bf16(const float* parts, int splits, int M, int N, __nv_bfloat16* out, long ldc, bool acc,
                                float* stats, int max_blocks, cudaStream_t st);
 cudaError_t reduce_splits(const float* parts, int splits, long n, float* out, bool acc, cudaStream_t st);
-// wb (optional): bf16 copy of w refreshed in the same pass
-cudaError_t sgd_update(float* w, const float* g, float* m, long n, float lr, float momentum, float wd,
-                       __nv_bfloat16* wb, cudaStream_t st);
+// hyper: device {lr, momentum, weight decay}; wb (optional): bf16 copy of w
+// refreshed in the same pass
+cudaError_t sgd_update(float* w, const float* g, float* m, long n, const float* hyper, __nv_bfloat16* wb,
+                       cudaStream_t st);
 cudaError_t conv_weight_prep(const float* w, int Cout, int R, int S, int Cpad, int Cin, int CoutPad,
                              __nv_bfloat16* wb, __nv_bfloat16* wt, cudaStream_t st);
 // One launch for every conv / fc layer after an SGD step: bf16 copy of the

@@ -93,6 +93,9 @@ _SIGS = {
     "rfx_net_param_info": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, C.POINTER(C.c_int32),
                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
     "rfx_net_read_param": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "rfx_net_param_slot": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "rfx_net_pack_param": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "rfx_net_unpack_param": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "rfx_net_write_param": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "rfx_net_read_tensor": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "rfx_net_read_bn_running": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
@@ -478,6 +481,28 @@ class ReforwardNet:
         p = self.params()[i]
         assert a.size == p.count, (p.name, a.shape, p.shape)
         _check(self.L.rfx_net_write_param(self.h, i, a.ctypes.data_as(C.c_void_p)))
+
+    def param_slot(self, i: int) -> Tuple[int, int]:
+        """(offset, count) of parameter i in the flat fp32 parameter / gradient buffers."""
+        off, cnt = C.c_int64(), C.c_int64()
+        _check(self.L.rfx_net_param_slot(self.h, i, C.byref(off), C.byref(cnt)))
+        return off.value, cnt.value
+
+    def pack_param(self, i: int, value):
+        """Host-only: canonical tensor -> its flat-buffer slice (GEMM layout, zero padding)."""
+        import numpy as np
+        a = np.ascontiguousarray(value, dtype=np.float32)
+        out = np.empty(self.param_slot(i)[1], dtype=np.float32)
+        _check(self.L.rfx_net_pack_param(self.h, i, a.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def unpack_param(self, i: int, flat_slice):
+        """Host-only: flat-buffer slice -> canonical tensor."""
+        import numpy as np
+        f = np.ascontiguousarray(flat_slice, dtype=np.float32)
+        out = np.empty(self.params()[i].shape, dtype=np.float32)
+        _check(self.L.rfx_net_unpack_param(self.h, i, f.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def read_tensor(self, t: int):
         import numpy as np

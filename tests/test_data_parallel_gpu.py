@@ -16,8 +16,14 @@ from paper_1808_00079_b200.executor import ReforwardNet
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("arch,hw,bucket_mb", [("resnet18", 32, 1), ("resnet50", 64, 4), ("densenet_tiny", 32, 1)])
-def test_single_rank_nccl_step_matches_local_step(arch, hw, bucket_mb):
+@pytest.mark.parametrize("arch,hw,bucket_mb,comm_sms", [("resnet18", 32, 1, None), ("resnet50", 64, 4, None),
+                                                       ("densenet_tiny", 32, 1, None), ("resnet50", 64, 4, "40")])
+def test_single_rank_nccl_step_matches_local_step(monkeypatch, arch, hw, bucket_mb, comm_sms):
+    """comm_sms: persistent GEMMs issued while a bucket is in flight leave that
+    many SMs to NCCL (RFK_COMM_SMS; default 16 when world > 1) -- a different
+    tile -> CTA mapping with the same per-tile K order, so still bit-identical."""
+    if comm_sms is not None:
+        monkeypatch.setenv("RFK_COMM_SMS", comm_sms)
     nets = []
     for with_comm in (False, True):
         net = ReforwardNet.named(arch, 4, hw, hw, 10)
@@ -34,6 +40,27 @@ def test_single_rank_nccl_step_matches_local_step(arch, hw, bucket_mb):
         torch.cuda.synchronize()
         nets.append((net, losses))
     (a, la), (b, lb) = nets
+    assert la == lb
+    for p in a.params():
+        assert np.array_equal(a.read_param(p.index, 0), b.read_param(p.index, 0)), p.name
+
+
+def test_lr_schedule_reuses_the_captured_step_graph():
+    """SGD hyperparameters are read from device memory: a graph step under a
+    changing learning rate equals the eager step, with one capture."""
+    runs = []
+    for use_graph in (False, True):
+        net = ReforwardNet.named("resnet18", 4, 32, 32, 10)
+        net.plan("reforward")
+        net.setup(seed=2)
+        x, y = random_batch(net, seed=3)
+        net.load_batch(x, y)
+        losses = []
+        for k in range(4):
+            net.step(lr=0.1 / (k + 1), momentum=0.9, weight_decay=1e-4 * k, use_graph=use_graph)
+            losses.append(net.read_loss())
+        runs.append((net, losses))
+    (a, la), (b, lb) = runs
     assert la == lb
     for p in a.params():
         assert np.array_equal(a.read_param(p.index, 0), b.read_param(p.index, 0)), p.name

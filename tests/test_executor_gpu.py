@@ -1,17 +1,18 @@
 """Re-forward training on sm_100a vs the CPU re-forward step (oracle/train_oracle.py).
 
-Levels, as BASELINE.json's north star asks:
-* the loss matches the CPU step (bf16-storage-emulating mode) within
-    |loss_gpu - loss_cpu| <= 2e-2 * |loss_cpu| + 2e-2
-  and, on the conv/ReLU chain (configs[0]), every parameter gradient within
-    ||g_gpu - g_cpu|| / ||g_cpu|| <= 5e-2;
-  for the BN ResNets (whose gradients at these tiny sizes move by tens of
-  percent under bf16 storage even on the CPU) the whole-gradient cosine
-  similarity must be >= 0.9 — per-kernel exactness is pinned separately by
-  tests/test_ops_teacher_forced_gpu.py;
+Levels, as BASELINE.json's north star asks (tolerances stated in DESIGN.md
+"Parity"):
+* whole step against the CPU step that stores bf16 at the same points
+  (emulate_bf16): loss within 1e-3 relative, and every parameter gradient
+  within  ||g_gpu - g_cpu|| / ||g_cpu|| <= max(2e-2, 3 x floor), where floor is
+  that parameter's distance between the CPU step with fp32 and with fp64
+  accumulation -- the configuration's own bf16 rounding-flip noise (the GPU's
+  fp32 accumulation order is an independent draw of it).  Plain random init:
+  no scaled residual gammas, no scaled classifier;
 * on the GPU, re-forward gradients are bit-identical to store-all gradients
   (deterministic kernels; same arithmetic whether a tensor was stored or
   recomputed).
+The BASELINE shapes run the same checks in tests/test_baseline_shapes_gpu.py.
 """
 import numpy as np
 import pytest
@@ -19,22 +20,17 @@ import torch
 
 from oracle.train_oracle import OracleNet, random_batch, rel_err
 from paper_1808_00079_b200.executor import ReforwardNet
+from _parity import plan
 
 pytestmark = pytest.mark.gpu
 
-LOSS_RTOL, LOSS_ATOL, GRAD_RTOL, COS_MIN = 2e-2, 2e-2, 5e-2, 0.9
-
 CASES = [("chain8", 4, 32, 10), ("resnet18", 4, 64, 10), ("resnet50", 2, 64, 16), ("densenet_tiny", 4, 32, 10),
-         ("vgg11", 4, 32, 10), ("alexnet", 4, 64, 10)]
-# no batch norm: per-parameter relative error, bounded by max(tolerance,
-# 1.5 x the configuration's own noise floor measured in the test) and a
-# cosine floor.
-EXACT_GRADS = {"chain8": GRAD_RTOL, "vgg11": 0.1, "alexnet": 0.1}
+         ("vgg11", 4, 32, 10), ("alexnet", 4, 64, 10), ("inception_v3", 2, 139, 10)]
 
 
-def _run(arch, batch, hw, classes, policy, oracle_weights, x, y):
+def _run(arch, batch, hw, classes, policy, oracle_weights, x, y, stored=None):
     net = ReforwardNet.named(arch, batch, hw, hw, classes)
-    rep = net.plan(policy)
+    rep = net.plan_with_stored(stored, "test") if stored is not None else net.plan(policy)
     net.setup(seed=0)
     oracle_weights.push_weights_to(net)
     net.load_batch(x, y)
@@ -48,43 +44,29 @@ def _run(arch, batch, hw, classes, policy, oracle_weights, x, y):
 @pytest.mark.parametrize("arch,batch,hw,classes", CASES)
 def test_parity_with_cpu_oracle_and_bit_identity(arch, batch, hw, classes):
     probe = ReforwardNet.named(arch, batch, hw, hw, classes)
-    probe.plan("reforward")
+    plan(probe, arch, batch, hw)  # memoised in plans/ (Inception-v3 takes minutes)
     o = OracleNet(probe, emulate_bf16=True)
-    o.init_weights(seed=11, residual_gamma=0.1)
-    if arch in ("vgg11", "alexnet"):
-        # keep the random classifier out of softmax saturation: saturated
-        # logits make these unnormalised stacks amplify bf16 storage noise
-        last = [op for op in probe.ops() if op.kind == "fc"][-1].name + ".weight"
-        o.weights[last] = o.weights[last] * 0.1
+    o.init_weights(seed=11)
     x, y = random_batch(probe, seed=5)
     stored, seg = probe.plan_sets()
     ref_loss, ref_grads, ref_peak = o.run_step(x, y, probe.schedule(), stored, seg)
+    o64 = OracleNet(probe, dtype=torch.float64, emulate_bf16=True)
+    o64.weights = {k: v.double() for k, v in o.weights.items()}
+    _, g64, _ = o64.run_step(x, y, probe.schedule(), stored, seg)
 
-    _, rep_r, loss_r, g_r = _run(arch, batch, hw, classes, "reforward", o, x, y)
+    _, rep_r, loss_r, g_r = _run(arch, batch, hw, classes, "reforward", o, x, y, stored=stored)
     _, rep_s, loss_s, g_s = _run(arch, batch, hw, classes, "store_all", o, x, y)
 
     assert rep_r.tracked_peak == rep_r.planned_total == ref_peak
     assert rep_r.planned_total < rep_s.planned_total
-    assert abs(loss_r - ref_loss) <= LOSS_RTOL * abs(ref_loss) + LOSS_ATOL, (loss_r, ref_loss)
-    if arch in EXACT_GRADS:
-        worst = max(rel_err(g_r[n], ref_grads[n].numpy()) for n in ref_grads)
-        # noise floor of the configuration itself: the same bf16-storage step
-        # with fp64 instead of fp32 accumulation (VGG-11 at 32x32 / batch 4
-        # moves ~11 % on its own -- bf16 rounding flips amplified through the
-        # unnormalised stack)
-        o64 = OracleNet(probe, dtype=torch.float64, emulate_bf16=True)
-        o64.weights = {k: v.double() for k, v in o.weights.items()}
-        _, g64, _ = o64.run_step(x, y, probe.schedule(), stored, seg)
-        floor = max(rel_err(ref_grads[n].double().numpy(), g64[n].numpy()) for n in ref_grads)
-        assert worst <= max(EXACT_GRADS[arch], 1.5 * floor), (worst, floor)
-        a = np.concatenate([g_r[n].ravel() for n in ref_grads]).astype(np.float64)
-        b = np.concatenate([ref_grads[n].numpy().ravel() for n in ref_grads]).astype(np.float64)
-        assert float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b))) >= 0.99
-    else:
-        a = np.concatenate([g_r[n].ravel() for n in ref_grads]).astype(np.float64)
-        b = np.concatenate([ref_grads[n].numpy().ravel() for n in ref_grads]).astype(np.float64)
-        cos = float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
-        assert cos >= COS_MIN, cos
+    assert abs(loss_r - ref_loss) <= 1e-3 * abs(ref_loss), (loss_r, ref_loss)
+    bad = []
+    for n in ref_grads:
+        err = rel_err(g_r[n], ref_grads[n].numpy())
+        floor = rel_err(ref_grads[n].double().numpy(), g64[n].numpy())
+        if err > max(2e-2, 3 * floor):
+            bad.append((n, err, floor))
+    assert not bad, bad[:10]
     # bit identity re-forward vs store-all
     assert loss_r == loss_s
     for n in g_r:

@@ -533,11 +533,23 @@ void Net::build_schedule() {
       }
     return s;
   };
+  // A tensor read by several ops receives one gradient contribution from each
+  // consumer's backward, accumulated in place in bf16 -- which is not
+  // associative.  So consumers run their backward in a fixed order (highest
+  // op id first) whatever the plan: re-forward and store-all form every
+  // gradient sum in the same order and stay bit-identical.  The highest-id
+  // remaining op is always eligible, so this cannot deadlock.
+  auto order_ok = [&](int o) {
+    for (int i : ops_[o].in)
+      for (int c : tensors_[i].consumers)
+        if (c > o && !done[c]) return false;
+    return true;
+  };
   long bwd = 0;
   while (remaining > 0) {
     int pick = -1, pick_any = -1;
     for (int o = no - 1; o >= 0; --o) {
-      if (done[o] || ops_[o].kind == OpKind::Input || pending[ops_[o].out] != 0) continue;
+      if (done[o] || ops_[o].kind == OpKind::Input || pending[ops_[o].out] != 0 || !order_ok(o)) continue;
       if (pick_any < 0) pick_any = o;
       const int s = seg_needed(o);
       if (s < 0 || s == live_seg) {

@@ -79,16 +79,21 @@ def test_reforward_bit_identical_to_store_all_at_baseline_shape(arch, batch, hw)
         assert np.array_equal(vr[n], vs[n]), n
 
 
-WHOLE = [("resnet50", 32, 224, 1000), ("alexnet", 32, 224, 1000), ("vgg16", 8, 224, 1000),
-         ("densenet121", 4, 224, 1000), ("inception_v3", 4, 299, 1000)]
+# (arch, batch, hw, classes, residual BN gamma init): 1.0 = plain init; 0.0 =
+# the zero-init of each residual block's last BN gamma of the standard
+# large-batch ResNet recipe (Goyal et al. 2017), under which a deep ResNet
+# starts well conditioned -- its floor is ~1 % instead of ~100 %, so the bar
+# is tight there
+WHOLE = [("resnet50", 32, 224, 1000, 0.0), ("resnet50", 32, 224, 1000, 1.0), ("alexnet", 32, 224, 1000, 1.0),
+         ("vgg16", 8, 224, 1000, 1.0), ("densenet121", 4, 224, 1000, 1.0), ("inception_v3", 4, 299, 1000, 1.0)]
 
 
 def _cat(g, names):
     return np.concatenate([np.asarray(g[n], dtype=np.float64).ravel() for n in names])
 
 
-@pytest.mark.parametrize("arch,batch,hw,classes", WHOLE)
-def test_whole_step_within_stated_tolerance(arch, batch, hw, classes):
+@pytest.mark.parametrize("arch,batch,hw,classes,gamma", WHOLE)
+def test_whole_step_within_stated_tolerance(arch, batch, hw, classes, gamma):
     from paper_1808_00079_b200.executor import ReforwardNet
     probe = ReforwardNet.named(arch, batch, hw, hw, classes)
     plan(probe, arch, batch, hw)
@@ -96,7 +101,7 @@ def test_whole_step_within_stated_tolerance(arch, batch, hw, classes):
     sched = probe.schedule()
     x, y = random_batch(probe, seed=5)
     o16 = OracleNet(probe, emulate_bf16=True)
-    o16.init_weights(seed=11)
+    o16.init_weights(seed=11, residual_gamma=gamma)
     with Timer() as t:
         l16, g16, peak = o16.run_step(x, y, sched, stored, seg)
         o64 = OracleNet(probe, dtype=torch.float64, emulate_bf16=True)
@@ -117,13 +122,14 @@ def test_whole_step_within_stated_tolerance(arch, batch, hw, classes):
     floor_p = {n: rel_err(g16[n].numpy(), g64[n].numpy()) for n in names}
     ratio = {n: per_param[n] / max(2e-2, 3 * floor_p[n]) for n in names}
     worst_p = max(ratio, key=ratio.get)
-    rep_ = {"loss_gpu": losses[0], "loss_cpu_bf16": l16, "loss_cpu_fp64": l64, "loss_cpu_fp32": l32,
-            "grad_err_vs_cpu_bf16": err16, "noise_floor_fp64": floor, "grad_err_vs_cpu_fp32": err32,
-            "cpu_bf16_vs_fp32": bf16_cost, "worst_param": [worst_p, per_param[worst_p], floor_p[worst_p]],
-            "cpu_seconds": t.s}
-    report(f"wholestep_{arch}_b{batch}_{hw}", rep_)
-    assert abs(losses[0] - l16) <= 1e-3 * abs(l16), rep_
-    assert abs(losses[0] - l32) <= 1.5 * abs(l16 - l32) + 1e-3 * abs(l32), rep_
+    loss_floor = abs(l16 - l64)
+    rep_ = {"residual_gamma": gamma, "loss_gpu": losses[0], "loss_cpu_bf16": l16, "loss_cpu_fp64": l64,
+            "loss_cpu_fp32": l32, "grad_err_vs_cpu_bf16": err16, "noise_floor_fp64": floor,
+            "grad_err_vs_cpu_fp32": err32, "cpu_bf16_vs_fp32": bf16_cost,
+            "worst_param": [worst_p, per_param[worst_p], floor_p[worst_p]], "cpu_seconds": t.s}
+    report(f"wholestep_{arch}_b{batch}_{hw}_g{gamma:g}", rep_)
+    assert abs(losses[0] - l16) <= max(1e-3 * abs(l16), 3 * loss_floor), rep_
+    assert abs(losses[0] - l32) <= 1.5 * abs(l16 - l32) + max(1e-3 * abs(l32), 3 * loss_floor), rep_
     assert err16 <= max(2e-2, 3 * floor), rep_
     assert ratio[worst_p] <= 1.0, rep_
     assert err32 <= 1.5 * bf16_cost + 1e-3, rep_
@@ -131,32 +137,47 @@ def test_whole_step_within_stated_tolerance(arch, batch, hw, classes):
 
 def test_multi_step_loss_trajectory_resnet50():
     """Three momentum-SGD steps through the captured graph against the CPU
-    step + the same SGD update on the host (fp32 masters, bf16 copies)."""
+    step + the same SGD update on the host (fp32 masters, bf16 copies), with
+    the trajectory's own floor (the same CPU run with fp64 accumulation)."""
     from paper_1808_00079_b200.executor import ReforwardNet
     arch, batch, hw, classes = "resnet50", 8, 224, 1000
     probe = ReforwardNet.named(arch, batch, hw, hw, classes)
-    probe.plan("reforward")
+    plan(probe, arch, batch, hw)
     stored, seg = probe.plan_sets()
     sched = probe.schedule()
     x, y = random_batch(probe, seed=9)
     o = OracleNet(probe, emulate_bf16=True)
-    o.init_weights(seed=12)
+    o.init_weights(seed=12, residual_gamma=0.0)
     w0 = {k: v.clone() for k, v in o.weights.items()}
     lr, mom, wd, steps = 0.05, 0.9, 1e-4, 3
-    cpu_losses = []
-    buf = {k: torch.zeros_like(v) for k, v in o.weights.items()}
-    for _ in range(steps):
-        loss, g, _ = o.run_step(x, y, sched, stored, seg)
-        cpu_losses.append(loss)
-        for k in o.weights:
-            d = g[k] + wd * o.weights[k]
-            buf[k] = mom * buf[k] + d
-            o.weights[k] = o.weights[k] - lr * buf[k]
+
+    def cpu_run(dtype):
+        oc = OracleNet(probe, dtype=dtype, emulate_bf16=True)
+        oc.weights = {k: v.to(dtype) for k, v in w0.items()}
+        buf = {k: torch.zeros_like(v) for k, v in oc.weights.items()}
+        losses = []
+        for _ in range(steps):
+            loss, g, _ = oc.run_step(x, y, sched, stored, seg)
+            losses.append(loss)
+            for k in oc.weights:
+                d = g[k] + wd * oc.weights[k]
+                buf[k] = mom * buf[k] + d
+                oc.weights[k] = oc.weights[k] - lr * buf[k]
+        return losses, {k: v.double().numpy() for k, v in oc.weights.items()}
+
+    cpu_losses, cpu_w = cpu_run(torch.float32)
+    cpu64_losses, cpu64_w = cpu_run(torch.float64)
     _, _, gpu_losses, _, vals = gpu_step(arch, batch, hw, classes, "reforward", w0, x, y, steps=steps, lr=lr,
                                          momentum=mom, wd=wd, use_graph=True)
-    werr = rel_err(_cat(vals, sorted(vals)), _cat({k: v.numpy() for k, v in o.weights.items()}, sorted(vals)))
-    report("trajectory_resnet50_b8_224", {"gpu": gpu_losses, "cpu": cpu_losses, "weight_err": werr})
-    for a, b in zip(gpu_losses, cpu_losses):
-        assert abs(a - b) <= 2e-3 * abs(b), (gpu_losses, cpu_losses)
+    names = sorted(vals)
+    # distance travelled from w0, GPU vs CPU, relative to the CPU's own floor
+    d_gpu = _cat(vals, names) - _cat({k: v.numpy() for k, v in w0.items()}, names)
+    d_cpu = _cat(cpu_w, names) - _cat({k: v.numpy() for k, v in w0.items()}, names)
+    d_64 = _cat(cpu64_w, names) - _cat({k: v.numpy() for k, v in w0.items()}, names)
+    werr, wfloor = rel_err(d_gpu, d_cpu), rel_err(d_cpu, d_64)
+    report("trajectory_resnet50_b8_224", {"gpu": gpu_losses, "cpu": cpu_losses, "cpu_fp64": cpu64_losses,
+                                          "update_err": werr, "update_floor": wfloor})
+    for a, b, c in zip(gpu_losses, cpu_losses, cpu64_losses):
+        assert abs(a - b) <= max(2e-3 * abs(b), 3 * abs(b - c)), (gpu_losses, cpu_losses, cpu64_losses)
     assert gpu_losses[-1] < gpu_losses[0]
-    assert werr <= 1e-3, werr
+    assert werr <= max(2e-2, 3 * wfloor), (werr, wfloor)

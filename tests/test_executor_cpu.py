@@ -178,3 +178,28 @@ def test_densenet121_plan_cut_and_exact_high_water():
     assert time.time() - t0 < 120
     assert r.tracked_peak == r.planned_total == r.stored_cost + r.max_segment
     assert 1 - r.planned_total / r.store_all_total >= 0.60
+
+
+@pytest.mark.parametrize("arch,batch,hw", [("inception_v3", 4, 299), ("densenet121", 2, 224), ("resnet50", 4, 224),
+                                           ("vgg16", 2, 224)])
+def test_gradient_sums_formed_in_plan_independent_order(arch, batch, hw):
+    """A tensor read by several ops gets one gradient contribution per
+    consumer, accumulated in place in bf16 (not associative): every plan runs
+    the consumers' backward in the same (descending op id) order, so
+    re-forward and store-all form every gradient sum identically."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from _parity import plan
+    orders = {}
+    for policy in ("reforward", "store_all"):
+        net = ReforwardNet.named(arch, batch, hw, hw, 1000)
+        plan(net, arch, batch, hw, policy)
+        pos = {op: k for k, (kind, op, _, _, _) in enumerate(net.schedule()) if kind == "backward"}
+        for t in net.tensors():
+            cons = sorted({o.id for o in net.ops() if t.id in o.inputs})
+            if len(cons) > 1:
+                seq = sorted(cons, key=lambda c: pos[c])
+                assert seq == sorted(cons, reverse=True), (policy, t.name, seq)
+                orders.setdefault(t.name, []).append(seq)
+    assert bool(orders) == (arch != "vgg16")  # a linear chain has no shared tensors
+    assert all(len(v) == 2 and v[0] == v[1] for v in orders.values())

@@ -3,12 +3,15 @@
 Levels, as BASELINE.json's north star asks (tolerances stated in DESIGN.md
 "Parity"):
 * whole step against the CPU step that stores bf16 at the same points
-  (emulate_bf16): loss within 1e-3 relative, and every parameter gradient
+  (emulate_bf16): loss within max(1e-3 relative, 3 x its floor), and every
+  parameter gradient
   within  ||g_gpu - g_cpu|| / ||g_cpu|| <= max(2e-2, 3 x floor), where floor is
   that parameter's distance between the CPU step with fp32 and with fp64
   accumulation -- the configuration's own bf16 rounding-flip noise (the GPU's
-  fp32 accumulation order is an independent draw of it).  Plain random init:
-  no scaled residual gammas, no scaled classifier;
+  fp32 accumulation order is an independent draw of it).  Plain random init
+  (residual BN gammas at 1): at these tiny sizes a BN net at init is chaotic
+  (batch-norm gradient explosion) and its floors are large; ResNet-50 with
+  the standard zero-init residual gammas gives a small floor, i.e. a tight bar;
 * on the GPU, re-forward gradients are bit-identical to store-all gradients
   (deterministic kernels; same arithmetic whether a tensor was stored or
   recomputed).
@@ -24,8 +27,9 @@ from _parity import plan
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("chain8", 4, 32, 10), ("resnet18", 4, 64, 10), ("resnet50", 2, 64, 16), ("densenet_tiny", 4, 32, 10),
-         ("vgg11", 4, 32, 10), ("alexnet", 4, 64, 10), ("inception_v3", 2, 139, 10)]
+CASES = [("chain8", 4, 32, 10, 1.0), ("resnet18", 4, 64, 10, 1.0), ("resnet50", 2, 64, 16, 1.0),
+         ("resnet50", 2, 64, 16, 0.0), ("densenet_tiny", 4, 32, 10, 1.0), ("vgg11", 4, 32, 10, 1.0),
+         ("alexnet", 4, 64, 10, 1.0), ("inception_v3", 2, 139, 10, 1.0)]
 
 
 def _run(arch, batch, hw, classes, policy, oracle_weights, x, y, stored=None):
@@ -41,25 +45,25 @@ def _run(arch, batch, hw, classes, policy, oracle_weights, x, y, stored=None):
     return net, rep, loss, grads
 
 
-@pytest.mark.parametrize("arch,batch,hw,classes", CASES)
-def test_parity_with_cpu_oracle_and_bit_identity(arch, batch, hw, classes):
+@pytest.mark.parametrize("arch,batch,hw,classes,gamma", CASES)
+def test_parity_with_cpu_oracle_and_bit_identity(arch, batch, hw, classes, gamma):
     probe = ReforwardNet.named(arch, batch, hw, hw, classes)
     plan(probe, arch, batch, hw)  # memoised in plans/ (Inception-v3 takes minutes)
     o = OracleNet(probe, emulate_bf16=True)
-    o.init_weights(seed=11)
+    o.init_weights(seed=11, residual_gamma=gamma)
     x, y = random_batch(probe, seed=5)
     stored, seg = probe.plan_sets()
     ref_loss, ref_grads, ref_peak = o.run_step(x, y, probe.schedule(), stored, seg)
     o64 = OracleNet(probe, dtype=torch.float64, emulate_bf16=True)
     o64.weights = {k: v.double() for k, v in o.weights.items()}
-    _, g64, _ = o64.run_step(x, y, probe.schedule(), stored, seg)
+    l64, g64, _ = o64.run_step(x, y, probe.schedule(), stored, seg)
 
     _, rep_r, loss_r, g_r = _run(arch, batch, hw, classes, "reforward", o, x, y, stored=stored)
     _, rep_s, loss_s, g_s = _run(arch, batch, hw, classes, "store_all", o, x, y)
 
     assert rep_r.tracked_peak == rep_r.planned_total == ref_peak
     assert rep_r.planned_total < rep_s.planned_total
-    assert abs(loss_r - ref_loss) <= 1e-3 * abs(ref_loss), (loss_r, ref_loss)
+    assert abs(loss_r - ref_loss) <= max(1e-3 * abs(ref_loss), 3 * abs(ref_loss - l64)), (loss_r, ref_loss, l64)
     bad = []
     for n in ref_grads:
         err = rel_err(g_r[n], ref_grads[n].numpy())

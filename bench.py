@@ -13,9 +13,10 @@ D2H read of the loss inside every timed step.  The same run also times the
 store-all plan to report the re-forward time overhead, and reports the
 activation memory (planner Eq. 1 vs store-all) the overhead buys.
 
-`--impl reference` times the CPU path instead: the reference planner compiled
-from the reference headers (oracle/_ref, when shipped) for the plan, and the CPU
-fp32 re-forward train step (oracle/train_oracle.py) on a bounded sample.
+`--impl reference` times the CPU path instead: the CPU fp32 re-forward train
+step (oracle/train_oracle.py) at the same batch, following the plan the
+reference planner chose (committed fixture oracle/fixtures/, exported once
+with oracle/_ref), on every host core; the product library is not loaded.
 """
 from __future__ import annotations
 
@@ -233,70 +234,75 @@ def build_net(batch, policy, seed=0):
     return net, rep, plan_s
 
 
-def cpu_baseline_sample(threads=None, gpu_stored=None):
-    """Bounded CPU sample: one re-forward train step of the benched network at batch 2."""
+def cpu_baseline_sample(threads=None, gpu_stored=None, batch=32):
+    """Bounded CPU sample: one re-forward train step of the benched network.
+
+    With a fixture (oracle/fixtures/<arch>_b<batch>_<hw>.json.gz: the graph,
+    the REFERENCE planner's stored set and the re-forward schedule, exported
+    once by oracle/make_fixture.py) the step runs at the benched batch without
+    touching the product library.  Networks without a fixture fall back to
+    batch 2 with the plan of the GPU run."""
     import torch
+    from oracle.fixture import FixtureNet, fixture_path
     from oracle.train_oracle import OracleNet, random_batch
-    from paper_1808_00079_b200.executor import ReforwardNet
     if threads:
         torch.set_num_threads(threads)
-    b = 2
-    net = ReforwardNet.named(ARCH, b, HW, HW, CLASSES)
-    plan_kind = "product planner"
-    stored = None
-    if gpu_stored is not None:
-        # DenseNet / Inception: the reference planner needs minutes on these
-        # graphs.  Every Eq. 1 cost is proportional to the batch, so the GPU
-        # run's optimal vertex set is also optimal at batch 2 (same tensor ids).
-        net.plan_with_stored(gpu_stored, "gpu-plan")
-        plan_kind = "the GPU run's plan (Eq. 1 costs scale with the batch)"
+    if os.path.exists(fixture_path(ARCH, batch, HW)):
+        net = FixtureNet.named(ARCH, batch, HW)
+        b = batch
+        plan_kind = net.meta["plan_source"]
     else:
-        try:
-            from paper_1808_00079_b200.planner import reference_planner
-            R = reference_planner()
-            verts, edges = net.graph()
-            g = R.from_named_edges(verts, edges)
-            stored = g.solve_acg().stored
-            net.plan_with_stored(stored, "reference-planner")
-            plan_kind = "reference planner (oracle/_ref)"
-        except Exception:
-            net.plan("reforward")
+        from paper_1808_00079_b200.executor import ReforwardNet
+        b = 2
+        net = ReforwardNet.named(ARCH, b, HW, HW, CLASSES)
+        # every Eq. 1 cost scales with the batch, so the GPU run's optimal
+        # vertex set is also optimal at batch 2 (same tensor ids)
+        net.plan_with_stored(gpu_stored, "gpu-plan") if gpu_stored is not None else net.plan("reforward")
+        plan_kind = "the GPU run's plan" if gpu_stored is not None else "product planner"
     o = OracleNet(net)
     o.init_weights(0)
     x, y = random_batch(net, 0)
     st, seg = net.plan_sets()
     sched = net.schedule()
-    o.run_step(x, y, sched, st, seg)  # warm-up
     t0 = time.time()
-    o.run_step(x, y, sched, st, seg)
+    loss, _, _ = o.run_step(x, y, sched, st, seg)
     dt = time.time() - t0
+    if not math.isfinite(loss):
+        raise RuntimeError("non-finite CPU loss")
     return {"value": b / dt, "unit": "imgs/s", "cores": torch.get_num_threads(), "kind": "port",
             "sample": f"1 re-forward train step of {ARCH} at batch {b}, 3x{HW}x{HW}, fp32 CPU "
-                      f"(oracle/train_oracle.py following the executor schedule; plan by {plan_kind})",
-            "seconds": dt}
+                      f"(oracle/train_oracle.py following the re-forward schedule; plan: {plan_kind})",
+            "batch": b, "seconds": dt}
 
 
 def run_reference(args):
+    """The reference arm: the CPU re-forward train step (oracle/train_oracle.py,
+    a port -- the reference has no training code) on every host core, at the
+    GPU arm's config (batch per step = --batch), plan from the reference
+    planner via the committed fixture; no product code on this path."""
     import torch
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     threads = os.cpu_count()
-    vals = []
+    torch.set_num_threads(threads)
     for _ in range(max(args.warmup, 0)):
-        cpu_baseline_sample(threads)
+        cpu_baseline_sample(threads, batch=args.batch)
+    vals = []
     t0 = time.time()
     for _ in range(args.steps):
-        vals.append(cpu_baseline_sample(threads))
+        vals.append(cpu_baseline_sample(threads, batch=args.batch))
     total = time.time() - t0
-    v = sum(x["value"] for x in vals) / len(vals)
+    b = vals[0]["batch"]
+    v = b * len(vals) / sum(x["seconds"] for x in vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "imgs/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic random images/labels, random-init weights",
-            "config": {"workload": "resnet50 re-forward training, 3x224x224 (CPU bounded sample, batch 2/step)",
-                       "global_batch": 2, "seq_len": None, "parallelism": "cpu"},
-            "cpu_baseline": {"value": v, "unit": "imgs/s", "cores": torch.get_num_threads(), "kind": "port",
+            "config": {"workload": f"{ARCH} re-forward training, batch {b}/step, 3x{HW}x{HW}, SGD (CPU)",
+                       "model": ARCH, "global_batch": b, "seq_len": None, "parallelism": "cpu",
+                       "same_config_as_gpu_arm": b == args.batch},
+            "cpu_baseline": {"value": v, "unit": "imgs/s", "cores": threads, "kind": "port",
                              "sample": vals[0]["sample"]},
             "e2e": {"value": v, "unit": "imgs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -330,6 +336,7 @@ def main():
     peaks, peak_kind = _peaks()
 
     net, rep, plan_s = build_net(args.batch, "reforward", seed=1234)
+    dev_bytes = net.report().device_bytes  # after setup, before the e2e staging buffers
     gpu_stored = net.plan_sets()[0] if ARCH.startswith(("densenet", "inception")) else None
     x, y = random_batch(net, seed=rank)
     net.load_batch(x.cuda(), y.cuda(), stream=stream)
@@ -383,6 +390,7 @@ def main():
     # store-all comparison (same kernels, plan = every tensor stored)
     overhead = None
     sa_value = None
+    sa_device = None
     if not args.no_store_all:
         del net
         torch.cuda.synchronize()
@@ -396,13 +404,15 @@ def main():
         ms_sa = time_steps(net_sa, args.steps, args.warmup, stream, world)
         sa_value = args.batch * world / (ms_sa / 1000.0)
         overhead = ms / ms_sa
+        sa_device = net_sa.report().device_bytes
         del net_sa
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_sample(os.cpu_count(), gpu_stored)
+            cpu = cpu_baseline_sample(os.cpu_count(), gpu_stored, batch=args.batch)
             cpu.pop("seconds", None)
+            cpu.pop("batch", None)
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": "imgs/s", "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 
@@ -422,7 +432,12 @@ def main():
                        "cut_percent": 100.0 * (1 - rep.planned_total / rep.store_all_total),
                        "arena_bytes": rep.arena_bytes, "grad_arena_bytes": rep.grad_arena_bytes,
                        "workspace_bytes": rep.workspace_bytes, "reforward_ops": rep.reforward_ops,
-                       "plan_seconds": plan_s},
+                       "plan_seconds": plan_s,
+                       # every cudaMalloc of the net (arena + guard band, gradient arena,
+                       # workspace, parameters / gradients / momentum / bf16 copies, BN state,
+                       # input and staging buffers), re-forward vs store-all
+                       "device_bytes": dev_bytes, "store_all_device_bytes": sa_device,
+                       "device_cut_percent": (100.0 * (1 - dev_bytes / sa_device)) if sa_device else None},
             "store_all": {"value": sa_value, "unit": "imgs/s"},
             "overhead_vs_store_all": overhead,
             "e2e": {"value": e2e_value, "unit": "imgs/s",

@@ -128,6 +128,9 @@ typedef struct rfx_memory_report {
   int64_t candidate_max_term;
   int32_t n_segments;
   int32_t n_stored;
+  int64_t device_bytes;      /* every device allocation of the net after setup (arena + guard band,
+                                gradient arena, workspace, parameters / gradients / momentum, bf16
+                                copies, BN state, input, staging, tables) */
 } rfx_memory_report;
 
 int rfx_net_plan_info(const rfx_net* net, uint8_t* stored_mask, int32_t* seg_of, rfx_memory_report* rep);

@@ -194,6 +194,7 @@ int rfx_net_plan_info(const rfx_net* n, uint8_t* mask, int32_t* seg_of, rfx_memo
       rep->forward_ops = r.forward_ops;
       rep->backward_ops = r.backward_ops;
       rep->launches_per_step = r.launches_per_step;
+      rep->device_bytes = r.device_bytes;
       rep->candidate_max_term = p.candidate_max_term;
       rep->n_segments = (int32_t)p.seg_cost.size();
       int32_t ns = 0;

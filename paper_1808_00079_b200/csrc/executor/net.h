@@ -121,6 +121,7 @@ struct MemoryReport {
   long grad_arena_bytes = 0, workspace_bytes = 0, param_bytes = 0, state_bytes = 0;
   long reforward_ops = 0, segment_loads = 0, forward_ops = 0, backward_ops = 0;
   long launches_per_step = 0;
+  long device_bytes = 0;  // every cudaMalloc of this net (arena + guard, gradients, workspace, parameters, ...)
 };
 
 struct SubpixelDim {

@@ -111,8 +111,10 @@ void Net::setup(uint64_t seed) {
     p.bf16_off = p.offset;
     p.bf16_count = p.count;
   }
+  rep_.device_bytes = 0;
   auto alloc = [&](void** p, long bytes, const char* what) {
     check(cudaMalloc(p, bytes > 0 ? bytes : 256), what);
+    rep_.device_bytes += bytes > 0 ? bytes : 256;
   };
   // the activation arena is exactly the planner's Eq. 1 total; a guard band
   // behind it (filled with a canary) lets tests check that no kernel of the
@@ -1137,6 +1139,7 @@ void Net::build_gather_tables() {
     }
   }
   check(cudaMalloc(&d_gather_, tab.size() * sizeof(rfk::BnGatherBlock)), "gather table");
+  rep_.device_bytes += (long)(tab.size() * sizeof(rfk::BnGatherBlock));
   check(cudaMemcpy(d_gather_, tab.data(), tab.size() * sizeof(rfk::BnGatherBlock), cudaMemcpyHostToDevice),
         "gather table");
 }
@@ -1184,6 +1187,7 @@ void Net::prep_weights_table(cudaStream_t st) {
     prep_layers_ = (int)tab.size();
     prep_total_ = start;
     check(cudaMalloc(&d_prep_table_, sizeof(rfk::WeightPrepLayer) * std::max<size_t>(1, tab.size())), "prep table");
+    rep_.device_bytes += (long)(sizeof(rfk::WeightPrepLayer) * std::max<size_t>(1, tab.size()));
     check(cudaMemcpy(d_prep_table_, tab.data(), sizeof(rfk::WeightPrepLayer) * tab.size(), cudaMemcpyHostToDevice),
           "prep table");
   }
@@ -1214,6 +1218,7 @@ void Net::ensure_staging() {
   for (int s = 0; s < 2; ++s) {
     check(cudaMalloc(&d_stage_images_[s], nimg * 4), "staging images");
     check(cudaMalloc(&d_stage_labels_[s], batch_ * 4), "staging labels");
+    rep_.device_bytes += nimg * 4 + batch_ * 4;
     check(cudaEventCreateWithFlags(&stage_ready_[s], cudaEventDisableTiming), "event");
     check(cudaEventCreateWithFlags(&stage_free_[s], cudaEventDisableTiming), "event");
   }

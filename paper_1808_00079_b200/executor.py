@@ -28,7 +28,7 @@ class MemoryReport(C.Structure):
         "planned_total", "stored_cost", "max_segment", "store_all_total", "tracked_peak", "arena_bytes",
         "grad_arena_bytes", "workspace_bytes", "param_bytes", "state_bytes", "reforward_ops", "segment_loads",
         "forward_ops", "backward_ops", "launches_per_step", "candidate_max_term")] + [
-        ("n_segments", C.c_int32), ("n_stored", C.c_int32)]
+        ("n_segments", C.c_int32), ("n_stored", C.c_int32), ("device_bytes", C.c_int64)]
 
     def as_dict(self) -> Dict[str, int]:
         return {k: getattr(self, k) for k, _ in self._fields_}

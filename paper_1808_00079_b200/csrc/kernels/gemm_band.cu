@@ -515,9 +515,6 @@ cudaError_t band_launch(BandParams& bp, cudaStream_t st) {
 bool gemm_band_ok(const GemmDesc& d) {
   const ConvGeom& g = d.a_geom;
   if (g.stride_h != 1 || g.stride_w != 1 || g.R * g.S < 2) return false;
-  // 5x5 (both dims > 3) misses taps at the band edge (round-2 parity test,
-  // ~1 % of outputs off by one tap): those shapes take the im2col kernel
-  if (g.R > 3 && g.S > 3) return false;
   const int Wp = g.W + 2 * g.pad_w;
   if (Wp > 256 || g.Q < 24) return false;  // junk columns (S - 1 of Wp) must stay a small fraction
   const int BR = band_rows(Wp, g.R);

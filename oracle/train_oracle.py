@@ -179,6 +179,17 @@ class OracleNet:
                 gs = torch.autograd.grad(z, [y] + ws, grad_outputs=g)
                 in_grads = [(op.inputs[0], gs[0]), (op.inputs[1], g)]
                 wgr = gs[1:]
+            elif op.kind == "bn" and self.attrs[op.id]["k"] == 1:
+                # BN + ReLU: the ReLU mask from the op's own output (as for
+                # the residual add above); recomputing it would let a value
+                # sitting exactly at 0 flip with the last bit of the stats
+                y = vals[op.inputs[0]].detach().clone().requires_grad_(True)
+                z = self._bn_only(op, y)
+                out = vals[op.out] if op.out in vals else self.rb(torch.relu(z.detach()))
+                g = dout * (out > 0).to(dout.dtype)
+                gs = torch.autograd.grad(z, [y] + ws, grad_outputs=g)
+                in_grads = [(op.inputs[0], gs[0])]
+                wgr = gs[1:]
             elif op.kind == "relu":  # mask from the output (the input may be released)
                 in_grads = [(op.inputs[0], dout * (vals[op.out] > 0).to(dout.dtype))]
                 wgr = []

@@ -10,7 +10,8 @@ import ctypes
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libreforward_b200.so")
+# RF_LIB_PATH: another build of the same library (A/B timing experiments)
+LIB_PATH = os.environ.get("RF_LIB_PATH") or os.path.join(PKG_DIR, "libreforward_b200.so")
 _lib = None
 
 

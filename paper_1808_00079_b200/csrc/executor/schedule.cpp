@@ -539,7 +539,9 @@ void Net::build_schedule() {
   // op id first) whatever the plan: re-forward and store-all form every
   // gradient sum in the same order and stay bit-identical.  The highest-id
   // remaining op is always eligible, so this cannot deadlock.
+  static const bool fixed_order = !std::getenv("RFK_BWD_ORDER") || std::atoi(std::getenv("RFK_BWD_ORDER")) != 0;
   auto order_ok = [&](int o) {
+    if (!fixed_order) return true;  // diagnostics only: plan-dependent sums
     for (int i : ops_[o].in)
       for (int c : tensors_[i].consumers)
         if (c > o && !done[c]) return false;

@@ -1534,6 +1534,18 @@ __global__ void __launch_bounds__(kThreads) add_bf16_kernel(const __nv_bfloat16*
 
 long rows_per_block_for(long M, int blocks) { return (M + blocks - 1) / blocks; }
 
+// Timing experiments only (results become wrong): RFK_ABLATE bit mask skips
+// kernels to bound what removing them could save -- 1 forward BN finalize,
+// 2 backward BN finalize, 4 backward BN reduce, 8 forward BN apply,
+// 16 backward BN apply.
+int ablate() {
+  static const int m = [] {
+    const char* e = std::getenv("RFK_ABLATE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
 }  // namespace
 
 // ============================================================ launchers
@@ -1554,6 +1566,7 @@ cudaError_t colstats(const __nv_bfloat16* x, long M, int C, float* partials, int
 cudaError_t bn_finalize(const float* partials, int parts, int C, long count, const float* gamma, const float* beta,
                         float eps, float* mean, float* invstd, float* scale, float* shift, float* run_mean,
                         float* run_var, float momentum, bool update_running, cudaStream_t st) {
+  if (ablate() & 1) return cudaSuccess;
   RFK_CHECK_LAUNCH(launch_k(bn_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, partials, parts, C, (float)count, gamma, beta, eps, mean,
                                                             invstd, scale, shift, run_mean, run_var, momentum,
                                                             update_running ? 1 : 0));
@@ -1573,6 +1586,7 @@ cudaError_t bn_apply(const __nv_bfloat16* y, const __nv_bfloat16* skip, const fl
                      bool relu, long M, int C, __nv_bfloat16* out, cudaStream_t st) {
   const long nvec = M * C / 8;
   if (nvec >= (1L << 31)) return cudaErrorInvalidValue;
+  if (ablate() & 8) return cudaSuccess;
   const int g = grid_for(nvec, kThreads * kVec, 148 * 8);
   const unsigned nv = (unsigned)nvec;
   if (skip) {
@@ -1595,19 +1609,20 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
   if (nvec >= (1L << 31)) return cudaErrorInvalidValue;
   dim3 grid(blocks, (C + 2047) / 2048);
   const long rpb = rows_per_block_for(M, blocks);
-  switch (mask_mode) {
+  if (!(ablate() & 4)) switch (mask_mode) {
     case 0: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<0>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials)); break;
     case 1: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<1>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials)); break;
     default: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<2>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials));
   }
-  RFK_CHECK_LAUNCH(launch_k(bn_bwd_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, partials, blocks, C, (float)M, gamma, mean, invstd,
+  if (!(ablate() & 2)) RFK_CHECK_LAUNCH(launch_k(bn_bwd_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, partials, blocks, C, (float)M, gamma, mean, invstd,
                                                                 dgamma, dbeta, coef));
   const int g = grid_for(nvec, kThreads * 2, 148 * 4);  // one wave at 4 blocks per SM
   const unsigned nv = (unsigned)nvec;
   const int ad = acc_dy ? 1 : 0, as = acc_dskip ? 1 : 0;
 #define RF_BWD_APPLY(MODE, SKIP) \
   RFK_CHECK_LAUNCH(launch_k(bn_bwd_apply_kernel<MODE, SKIP>, g, kThreads, 0, st, y, dout, out, scale, shift, coef, nv, C, dy, ad, dskip, as))
-  if (dskip) {
+  if (ablate() & 16) {
+  } else if (dskip) {
     switch (mask_mode) {
       case 0: RF_BWD_APPLY(0, true); break;
       case 1: RF_BWD_APPLY(1, true); break;

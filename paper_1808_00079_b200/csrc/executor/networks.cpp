@@ -1,7 +1,10 @@
 // Reference network topologies of the paper's experiments (§6, Table 1) and
 // BASELINE.json's configs, built on the executor IR.  Random-init weights;
 // the point is the graph shape and the kernels it exercises.
+#include <algorithm>
 #include <stdexcept>
+#include <cstdio>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -245,7 +248,7 @@ int inception_e(Net& n, int x, const std::string& nm) {
 
 // torchvision Inception-v3 (Szegedy et al. 2016), training graph without the
 // auxiliary classifier and dropout; BN eps 1e-5 like every BN here.
-void build_inception3(Net& n, int H, int W, int classes) {
+void build_inception3(Net& n, int H, int W, int classes, int mixed_blocks) {
   int x = n.input(H, W, 3);
   x = bconv(n, x, 32, 3, 3, 2, 0, 0, "Conv2d_1a_3x3");
   x = bconv(n, x, 32, 3, 3, 1, 0, 0, "Conv2d_2a_3x3");
@@ -254,24 +257,36 @@ void build_inception3(Net& n, int H, int W, int classes) {
   x = bconv(n, x, 80, 1, 1, 1, 0, 0, "Conv2d_3b_1x1");
   x = bconv(n, x, 192, 3, 3, 1, 0, 0, "Conv2d_4a_3x3");
   x = n.maxpool(x, 3, 2, 0, "maxpool2");
-  x = inception_a(n, x, 32, "Mixed_5b");
-  x = inception_a(n, x, 64, "Mixed_5c");
-  x = inception_a(n, x, 64, "Mixed_5d");
-  x = inception_b(n, x, "Mixed_6a");
-  x = inception_c(n, x, 128, "Mixed_6b");
-  x = inception_c(n, x, 160, "Mixed_6c");
-  x = inception_c(n, x, 160, "Mixed_6d");
-  x = inception_c(n, x, 192, "Mixed_6e");
-  x = inception_d(n, x, "Mixed_7a");
-  x = inception_e(n, x, "Mixed_7b");
-  x = inception_e(n, x, "Mixed_7c");
+  // the eleven mixed blocks in order; a reduced variant keeps the first k
+  // (test-scale graphs the reference planner can solve in minutes)
+  const std::function<int(int)> blocks[11] = {
+      [&](int v) { return inception_a(n, v, 32, "Mixed_5b"); },
+      [&](int v) { return inception_a(n, v, 64, "Mixed_5c"); },
+      [&](int v) { return inception_a(n, v, 64, "Mixed_5d"); },
+      [&](int v) { return inception_b(n, v, "Mixed_6a"); },
+      [&](int v) { return inception_c(n, v, 128, "Mixed_6b"); },
+      [&](int v) { return inception_c(n, v, 160, "Mixed_6c"); },
+      [&](int v) { return inception_c(n, v, 160, "Mixed_6d"); },
+      [&](int v) { return inception_c(n, v, 192, "Mixed_6e"); },
+      [&](int v) { return inception_d(n, v, "Mixed_7a"); },
+      [&](int v) { return inception_e(n, v, "Mixed_7b"); },
+      [&](int v) { return inception_e(n, v, "Mixed_7c"); }};
+  for (int b = 0; b < std::min(11, mixed_blocks); ++b) x = blocks[b](x);
   x = n.avgpool(x, "avgpool");
   x = n.fc(x, classes, "fc");
   n.loss(x, "loss");
 }
 
 void build_named(Net& n, const std::string& arch, int H, int W, int classes) {
-  if (arch == "inception_v3") return build_inception3(n, H, W, classes);
+  if (arch == "inception_v3") return build_inception3(n, H, W, classes, 11);
+  // reduced variants for reference-pinned plans: inception_v3_m<k> (first k
+  // mixed blocks), densenet_<b1>_<b2>_<b3>_<b4> (growth 32, 64 initial features)
+  if (arch.rfind("inception_v3_m", 0) == 0) return build_inception3(n, H, W, classes, std::stoi(arch.substr(14)));
+  if (arch.rfind("densenet_", 0) == 0 && arch != "densenet_tiny") {
+    int b[4];
+    if (std::sscanf(arch.c_str(), "densenet_%d_%d_%d_%d", &b[0], &b[1], &b[2], &b[3]) == 4)
+      return build_densenet(n, b, 32, 64, H, W, classes);
+  }
   static const int d121[4] = {6, 12, 24, 16}, d169[4] = {6, 12, 32, 32}, d201[4] = {6, 12, 48, 32},
                    d161[4] = {6, 12, 36, 24};
   static const int dtiny[4] = {2, 2, 2, 2};

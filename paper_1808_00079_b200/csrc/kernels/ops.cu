@@ -290,11 +290,13 @@ __global__ void __launch_bounds__(kThreads) bn_apply_kernel(const __nv_bfloat16*
 // (same expression as the forward), 2 relu of the stored output (out > 0).
 // Two rows per thread in flight and <= 85 registers (3 blocks of 256 per SM)
 // keep enough loads outstanding for HBM.
+// gout (MODE 2 only, optional): also store g = dout * mask -- the residual
+// add's skip gradient -- so the apply pass reads g instead of dout and out.
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 3) bn_bwd_reduce_kernel(
     const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
     const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ shift, long M, int C,
-    long rows_per_block, float* __restrict__ partials) {
+    long rows_per_block, float* __restrict__ partials, __nv_bfloat16* __restrict__ gout) {
   pdl_enter();
   __shared__ float sh[2][kThreads][8];
   const int cchunk = blockIdx.y;
@@ -339,9 +341,13 @@ __global__ void __launch_bounds__(kThreads, 3) bn_bwd_reduce_kernel(
           float g = fd[i];
           if (MODE == 1) g = (fmaf(fy[i], sc[i], sf[i]) > 0.f) ? g : 0.f;
           if (MODE == 2) g = (fo[i] > 0.f) ? g : 0.f;
+          fd[i] = g;
           a[i] += g;
           b[i] = fmaf(g, fy[i] - mu[i], b[i]);
         }
+        // g is dout with some lanes zeroed: exactly representable, so the
+        // stored bf16 equals what the separate apply pass would write
+        if (MODE == 2 && gout) *reinterpret_cast<uint4*>(gout + (u ? off1 : off0)) = pack8(fd);
       }
     }
   }
@@ -432,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, 4) bn_bwd_apply_kernel(
 #pragma unroll
         for (int i = 0; i < 8; ++i) fd[i] = (fmaf(fy[i], sc[i], sh[i]) > 0.f) ? fd[i] : 0.f;
       }
+      // MODE 3: `dout` already holds g (written by the reduction), no mask
       {
         float k[8];
         ld8f(coef + c0, k);
@@ -1538,6 +1545,15 @@ long rows_per_block_for(long M, int blocks) { return (M + blocks - 1) / blocks; 
 // kernels to bound what removing them could save -- 1 forward BN finalize,
 // 2 backward BN finalize, 4 backward BN reduce, 8 forward BN apply,
 // 16 backward BN apply.
+// RFK_G_EARLY=0: the residual-add BN backward re-derives g in the apply pass
+bool g_early_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("RFK_G_EARLY");
+    return e && std::atoi(e) == 0;
+  }();
+  return off;
+}
+
 int ablate() {
   static const int m = [] {
     const char* e = std::getenv("RFK_ABLATE");
@@ -1609,10 +1625,15 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
   if (nvec >= (1L << 31)) return cudaErrorInvalidValue;
   dim3 grid(blocks, (C + 2047) / 2048);
   const long rpb = rows_per_block_for(M, blocks);
+  // residual add whose skip gradient is written (not accumulated): the
+  // reduction stores g there, and the apply reads g back (7 passes over the
+  // tensor instead of 8: dout and out are read once, not twice)
+  const bool g_early = mask_mode == 2 && dskip && !acc_dskip && !g_early_off();
+  __nv_bfloat16* gout = g_early ? dskip : nullptr;
   if (!(ablate() & 4)) switch (mask_mode) {
-    case 0: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<0>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials)); break;
-    case 1: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<1>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials)); break;
-    default: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<2>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials));
+    case 0: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<0>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout)); break;
+    case 1: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<1>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout)); break;
+    default: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<2>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout));
   }
   if (!(ablate() & 2)) RFK_CHECK_LAUNCH(launch_k(bn_bwd_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, partials, blocks, C, (float)M, gamma, mean, invstd,
                                                                 dgamma, dbeta, coef));
@@ -1622,6 +1643,10 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
 #define RF_BWD_APPLY(MODE, SKIP) \
   RFK_CHECK_LAUNCH(launch_k(bn_bwd_apply_kernel<MODE, SKIP>, g, kThreads, 0, st, y, dout, out, scale, shift, coef, nv, C, dy, ad, dskip, as))
   if (ablate() & 16) {
+  } else if (g_early) {
+    const __nv_bfloat16* gbuf = dskip;
+    RFK_CHECK_LAUNCH(launch_k(bn_bwd_apply_kernel<3, false>, g, kThreads, 0, st, y, gbuf, out, scale, shift, coef, nv,
+                              C, dy, ad, static_cast<__nv_bfloat16*>(nullptr), 0));
   } else if (dskip) {
     switch (mask_mode) {
       case 0: RF_BWD_APPLY(0, true); break;

@@ -62,7 +62,8 @@ struct alignas(64) KParams {
   const float* bn_scale;
   const float* bn_shift;
   int bn_relu, fuse_bn;
-  int experiment;  // tuning only: 2 drop the output, 3 also skip TMEM loads, 4 also skip the MMAs
+  int experiment;  // tuning only: 2 drop the output, 3 also skip TMEM loads, 4 also skip the MMAs,
+                  // 5 skip the statistics smem reads, 6 skip the statistics accumulation
 };
 
 template <int BN>
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll 1
       for (int c0 = (int)half * 32; c0 < BN; c0 += 64) {
         uint32_t r[32];
-        if (!empty_k && p.experiment < 3) {
+        if (!empty_k && (p.experiment < 3 || p.experiment > 4)) {
           tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
           tmem_ld_wait();
         } else {
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int col0 = tc.n0 + c0;
-        if (col0 >= p.N || p.experiment >= 2) continue;  // warp-uniform
+        if (col0 >= p.N || (p.experiment >= 2 && p.experiment <= 4)) continue;  // warp-uniform
         const bool full_cols = col0 + 32 <= p.N;
         if (p.bias) {
 #pragma unroll
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const uint32_t cp = lane & 15, par = lane >> 4;
           float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
 #pragma unroll
-          for (int rr = 0; rr < 16; ++rr) {
+          for (int rr = 0; rr < (p.experiment == 5 ? 0 : 16); ++rr) {
             const uint32_t row = 2 * rr + par;
             const uint32_t off = row * 64 + (((cp >> 2) ^ ((row >> 1) & 3u)) * 16) + (cp & 3) * 4;
             const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sbuf + off));
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
           q0 += __shfl_xor_sync(0xffffffffu, q0, 16);
           q1 += __shfl_xor_sync(0xffffffffu, q1, 16);
-          if (lane < 16) {
+          if (lane < 16 && p.experiment != 6) {
             const int lc = ((c0 >> 6) << 5) + 2 * (int)lane;  // this warp's local column
             my_sum[lc] += s0;
             my_sum[lc + 1] += s1;

@@ -80,12 +80,12 @@ __device__ __forceinline__ RedShape red_shape(int C) {
 // mode: 0 = plain column sum / sum of squares of x
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) colstats_kernel(const __nv_bfloat16* __restrict__ x, long M, int C,
-                                                            long rows_per_block, float* __restrict__ partials) {
+                                                            long rows_per_block, float* __restrict__ partials, int cw) {
   pdl_enter();
-  // handles C <= 2048 per pass; channel chunks via blockIdx.y
+  // handles cw <= 2048 channels per pass; channel chunks via blockIdx.y
   __shared__ float sh[2][kThreads][8];
-  const int cchunk = blockIdx.y;  // chunk of 2048 channels
-  const int Cc = min(2048, C - cchunk * 2048);
+  const int cchunk = blockIdx.y;  // chunk of cw channels
+  const int Cc = min(cw, C - cchunk * cw);
   const RedShape s = red_shape(Cc);
   const int t = threadIdx.x;
   const int lane = t % s.tpr, rgrp = t / s.tpr;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) colstats_kernel(const __nv_bfloat16*
   if (rgrp < s.rows_per_pass) {
     for (long r = r0 + rgrp; r < r1; r += s.rows_per_pass) {
       float f[8];
-      unpack8(ldg16(x + r * C + cchunk * 2048 + lane * 8), f);
+      unpack8(ldg16(x + r * C + cchunk * cw + lane * 8), f);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         a[i] += f[i];
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kThreads) colstats_kernel(const __nv_bfloat16*
         a[i] += sh[0][g * s.tpr + t][i];
         b[i] += sh[1][g * s.tpr + t][i];
       }
-    float* out = partials + (long)blockIdx.x * 2 * C + cchunk * 2048 + t * 8;
+    float* out = partials + (long)blockIdx.x * 2 * C + cchunk * cw + t * 8;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       out[i] = a[i];
@@ -296,15 +296,15 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads, 3) bn_bwd_reduce_kernel(
     const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dout, const __nv_bfloat16* __restrict__ out,
     const float* __restrict__ mean, const float* __restrict__ scale, const float* __restrict__ shift, long M, int C,
-    long rows_per_block, float* __restrict__ partials, __nv_bfloat16* __restrict__ gout) {
+    long rows_per_block, float* __restrict__ partials, __nv_bfloat16* __restrict__ gout, int cw) {
   pdl_enter();
   __shared__ float sh[2][kThreads][8];
   const int cchunk = blockIdx.y;
-  const int Cc = min(2048, C - cchunk * 2048);
+  const int Cc = min(cw, C - cchunk * cw);
   const RedShape s = red_shape(Cc);
   const int t = threadIdx.x;
   const int lane = t % s.tpr, rgrp = t / s.tpr;
-  const int c0 = cchunk * 2048 + lane * 8;
+  const int c0 = cchunk * cw + lane * 8;
   float a[8], b[8], mu[8], sc[8], sf[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) a[i] = b[i] = 0.f;
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 3) bn_bwd_reduce_kernel(
         a[i] += sh[0][gi * s.tpr + t][i];
         b[i] += sh[1][gi * s.tpr + t][i];
       }
-    float* o = partials + (long)blockIdx.x * 2 * C + cchunk * 2048 + t * 8;
+    float* o = partials + (long)blockIdx.x * 2 * C + cchunk * cw + t * 8;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       o[i] = a[i];
@@ -1541,6 +1541,17 @@ __global__ void __launch_bounds__(kThreads) add_bf16_kernel(const __nv_bfloat16*
 
 long rows_per_block_for(long M, int blocks) { return (M + blocks - 1) / blocks; }
 
+// Channel chunk of a column reduction's blocks (blockIdx.y): all of C when
+// C <= 2048, else 2048; halved (while it divides C, down to 256 channels)
+// until the grid holds two waves -- the deep 14x14 / 7x7 BNs have few rows,
+// so rows alone gave them 25-98 blocks on 148 SMs.  0 = no valid chunking.
+int reduce_chunk(int C, int blocks) {
+  int cw = C <= 2048 ? C : 2048;
+  if (C % cw) return 0;
+  while ((long)blocks * (C / cw) < 2 * 148 && cw >= 512 && (cw / 2) % 8 == 0 && C % (cw / 2) == 0) cw /= 2;
+  return cw;
+}
+
 // Timing experiments only (results become wrong): RFK_ABLATE bit mask skips
 // kernels to bound what removing them could save -- 1 forward BN finalize,
 // 2 backward BN finalize, 4 backward BN reduce, 8 forward BN apply,
@@ -1573,9 +1584,11 @@ int colstats_blocks(long M) {
 }
 
 cudaError_t colstats(const __nv_bfloat16* x, long M, int C, float* partials, int blocks, cudaStream_t st) {
-  if (C % 8 || (C > 2048 && C % 2048)) return cudaErrorInvalidValue;
-  dim3 grid(blocks, (C + 2047) / 2048);
-  RFK_CHECK_LAUNCH(launch_k(colstats_kernel<0>, grid, kThreads, 0, st, x, M, C, rows_per_block_for(M, blocks), partials));
+  const int cw = reduce_chunk(C, blocks);
+  if (C % 8 || cw == 0) return cudaErrorInvalidValue;
+  dim3 grid(blocks, C / cw);
+  RFK_CHECK_LAUNCH(launch_k(colstats_kernel<0>, grid, kThreads, 0, st, x, M, C, rows_per_block_for(M, blocks), partials,
+                            cw));
   return cudaGetLastError();
 }
 
@@ -1620,10 +1633,11 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
                         const float* shift, long M, int C, float* partials, int blocks, float* coef, float* dgamma,
                         float* dbeta, __nv_bfloat16* dy, bool acc_dy, __nv_bfloat16* dskip, bool acc_dskip,
                         cudaStream_t st) {
-  if (C % 8 || (C > 2048 && C % 2048) || mask_mode < 0 || mask_mode > 2) return cudaErrorInvalidValue;
+  const int cw = reduce_chunk(C, blocks);
+  if (C % 8 || cw == 0 || mask_mode < 0 || mask_mode > 2) return cudaErrorInvalidValue;
   const long nvec = M * C / 8;
   if (nvec >= (1L << 31)) return cudaErrorInvalidValue;
-  dim3 grid(blocks, (C + 2047) / 2048);
+  dim3 grid(blocks, C / cw);
   const long rpb = rows_per_block_for(M, blocks);
   // residual add whose skip gradient is written (not accumulated): the
   // reduction stores g there, and the apply reads g back (7 passes over the
@@ -1631,9 +1645,9 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
   const bool g_early = mask_mode == 2 && dskip && !acc_dskip && !g_early_off();
   __nv_bfloat16* gout = g_early ? dskip : nullptr;
   if (!(ablate() & 4)) switch (mask_mode) {
-    case 0: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<0>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout)); break;
-    case 1: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<1>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout)); break;
-    default: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<2>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout));
+    case 0: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<0>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout, cw)); break;
+    case 1: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<1>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout, cw)); break;
+    default: RFK_CHECK_LAUNCH(launch_k(bn_bwd_reduce_kernel<2>, grid, kThreads, 0, st, y, dout, out, mean, scale, shift, M, C, rpb, partials, gout, cw));
   }
   if (!(ablate() & 2)) RFK_CHECK_LAUNCH(launch_k(bn_bwd_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, partials, blocks, C, (float)M, gamma, mean, invstd,
                                                                 dgamma, dbeta, coef));

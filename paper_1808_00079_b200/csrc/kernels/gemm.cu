@@ -454,39 +454,53 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             *reinterpret_cast<uint4*>(gb + lane * 64 + sw * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
           }
           __syncwarp();
-#pragma unroll 1
-          for (int it = 0; it < 4; ++it) {
-            const uint32_t row = it * 8 + (lane >> 2), chunk = lane & 3;
-            const uint4 val = *reinterpret_cast<const uint4*>(gb + row * 64 + ((chunk ^ ((row >> 1) & 3u)) * 16));
-            const int mr = my + (int)row;
-            if (mr < p.M && (full_cols || col0 + (int)chunk * 8 < p.N)) {
-              long orow = mr;
-              if (p.remap) {
-                const int q = mr % p.rQ, tt = mr / p.rQ, pp = tt % p.rP, nn = tt / p.rP;
-                orow = (long)nn * p.rH * p.rW + (long)(pp * p.rsh) * p.rW + (long)q * p.rsw;
-              }
-              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + (long)tc.z * p.split_stride +
-                                   orow * p.ldc + col0 + chunk * 8;
-              const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&val);
-              if (full_cols || col0 + (int)chunk * 8 + 8 <= p.N) {
-                uint4 o = val;
-                if (p.accumulate_out) {
-                  const uint4 prev = *reinterpret_cast<const uint4*>(dst);
-                  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&val);
-                  const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&prev);
-                  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+          // four 8-row passes: addresses and (accumulating) the previous
+          // values of all four are loaded before any store, so the scattered
+          // read-modify-write of a remapped output costs one memory round
+          // trip per chunk, not four
+          const uint32_t chunk = lane & 3;
+          __nv_bfloat16* dsts[4];
+          uint4 vals[4], prevs[4];
+          bool oks[4], fulls[4];
 #pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    const float2 fa = __bfloat1622float2(a2[e]), fb = __bfloat1622float2(b2[e]);
-                    o2[e] = __floats2bfloat162_rn(fa.x + fb.x, fa.y + fb.y);
-                  }
+          for (int it = 0; it < 4; ++it) {
+            const uint32_t row = it * 8 + (lane >> 2);
+            vals[it] = *reinterpret_cast<const uint4*>(gb + row * 64 + ((chunk ^ ((row >> 1) & 3u)) * 16));
+            const int mr = my + (int)row;
+            oks[it] = mr < p.M && (full_cols || col0 + (int)chunk * 8 < p.N);
+            fulls[it] = full_cols || col0 + (int)chunk * 8 + 8 <= p.N;
+            long orow = mr;
+            if (p.remap) {
+              const int q = mr % p.rQ, tt = mr / p.rQ, pp = tt % p.rP, nn = tt / p.rP;
+              orow = (long)nn * p.rH * p.rW + (long)(pp * p.rsh) * p.rW + (long)q * p.rsw;
+            }
+            dsts[it] = reinterpret_cast<__nv_bfloat16*>(p.out) + (long)tc.z * p.split_stride + orow * p.ldc + col0 +
+                       chunk * 8;
+            if (p.accumulate_out && oks[it] && fulls[it]) prevs[it] = *reinterpret_cast<const uint4*>(dsts[it]);
+          }
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            if (!oks[it]) continue;
+            __nv_bfloat16* dst = dsts[it];
+            const uint4 val = vals[it];
+            const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&val);
+            if (fulls[it]) {
+              uint4 o = val;
+              if (p.accumulate_out) {
+                const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&val);
+                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&prevs[it]);
+                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 fa = __bfloat1622float2(a2[e]), fb = __bfloat1622float2(b2[e]);
+                  o2[e] = __floats2bfloat162_rn(fa.x + fb.x, fa.y + fb.y);
                 }
-                *reinterpret_cast<uint4*>(dst) = o;
-              } else {
-                for (int e = 0; e < 8 && col0 + (int)chunk * 8 + e < p.N; ++e)
-                  dst[e] = p.accumulate_out ? __float2bfloat16_rn(__bfloat162float(dst[e]) + __bfloat162float(vb[e]))
-                                            : vb[e];
               }
+              *reinterpret_cast<uint4*>(dst) = o;
+            } else {
+              for (int e = 0; e < 8 && col0 + (int)chunk * 8 + e < p.N; ++e)
+                dst[e] = p.accumulate_out ? __float2bfloat16_rn(__bfloat162float(dst[e]) + __bfloat162float(vb[e]))
+                                          : vb[e];
             }
           }
           sbuf = gb;

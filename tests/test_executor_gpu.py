@@ -29,7 +29,11 @@ pytestmark = pytest.mark.gpu
 
 CASES = [("chain8", 4, 32, 10, 1.0), ("resnet18", 4, 64, 10, 1.0), ("resnet50", 2, 64, 16, 1.0),
          ("resnet50", 2, 64, 16, 0.0), ("densenet_tiny", 4, 32, 10, 1.0), ("vgg11", 4, 32, 10, 1.0),
-         ("alexnet", 4, 64, 10, 1.0), ("inception_v3", 2, 139, 10, 1.0)]
+         ("alexnet", 4, 64, 10, 1.0), ("inception_v3_m3", 4, 139, 10, 1.0)]
+# (the full Inception-v3 at batch 2 / 139^2 is chaotic at init: rounding-level
+# differences grow ~1.5x per mixed block, see tools/diag_forward_drift.py and
+# DESIGN.md "Parity"; its per-op parity is in test_ops_teacher_forced_gpu.py
+# and its whole step at 4 x 299^2 in test_baseline_shapes_gpu.py)
 
 
 def _goyal(net, seed):

@@ -129,6 +129,29 @@ def cases():
     out.append(("floor: 148 tiles, K=64", Mt, 128, 64,
                 dict(M=Mt, N=128, K=64, a_kind=K.KMAJOR, a=at.data_ptr(), a_ld=64, b_kind=K.KMAJOR, b=bt.data_ptr(),
                      b_ld=64, out=ot.data_ptr(), ldc=128, splits=1), (at, bt, ot), {}))
+    # 1x1 dgrad shape of layer2 (dY 25088x512 K-major, W MN-major): the
+    # largest gap to its roofline in the step breakdown; same with K-major B
+    a5 = bf(25088, 512)
+    w5 = bf(512, 256)   # [Cout=K][Cin=N]: MN-major B
+    w5k = bf(256, 512)  # K-major B
+    o5 = bf(25088, 256)
+    for bn_ in (128, 256):
+        out.append((f"1x1 dgrad 25088x256x512 MN-major B bn={bn_}", 25088, 256, 512,
+                    dict(M=25088, N=256, K=512, a_kind=K.KMAJOR, a=a5.data_ptr(), a_ld=512, b_kind=K.MNMAJOR,
+                         b=w5.data_ptr(), b_ld=256, out=o5.data_ptr(), ldc=256, splits=1), (a5, w5, o5),
+                    {"b_extent": 256, "block_n": bn_}))
+        out.append((f"1x1 25088x256x512 K-major B bn={bn_}", 25088, 256, 512,
+                    dict(M=25088, N=256, K=512, a_kind=K.KMAJOR, a=a5.data_ptr(), a_ld=512, b_kind=K.KMAJOR,
+                         b=w5k.data_ptr(), b_ld=512, out=o5.data_ptr(), ldc=256, splits=1), (a5, w5k, o5),
+                    {"block_n": bn_}))
+    # 1x1 stride-2 dgrad (layer2.0 downsample): rows scattered to the even
+    # pixels of 56x56 and accumulated into the block-input gradient
+    o6 = bf(32 * 56 * 56, 256)
+    for acc in (0, 1):
+        out.append((f"1x1/2 dgrad remap 25088x256x512 acc={acc}", 25088, 256, 512,
+                    dict(M=25088, N=256, K=512, a_kind=K.KMAJOR, a=a5.data_ptr(), a_ld=512, b_kind=K.MNMAJOR,
+                         b=w5.data_ptr(), b_ld=256, out=o6.data_ptr(), ldc=256, splits=1, remap=1, rP=28, rQ=28,
+                         rH=56, rW=56, rsh=2, rsw=2, accumulate_out=acc), (a5, w5, o6), {"b_extent": 256}))
     # large square 2-D GEMM: the engine's best case
     S = 8192
     a4, b4, o4 = bf(S, S), bf(S, S), bf(S, S)

@@ -1,6 +1,7 @@
 // Network building, planning (host planner on the tensor graph), the
 // re-forward schedule and the arena layouts.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <functional>
 #include <map>
@@ -785,9 +786,6 @@ void Net::layout() {
         op.im2col_imgs = (int)std::max(1L, std::min((long)y.N, im2col_chunk_bytes() / per_img));
         ws_im2col_ = std::max(ws_im2col_, align_up(op.im2col_imgs * per_img));
       }
-      if (op.stride > 1 && op.R > 1)
-        ws_zero_ = std::max(ws_zero_, align_up((long)x.N * (x.H - op.R + 1 + 2 * op.pad) *
-                                               (x.W - op.S + 1 + 2 * op.pad_w) * op.cout * 2));
       const long kw = op.explicit_im2col ? op.kpad : (long)op.R * op.S * op.cpad;
       op.wg_bn = kw <= 64 ? 64 : (kw <= 128 ? 128 : 256);
       const long tiles = ((op.cout + 127) / 128) * ((kw + op.wg_bn - 1) / op.wg_bn);
@@ -816,6 +814,13 @@ void Net::layout() {
         }
       }
       op.dg_subpixel = subpixel_ok(op, x);
+      // zero-insertion buffer of a strided k x k data gradient: only where the
+      // dgrad exists (not for a conv on the network input, e.g. the stem --
+      // 205 MB at batch 32 otherwise) and does not use the sub-pixel classes
+      if (op.stride > 1 && !(op.R == 1 && op.S == 1) && op.in[0] != input_t_ && !op.explicit_im2col &&
+          !op.dg_subpixel)
+        ws_zero_ = std::max(ws_zero_, align_up((long)x.N * (x.H - op.R + 1 + 2 * op.pad) *
+                                               (x.W - op.S + 1 + 2 * op.pad_w) * op.cout * 2));
       const bool dgrad_taps = !op.dg_subpixel && op.in[0] != input_t_ && !op.explicit_im2col && !(op.R == 1 && op.S == 1 &&
                                                                                 op.pad == 0 && op.pad_w == 0);
       if (dgrad_taps && op.cin % 4 == 0 && op.cin / 4 <= 256) {
@@ -910,6 +915,10 @@ void Net::layout() {
   ws_counters_ = 0;
   rep_.workspace_bytes =
       ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_ + ws_counters_ + ws_dsplit_;
+  if (std::getenv("RFK_TRACE_WS"))
+    std::fprintf(stderr, "workspace MB: im2col %.1f partials %.1f zero/argmax %.1f wgrad-split %.1f stats %.1f misc %.1f "
+                 "fprop/dgrad-split %.1f\n", ws_im2col_ / 1e6, ws_partials_ / 1e6, ws_zero_ / 1e6, ws_split_ / 1e6,
+                 ws_stats_ / 1e6, ws_misc_ / 1e6, ws_dsplit_ / 1e6);
   rep_.param_bytes = n_params_ * 4 * 3;
   rep_.state_bytes = n_state_ * 4;
 }

@@ -436,7 +436,8 @@ def main():
                        # every cudaMalloc of the net (arena + guard band, gradient arena,
                        # workspace, parameters / gradients / momentum / bf16 copies, BN state,
                        # input and staging buffers), re-forward vs store-all
-                       "device_bytes": dev_bytes, "store_all_device_bytes": sa_device,
+                       "device_bytes": dev_bytes, "device_peak_bytes": dev_bytes,
+                       "store_all_device_bytes": sa_device,
                        "device_cut_percent": (100.0 * (1 - dev_bytes / sa_device)) if sa_device else None},
             "store_all": {"value": sa_value, "unit": "imgs/s"},
             "overhead_vs_store_all": overhead,

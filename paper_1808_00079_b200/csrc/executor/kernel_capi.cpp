@@ -39,6 +39,13 @@ extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
     d.b_tap_dr = a->b_tap_dr;
     d.b_tap_ds = a->b_tap_ds;
   }
+  d.stats_bwd = a->stats_bwd != 0;
+  d.replay = a->replay != 0;
+  d.bs_y = a->bs_y;
+  d.bs_ldy = a->bs_ldy;
+  d.bs_mean = a->bs_mean;
+  d.bs_scale = a->bs_scale;
+  d.bs_shift = a->bs_shift;
   cudaError_t e = rfk::gemm_launch(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     rfexec::set_last_error(std::string("rfx_gemm: ") + cudaGetErrorString(e));

@@ -62,6 +62,17 @@ struct alignas(64) KParams {
   const float* bn_scale;
   const float* bn_shift;
   int bn_relu, fuse_bn;
+  // BN backward statistics in the epilogue (stats_bwd): the output is dout of
+  // a BN+ReLU's output; it is stored masked (g = dout * [y*scale+shift > 0])
+  // and the statistics rows hold sum g and sum g*(y - mean) per column.
+  // replay: no GEMM -- the epilogue re-reads the stored output instead of TMEM
+  // (same tiles, same CTAs, same arithmetic: bit-identical rows).
+  int stats_bwd, replay;
+  const __nv_bfloat16* bs_y;
+  long bs_ldy;
+  const float* bs_mean;
+  const float* bs_scale;
+  const float* bs_shift;
   int experiment;  // tuning only: 2 drop the output, 3 also skip TMEM loads, 4 also skip the MMAs,
                   // 5 skip the statistics smem reads, 6 skip the statistics accumulation
 };
@@ -157,8 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const int total = p.m_tiles * p.n_tiles * p.splits;
 
   if (warp == 0 && elect_one()) {
-    tma_prefetch(&p.ta);
-    tma_prefetch(&p.tb);
+    if (!p.replay) {
+      tma_prefetch(&p.ta);
+      tma_prefetch(&p.tb);
+    }
     if (p.out_mode) tma_prefetch(&p.tc);
     if (p.fuse_bn) tma_prefetch(&p.tc2);
     for (int s = 0; s < nst; ++s) {
@@ -182,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
-    if (elect_one()) {
+    if (elect_one() && !p.replay) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -254,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+    for (int t = blockIdx.x; t < (p.replay ? 0 : total); t += gridDim.x, ++local) {
       const TileCoord tc = tile_coord(p, t, BN);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -359,22 +372,39 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (cur_nt >= 0) flush_stats(cur_nt);
         cur_nt = tc.n0 / BN;
       }
-      mbar_wait(&acc_full[acc], acc_phase);
-      tc_fence_after();
+      if (!p.replay) {
+        mbar_wait(&acc_full[acc], acc_phase);
+        tc_fence_after();
+      }
       const int my = tc.m0 + (int)(quarter * 32);
       const int m = my + (int)lane;
       const bool row_ok = m < p.M;
 #pragma unroll 1
       for (int c0 = (int)half * 32; c0 < BN; c0 += 64) {
         uint32_t r[32];
-        if (!empty_k && (p.experiment < 3 || p.experiment > 4)) {
+        if (p.replay) {
+          // the stored bf16 output of this lane's row, 32 columns
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 u = make_uint4(0u, 0u, 0u, 0u);
+            if (row_ok && tc.n0 + c0 + 8 * j < p.N)
+              u = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.out) +
+                                                       (long)m * p.ldc + tc.n0 + c0 + 8 * j));
+            const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              r[8 * j + 2 * e] = uw[e] << 16;              // low bf16 -> fp32 bits
+              r[8 * j + 2 * e + 1] = uw[e] & 0xffff0000u;  // high bf16 -> fp32 bits
+            }
+          }
+        } else if (!empty_k && (p.experiment < 3 || p.experiment > 4)) {
           tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
           tmem_ld_wait();
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
-        if (c0 + 64 >= BN) {
+        if (c0 + 64 >= BN && !p.replay) {
           // this warp's last chunk of the accumulator is in registers: hand it back
           tc_fence_before();
           __syncwarp();
@@ -414,8 +444,45 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         uint32_t w[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) w[i] = row_ok ? pack_bf16(v[2 * i], v[2 * i + 1]) : 0u;
+        if (p.stats_bwd && row_ok) {
+          // g = dout * [y * scale + shift > 0] (the BN+ReLU backward's mask,
+          // same expression as bn_bwd_apply MODE 1); g is dout with lanes
+          // zeroed, so it is exact in bf16 and is what gets stored
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int c = col0 + 8 * j;
+            if (c >= p.N) break;
+            const uint4 yu = __ldg(reinterpret_cast<const uint4*>(p.bs_y + (long)m * p.bs_ldy + c));
+            const float4 sc0 = __ldg(reinterpret_cast<const float4*>(p.bs_scale + c));
+            const float4 sc1 = __ldg(reinterpret_cast<const float4*>(p.bs_scale + c + 4));
+            const float4 sh0 = __ldg(reinterpret_cast<const float4*>(p.bs_shift + c));
+            const float4 sh1 = __ldg(reinterpret_cast<const float4*>(p.bs_shift + c + 4));
+            const float sc[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
+            const float sh[8] = {sh0.x, sh0.y, sh0.z, sh0.w, sh1.x, sh1.y, sh1.z, sh1.w};
+            const uint32_t yw[4] = {yu.x, yu.y, yu.z, yu.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float ylo = __uint_as_float(yw[e] << 16), yhi = __uint_as_float(yw[e] & 0xffff0000u);
+              uint32_t g = w[4 * j + e];
+              if (!(fmaf(ylo, sc[2 * e], sh[2 * e]) > 0.f)) g &= 0xffff0000u;
+              if (!(fmaf(yhi, sc[2 * e + 1], sh[2 * e + 1]) > 0.f)) g &= 0x0000ffffu;
+              w[4 * j + e] = g;
+            }
+          }
+        }
         const uint8_t* sbuf;
-        if (mode != 0) {
+        if (p.replay) {
+          // statistics only: stage (same layout as the store paths), no write
+          uint8_t* gb = stg;
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t sw = (uint32_t)j ^ ((lane >> 1) & 3u);
+            *reinterpret_cast<uint4*>(gb + lane * 64 + sw * 16) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+          }
+          __syncwarp();
+          sbuf = gb;
+        } else if (mode != 0) {
           sbuf = stg + buf * 2048;
           tma_out(w, col0, my, tc.z);
           if (p.fuse_bn) {
@@ -513,6 +580,31 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           // 64-byte halves of the bank space, so the reads are conflict-free.
           const uint32_t cp = lane & 15, par = lane >> 4;
           float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
+          if (p.stats_bwd) {
+            // sum g and sum g * (y - mean) over the chunk's rows (rows past M
+            // and columns past N were staged as g = 0)
+            const int c = col0 + 2 * (int)cp;
+            const bool col_ok = c < p.N;
+            const float2 mu = col_ok ? __ldg(reinterpret_cast<const float2*>(p.bs_mean + c)) : make_float2(0.f, 0.f);
+            uint32_t yv[16];
+#pragma unroll
+            for (int rr = 0; rr < 16; ++rr) {
+              const int mr = my + 2 * rr + (int)par;
+              yv[rr] = (col_ok && mr < p.M) ? __ldg(reinterpret_cast<const unsigned int*>(p.bs_y + (long)mr * p.bs_ldy + c))
+                                            : 0u;
+            }
+#pragma unroll
+            for (int rr = 0; rr < 16; ++rr) {
+              const uint32_t row = 2 * rr + par;
+              const uint32_t off = row * 64 + (((cp >> 2) ^ ((row >> 1) & 3u)) * 16) + (cp & 3) * 4;
+              const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sbuf + off));
+              const float ylo = __uint_as_float(yv[rr] << 16), yhi = __uint_as_float(yv[rr] & 0xffff0000u);
+              s0 += g.x;
+              s1 += g.y;
+              q0 = fmaf(g.x, ylo - mu.x, q0);
+              q1 = fmaf(g.y, yhi - mu.y, q1);
+            }
+          } else {
 #pragma unroll
           for (int rr = 0; rr < (p.experiment == 5 ? 0 : 16); ++rr) {
             const uint32_t row = 2 * rr + par;
@@ -522,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             s1 += f.y;
             q0 = fmaf(f.x, f.x, q0);
             q1 = fmaf(f.y, f.y, q1);
+          }
           }
           s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
           s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
@@ -633,6 +726,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     return e ? std::atoi(e) : 0;
   }();
   if (force_stages >= 2) kp.stages = std::min(force_stages, C::kStages);
+  if (kp.replay) kp.stages = 2;  // no operand ring in a statistics replay
   static const int experiment = [] {
     const char* e = std::getenv("RFK_GEMM_EXPERIMENT");  // tuning experiments only
     return e ? std::atoi(e) : 0;
@@ -693,12 +787,38 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   const int bn = gemm_block_n(d);
   if (bn != 64 && bn != 128 && bn != 256) return cudaErrorInvalidValue;
   if (d.stats && d.out_f32) return cudaErrorInvalidValue;  // statistics are of the stored bf16 values
+  if (d.stats_bwd && (!d.stats || !d.bs_y || !d.bs_mean || !d.bs_scale || !d.bs_shift || d.splits > 1 || d.remap ||
+                      d.accumulate_out || d.bn_out || d.N % 8 || d.bs_ldy % 8 ||
+                      (reinterpret_cast<uintptr_t>(d.bs_y) & 15) || (reinterpret_cast<uintptr_t>(d.out) & 15)))
+    return cudaErrorInvalidValue;
+  if (d.replay && (!d.stats_bwd || d.block_n == 0)) return cudaErrorInvalidValue;
 
   KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   kp.M = d.M;
   kp.N = d.N;
   kp.K = d.K;
+  kp.stats_bwd = d.stats_bwd ? 1 : 0;
+  kp.replay = d.replay ? 1 : 0;
+  kp.bs_y = static_cast<const __nv_bfloat16*>(d.bs_y);
+  kp.bs_ldy = d.bs_ldy;
+  kp.bs_mean = d.bs_mean;
+  kp.bs_scale = d.bs_scale;
+  kp.bs_shift = d.bs_shift;
+  if (d.replay) {
+    // statistics replay: no operands, no output write; same tile space
+    kp.num_kb = 1;
+    kp.kb_per_split = 1;
+    kp.out = d.out;
+    kp.ldc = d.ldc;
+    kp.stats = d.stats;
+    const int m_tiles = gemm_m_tiles(d), n_tiles = (d.N + bn - 1) / bn;
+    switch (bn) {
+      case 64: return launch_bn<64>(kp, m_tiles, n_tiles, 1, 0, stream);
+      case 128: return launch_bn<128>(kp, m_tiles, n_tiles, 1, 0, stream);
+      default: return launch_bn<256>(kp, m_tiles, n_tiles, 1, 0, stream);
+    }
+  }
   kp.a_kind = (int)d.a_kind;
   kp.b_kind = (int)d.b_kind;
   const ConvGeom* geo = nullptr;

@@ -73,6 +73,18 @@ struct GemmDesc {
   // persistent grid cap (0 = one CTA per SM): leaves SMs free for NCCL kernels
   // on a side stream while gradient buckets are in flight
   int max_ctas = 0;
+  // BN backward statistics (with `stats`, bf16 output = dout of a BN+ReLU
+  // output): store g = dout * [bs_y * bs_scale + bs_shift > 0] and write rows
+  // of (sum g, sum g * (bs_y - bs_mean)) per column instead of (sum, sum^2).
+  // replay: no GEMM; the epilogue re-reads `out` and emits the same rows a
+  // fused launch of the same M / N / block_n would (bit-identical).
+  bool stats_bwd = false;
+  bool replay = false;
+  const void* bs_y = nullptr;  // bf16 [M][bs_ldy]: the BN input
+  long bs_ldy = 0;
+  const float* bs_mean = nullptr;
+  const float* bs_scale = nullptr;
+  const float* bs_shift = nullptr;
 };
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream);

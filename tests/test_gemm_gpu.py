@@ -388,3 +388,76 @@ def test_conv_wgrad_multiwave(splits):
     torch.cuda.synchronize()
     got = out.sum(0).reshape(Co, R, R, 64)[..., :Ci].permute(0, 3, 1, 2)
     _check(got, ref)
+
+
+def _bwd_stats_case(kind, M, N, Kd, bn, seed):
+    """A data-gradient GEMM whose output is dout of a BN+ReLU output."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    y = (torch.randn(M, N, generator=g) * 2 + 0.3).to(torch.bfloat16).to(dev)   # the BN input
+    mean = (torch.randn(N, generator=g) * 0.1).to(dev)
+    scale = (torch.rand(N, generator=g) + 0.5).to(dev)
+    shift = (torch.randn(N, generator=g) * 0.5).to(dev)
+    a = _bf(M, Kd, seed=seed + 1)
+    if kind == "kmajor":
+        b = _bf(N, Kd, seed=seed + 2)
+        ref = a.float() @ b.float().t()
+        kw = dict(b_kind=K.KMAJOR, b=b.data_ptr(), b_ld=Kd)
+        keep = (a, b)
+    else:  # 1x1 dgrad: W [Cout=K][Cin=N] MN-major
+        wt = _bf(Kd, N, seed=seed + 2)
+        ref = a.float() @ wt.float()
+        kw = dict(b_kind=K.MNMAJOR, b=wt.data_ptr(), b_ld=N)
+        keep = (a, wt)
+    return y, mean, scale, shift, a, ref, kw, keep
+
+
+@pytest.mark.parametrize("kind,M,N,Kd,bn", [("kmajor", 6272, 256, 512, 128), ("mnmajor", 25088, 128, 512, 64),
+                                            ("mnmajor", 1000, 72, 256, 64), ("kmajor", 100352, 64, 256, 64)])
+def test_bn_backward_statistics_epilogue_and_replay(kind, M, N, Kd, bn):
+    """The dgrad GEMM epilogue stores g = dout * [y*scale + shift > 0] and
+    emits per-CTA rows of (sum g, sum g*(y - mean)); a replay launch (no GEMM,
+    the epilogue re-reads the stored output) writes bit-identical rows -- so a
+    BN backward gets the same statistics whether or not its input was resident
+    when the dgrad ran."""
+    y, mean, scale, shift, a, ref, kw, keep = _bwd_stats_case(kind, M, N, Kd, bn, seed=40)
+    out = torch.zeros(M, N, device=dev, dtype=torch.bfloat16)
+    rows = torch.full((160, 2, N), 0.0, device=dev)
+    args = K.GemmArgs(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, out=out.data_ptr(), ldc=N,
+                      stats=rows.data_ptr(), splits=1, block_n=bn, stats_bwd=1, bs_y=y.data_ptr(), bs_ldy=N,
+                      bs_mean=mean.data_ptr(), bs_scale=scale.data_ptr(), bs_shift=shift.data_ptr(),
+                      b_extent=N if kind == "mnmajor" else 0, **kw)
+    K.gemm(args)
+    torch.cuda.synchronize()
+    mask = (y.float() * scale + shift) > 0
+    # stored output: the masked dout (one bf16 rounding of the GEMM)
+    _check(out, torch.where(mask, ref, torch.zeros_like(ref)))
+    gm = out.float().double()  # exactly what the statistics sum
+    s_ref = gm.sum(0)
+    q_ref = (gm * (y.double() - mean.double())).sum(0)
+    s, q = rows[:, 0].double().sum(0), rows[:, 1].double().sum(0)
+    assert torch.allclose(s, s_ref, rtol=1e-5, atol=1e-3 * gm.abs().sum(0).max().item() / M), (s - s_ref).abs().max()
+    assert torch.allclose(q, q_ref, rtol=1e-4, atol=1e-5 * (gm * (y.double() - mean.double())).abs().sum(0).max().item())
+    # replay over the stored output: bit-identical rows
+    rows2 = torch.full((160, 2, N), 0.0, device=dev)
+    args2 = K.GemmArgs(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=0, a_ld=Kd, out=out.data_ptr(), ldc=N,
+                       stats=rows2.data_ptr(), splits=1, block_n=bn, stats_bwd=1, replay=1, bs_y=y.data_ptr(),
+                       bs_ldy=N, bs_mean=mean.data_ptr(), bs_scale=scale.data_ptr(), bs_shift=shift.data_ptr())
+    before = out.clone()
+    K.gemm(args2)
+    torch.cuda.synchronize()
+    assert torch.equal(rows2, rows)
+    assert torch.equal(out, before)  # the replay writes nothing
+    # replay over an UNMASKED dout (produced by a path without the fused
+    # epilogue) gives the same rows too: the mask is idempotent
+    out_unmasked = torch.zeros(M, N, device=dev, dtype=torch.bfloat16)
+    plain = K.GemmArgs(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, out=out_unmasked.data_ptr(), ldc=N,
+                       splits=1, block_n=bn, b_extent=N if kind == "mnmajor" else 0, **kw)
+    K.gemm(plain)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.where(mask, out_unmasked, torch.zeros_like(out_unmasked)), out)
+    rows3 = torch.full((160, 2, N), 0.0, device=dev)
+    args2.out = out_unmasked.data_ptr()
+    args2.stats = rows3.data_ptr()
+    K.gemm(args2)
+    torch.cuda.synchronize()
+    assert torch.equal(rows3, rows)

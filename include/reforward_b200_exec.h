@@ -43,9 +43,9 @@ typedef struct rfx_gemm_args {
   int32_t band;                      /* stride-1 im2col A: use the shifted-band kernel when eligible */
   int32_t b_tap_map;                 /* kind 4: nonzero = weight tap of A tap (r, s) is base - r*dr - s*ds */
   int32_t b_tap_base, b_tap_dr, b_tap_ds;  /* (sub-pixel dgrad classes); zero = flipped full filter */
-  /* BN+ReLU backward statistics in the epilogue (with `stats`): out is stored
-   * as g = dout * [y*scale + shift > 0]; stats rows [CTA][2][N] hold sum g and
-   * sum g*(y - mean).  replay: no GEMM, the epilogue re-reads `out` (a fixed
+  /* BN+ReLU backward statistics in the epilogue (with `stats`): out (dout of
+   * the BN+ReLU output) is stored as is; stats rows [CTA][2][N] hold sum g and
+   * sum g*(y - mean), g = dout * [y*scale + shift > 0].  replay: no GEMM, the epilogue re-reads `out` (a fixed
    * block_n is required) and writes bit-identical rows. */
   int32_t stats_bwd, replay;
   const void* bs_y;                  /* bf16 [M][bs_ldy], the BN input */

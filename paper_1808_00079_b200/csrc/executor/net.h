@@ -85,6 +85,16 @@ struct Op {
   int fused_bn = -1;               // conv: BN op whose re-forward runs in this conv's epilogue
   bool reforward_in_producer = false;  // BN: re-forwarded by its producing conv's epilogue
   int bn_gather = -1;              // BN over a concatenation: index of its statistics-gather table
+  // BN+ReLU backward statistics from rows (sum g, sum g*(y-mean)) written by
+  // the consumer conv's dgrad epilogue when the BN input is resident at that
+  // point (bstat_fused), else by a replay over the stored dout at the BN's
+  // backward -- same tiles, same CTAs, so the rows are plan-independent
+  bool bstat = false;              // BN: backward statistics from rows
+  bool bstat_resident = false;     // BN: input resident at the consumer conv's backward (schedule)
+  bool bstat_fused = false;        // BN: rows produced by the consumer conv's dgrad epilogue
+  long bstat_off = -1;             // BN: its rows slot in the statistics workspace (floats)
+  int bstat_bn = 0;                // BN: tile width of the rows (the dgrad's, fixed)
+  int bstat_src = -1;              // conv: BN whose rows its dgrad epilogue produces
   // pool
   int k = 1;
   // classifier / linear
@@ -208,6 +218,7 @@ class Net {
   // host-only layout conversion: canonical <-> the slice [param_offset(i),
   // + param_count(i)) of the flat fp32 parameter / gradient buffers
   void pack_param(int i, const float* canonical, float* flat_slice) const;
+  float* ws_stats_base() const;  // BN statistics rows region of the workspace
   void unpack_param(int i, const float* flat_slice, float* canonical) const;
   long param_offset(int i) const { return params_.at(i).offset; }
   long param_count(int i) const { return params_.at(i).count; }

@@ -432,6 +432,7 @@ void Net::autotune(cudaStream_t st) {
       // slot: each width maps tiles to different CTA rows, and the finalize
       // sums every row (rows a CTA never touches are assumed zero)
       dc.stats = nullptr;
+      dc.stats_bwd = false;
       cudaGraphExec_t g = capture(
           [&](cudaStream_t s) {
             for (int i = 0; i < 3; ++i) check(rfk::gemm_launch(dc, s), "gemm");
@@ -495,6 +496,10 @@ void Net::gemm(const rfk::GemmDesc& d0, cudaStream_t st) {
   }
   if (tracing_) gemm_trace_.push_back({d, gemm_launch_flops(d, trace_flops_), gemm_algorithmic_bytes(d)});
   check(rfk::gemm_launch(d, st), "gemm");
+}
+
+float* Net::ws_stats_base() const {
+  return reinterpret_cast<float*>(d_ws_ + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_);
 }
 
 // ============================================================ op dispatch
@@ -892,6 +897,22 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
                                         (int)kStatRows, st),
                 "reduce_splits_bf16");
         } else if (!op.dg_subpixel) {
+          if (op.bstat_src >= 0) {
+            // this dgrad's output is dout of a BN+ReLU whose input is
+            // resident: store g and emit that BN's backward statistics rows
+            const Op& bn = ops_[op.bstat_src];
+            const BNState& b = bns_[bn.bn];
+            if (d.remap || d.accumulate_out || d.splits > 1) throw std::runtime_error("bstat dgrad is not a plain launch");
+            d.stats = ws_stats_base() + bn.bstat_off;
+            d.stats_bwd = true;
+            d.block_n = bn.bstat_bn;
+            d.band = false;
+            d.bs_y = tptr(bn.in[0]);
+            d.bs_ldy = tensors_[bn.in[0]].C;
+            d.bs_mean = d_state_ + b.mean;
+            d.bs_scale = d_state_ + b.scale;
+            d.bs_shift = d_state_ + b.shift;
+          }
           gemm(d, st);
         }
       }
@@ -978,6 +999,35 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       float* S = d_state_;
       const bool add = op.kind == OpKind::BNAddReLU;
       const int mode = add ? 2 : (op.k == 1 ? 1 : 0);
+      if (op.bstat) {
+        // statistics rows from the consumer conv's dgrad epilogue, or a replay
+        // over the stored dout with the same tiles (bit-identical rows)
+        float* rows = ws_stats_base() + op.bstat_off;
+        if (!op.bstat_fused) {
+          rfk::GemmDesc r;
+          r.M = (int)y.rows();
+          r.N = y.C;
+          r.K = 0;
+          r.out = gptr(op.out);
+          r.ldc = y.C;
+          r.stats = rows;
+          r.stats_bwd = true;
+          r.replay = true;
+          r.block_n = op.bstat_bn;
+          r.bs_y = tb(op.in[0]);
+          r.bs_ldy = y.C;
+          r.bs_mean = S + b.mean;
+          r.bs_scale = S + b.scale;
+          r.bs_shift = S + b.shift;
+          check(rfk::gemm_launch(r, st), "bstat replay");  // not a GEMM: kept out of the GEMM trace
+        }
+        check(rfk::bn_backward_from_rows(tb(op.in[0]), gptr(op.out), d_param_ + params_[op.w_param].offset,
+                                         S + b.mean, S + b.invstd, S + b.scale, S + b.shift, y.rows(), y.C, rows,
+                                         (int)kStatRows, S + b.coef, d_grad_ + params_[op.w_param].offset,
+                                         d_grad_ + params_[op.b_param].offset, gptr(op.in[0]), acc(0), st),
+              "bn_backward_from_rows");
+        break;
+      }
       const int blocks = rfk::colstats_blocks(y.rows());
       __nv_bfloat16* dskip = add ? gptr(op.in[1]) : nullptr;
       check(rfk::bn_backward(tb(op.in[0]), gptr(op.out), add ? tb(op.out) : nullptr, mode,
@@ -1563,6 +1613,7 @@ double Net::gemm_try(int idx, int block_n, int splits, int iters, cudaStream_t s
   d.block_n = block_n;
   d.splits = splits < 1 ? 1 : splits;
   d.stats = nullptr;
+  d.stats_bwd = false;
   d.bias = nullptr;
   d.remap = false;
   d.accumulate_out = false;

@@ -392,6 +392,7 @@ static std::vector<int> backward_needs(const Op& op) {
 void Net::build_schedule() {
   const int nt = (int)tensors_.size(), no = (int)ops_.size();
   sched_.clear();
+  for (auto& op : ops_) op.bstat_resident = false;
   std::vector<char> computed(nt, 0), ever(no, 0);
   computed[input_t_] = 1;
   int live_seg = -1;
@@ -579,6 +580,12 @@ void Net::build_schedule() {
     for (int t : backward_needs(ops_[pick]))
       if (!computed[t]) ensure(t);
     sched_.push_back({InstrKind::Backward, pick, s, false});
+    // a conv whose input is a BN's output: is that BN's input resident now?
+    // (its dgrad epilogue can then produce the BN's backward statistics)
+    if (ops_[pick].kind == OpKind::Conv) {
+      const int bp = tensors_[ops_[pick].in[0]].producer;
+      if (bp >= 0 && ops_[bp].kind == OpKind::BN) ops_[bp].bstat_resident = computed[ops_[bp].in[0]] != 0;
+    }
     ++bwd;
     done[pick] = 1;
     --remaining;
@@ -901,6 +908,55 @@ void Net::layout() {
     if (s_y < 0 || s_o != s_y) continue;
     op.fused_bn = b;
     bn.reforward_in_producer = true;
+  }
+  // BN+ReLU backward statistics from rows (see Op::bstat): eligible when the
+  // BN's output feeds exactly one conv; fused into that conv's dgrad when
+  // the dgrad is one plain launch (1x1 stride 1, or k x k stride 1 without
+  // split-K) and the BN input is resident there, else replayed at the BN's
+  // backward over the stored dout with the same tiles
+  const bool bstat_on = !std::getenv("RFK_BSTAT") || std::atoi(std::getenv("RFK_BSTAT")) != 0;
+  for (auto& op : ops_) op.bstat_src = -1;
+  for (int o = 0; o < (int)ops_.size(); ++o) {
+    Op& bn = ops_[o];
+    bn.bstat = bn.bstat_fused = false;
+    bn.bstat_off = -1;
+    if (!bstat_on || bn.kind != OpKind::BN || bn.k != 1) continue;
+    const Tensor& yt = tensors_[bn.in[0]];
+    if (tensors_[bn.out].consumers.size() != 1 || yt.C % 8) continue;
+    const int c = tensors_[bn.out].consumers[0];
+    Op& conv = ops_[c];
+    if (conv.kind != OpKind::Conv || conv.in[0] != bn.out || conv.explicit_im2col) continue;
+    const bool one_by_one = conv.R == 1 && conv.S == 1 && conv.pad == 0 && conv.pad_w == 0;
+    const bool fusible = one_by_one ? conv.stride == 1 : (conv.stride == 1 && !conv.dg_subpixel && conv.dg_splits <= 1);
+    // (a dgrad that can never fuse keeps the streaming reduction: replaying
+    // it through the GEMM epilogue measured slower)
+    if (!fusible) continue;
+    bn.bstat = true;
+    // the rows' tile width: the dgrad's own (auto) choice when it can fuse
+    rfk::GemmDesc d;
+    d.M = (int)yt.rows();
+    d.N = yt.C;
+    if (fusible && one_by_one) {
+      d.K = conv.cout;
+      d.a_kind = rfk::Operand::KMajor2D;
+      d.b_kind = rfk::Operand::MNMajor2D;
+    } else if (fusible) {
+      const Tensor& ct = tensors_[conv.out];
+      d.K = conv.R * conv.S * conv.coutpad;
+      d.a_kind = rfk::Operand::Im2colK;
+      d.a_geom = rfk::ConvGeom{ct.N, ct.H, ct.W, conv.cout, yt.H, yt.W, conv.R, conv.S, conv.R - 1 - conv.pad,
+                               conv.S - 1 - conv.pad_w, 1, 1};
+      d.b_kind = rfk::Operand::WeightTapsMN;
+    } else {
+      d.K = 64;
+      d.a_kind = rfk::Operand::KMajor2D;
+      d.b_kind = rfk::Operand::KMajor2D;
+    }
+    bn.bstat_bn = rfk::gemm_block_n(d);
+    bn.bstat_fused = fusible && bn.bstat_resident;
+    if (bn.bstat_fused) conv.bstat_src = o;
+    bn.bstat_off = ws_stats_ / 4;  // [kStatRows][2][C], written only by this BN's rows producer
+    ws_stats_ += align_up(kStatRows * 2 * (long)yt.C * 4);
   }
   for (auto& op : ops_)
     if (op.kind == OpKind::Conv && op.fuse_stats) {

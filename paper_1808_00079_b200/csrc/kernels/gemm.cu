@@ -63,8 +63,8 @@ struct alignas(64) KParams {
   const float* bn_shift;
   int bn_relu, fuse_bn;
   // BN backward statistics in the epilogue (stats_bwd): the output is dout of
-  // a BN+ReLU's output; it is stored masked (g = dout * [y*scale+shift > 0])
-  // and the statistics rows hold sum g and sum g*(y - mean) per column.
+  // a BN+ReLU's output (stored as is); the statistics rows hold sum g and
+  // sum g*(y - mean) per column, g = dout * [y*scale+shift > 0].
   // replay: no GEMM -- the epilogue re-reads the stored output instead of TMEM
   // (same tiles, same CTAs, same arithmetic: bit-identical rows).
   int stats_bwd, replay;
@@ -148,7 +148,7 @@ __device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const 
   }
 }
 
-template <int BN>
+template <int BN, bool EXT>  // EXT: BN-backward statistics / replay epilogue variants
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   const int total = p.m_tiles * p.n_tiles * p.splits;
 
   if (warp == 0 && elect_one()) {
-    if (!p.replay) {
+    if (!(EXT && p.replay)) {
       tma_prefetch(&p.ta);
       tma_prefetch(&p.tb);
     }
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
-    if (elect_one() && !p.replay) {
+    if (elect_one() && !(EXT && p.replay)) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < (p.replay ? 0 : total); t += gridDim.x, ++local) {
+    for (int t = blockIdx.x; t < ((EXT && p.replay) ? 0 : total); t += gridDim.x, ++local) {
       const TileCoord tc = tile_coord(p, t, BN);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (cur_nt >= 0) flush_stats(cur_nt);
         cur_nt = tc.n0 / BN;
       }
-      if (!p.replay) {
+      if (!(EXT && p.replay)) {
         mbar_wait(&acc_full[acc], acc_phase);
         tc_fence_after();
       }
@@ -381,8 +381,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const bool row_ok = m < p.M;
 #pragma unroll 1
       for (int c0 = (int)half * 32; c0 < BN; c0 += 64) {
+        // BN-backward statistics: this chunk's BN-input values (lane: column
+        // pair 2 (lane & 15), even / odd rows) are loaded first, so their
+        // latency overlaps the TMEM load and the output staging
+        uint32_t yv[16];
+        float2 bmu = make_float2(0.f, 0.f), bsc = bmu, bsh = bmu;
+        if (EXT && p.stats_bwd) {
+          const int c = tc.n0 + c0 + 2 * (int)(lane & 15);
+          const bool col_ok = c < p.N;
+          if (col_ok) {
+            bmu = __ldg(reinterpret_cast<const float2*>(p.bs_mean + c));
+            bsc = __ldg(reinterpret_cast<const float2*>(p.bs_scale + c));
+            bsh = __ldg(reinterpret_cast<const float2*>(p.bs_shift + c));
+          }
+#pragma unroll
+          for (int rr = 0; rr < 16; ++rr) {
+            const int mr = my + 2 * rr + (int)(lane >> 4);
+            yv[rr] = (col_ok && mr < p.M) ? __ldg(reinterpret_cast<const unsigned int*>(p.bs_y + (long)mr * p.bs_ldy + c))
+                                          : 0u;
+          }
+        }
         uint32_t r[32];
-        if (p.replay) {
+        if (EXT && p.replay) {
           // the stored bf16 output of this lane's row, 32 columns
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -404,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
-        if (c0 + 64 >= BN && !p.replay) {
+        if (c0 + 64 >= BN && !(EXT && p.replay)) {
           // this warp's last chunk of the accumulator is in registers: hand it back
           tc_fence_before();
           __syncwarp();
@@ -444,34 +464,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         uint32_t w[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) w[i] = row_ok ? pack_bf16(v[2 * i], v[2 * i + 1]) : 0u;
-        if (p.stats_bwd && row_ok) {
-          // g = dout * [y * scale + shift > 0] (the BN+ReLU backward's mask,
-          // same expression as bn_bwd_apply MODE 1); g is dout with lanes
-          // zeroed, so it is exact in bf16 and is what gets stored
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int c = col0 + 8 * j;
-            if (c >= p.N) break;
-            const uint4 yu = __ldg(reinterpret_cast<const uint4*>(p.bs_y + (long)m * p.bs_ldy + c));
-            const float4 sc0 = __ldg(reinterpret_cast<const float4*>(p.bs_scale + c));
-            const float4 sc1 = __ldg(reinterpret_cast<const float4*>(p.bs_scale + c + 4));
-            const float4 sh0 = __ldg(reinterpret_cast<const float4*>(p.bs_shift + c));
-            const float4 sh1 = __ldg(reinterpret_cast<const float4*>(p.bs_shift + c + 4));
-            const float sc[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
-            const float sh[8] = {sh0.x, sh0.y, sh0.z, sh0.w, sh1.x, sh1.y, sh1.z, sh1.w};
-            const uint32_t yw[4] = {yu.x, yu.y, yu.z, yu.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float ylo = __uint_as_float(yw[e] << 16), yhi = __uint_as_float(yw[e] & 0xffff0000u);
-              uint32_t g = w[4 * j + e];
-              if (!(fmaf(ylo, sc[2 * e], sh[2 * e]) > 0.f)) g &= 0xffff0000u;
-              if (!(fmaf(yhi, sc[2 * e + 1], sh[2 * e + 1]) > 0.f)) g &= 0x0000ffffu;
-              w[4 * j + e] = g;
-            }
-          }
-        }
         const uint8_t* sbuf;
-        if (p.replay) {
+        if (EXT && p.replay) {
           // statistics only: stage (same layout as the store paths), no write
           uint8_t* gb = stg;
           __syncwarp();
@@ -580,25 +574,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           // 64-byte halves of the bank space, so the reads are conflict-free.
           const uint32_t cp = lane & 15, par = lane >> 4;
           float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
-          if (p.stats_bwd) {
+          if (EXT && p.stats_bwd) {
             // sum g and sum g * (y - mean) over the chunk's rows (rows past M
             // and columns past N were staged as g = 0)
-            const int c = col0 + 2 * (int)cp;
-            const bool col_ok = c < p.N;
-            const float2 mu = col_ok ? __ldg(reinterpret_cast<const float2*>(p.bs_mean + c)) : make_float2(0.f, 0.f);
-            uint32_t yv[16];
-#pragma unroll
-            for (int rr = 0; rr < 16; ++rr) {
-              const int mr = my + 2 * rr + (int)par;
-              yv[rr] = (col_ok && mr < p.M) ? __ldg(reinterpret_cast<const unsigned int*>(p.bs_y + (long)mr * p.bs_ldy + c))
-                                            : 0u;
-            }
+            const float2 mu = bmu, sc = bsc, sh = bsh;
 #pragma unroll
             for (int rr = 0; rr < 16; ++rr) {
               const uint32_t row = 2 * rr + par;
               const uint32_t off = row * 64 + (((cp >> 2) ^ ((row >> 1) & 3u)) * 16) + (cp & 3) * 4;
-              const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sbuf + off));
+              float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sbuf + off));
               const float ylo = __uint_as_float(yv[rr] << 16), yhi = __uint_as_float(yv[rr] & 0xffff0000u);
+              // g = dout * [y * scale + shift > 0]: the BN+ReLU backward's
+              // mask, same expression as bn_bwd_apply MODE 1
+              if (!(fmaf(ylo, sc.x, sh.x) > 0.f)) g.x = 0.f;
+              if (!(fmaf(yhi, sc.y, sh.y) > 0.f)) g.y = 0.f;
               s0 += g.x;
               s1 += g.y;
               q0 = fmaf(g.x, ylo - mu.x, q0);
@@ -702,7 +691,9 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   using C = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -734,7 +725,8 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   kp.experiment = experiment;
   if (experiment == 1) kp.out_mode = 0;
   const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
-  return launch_k(gemm_kernel<BN>, grid, kThreads, smem, st, kp);
+  if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true>, grid, kThreads, smem, st, kp);
+  return launch_k(gemm_kernel<BN, false>, grid, kThreads, smem, st, kp);
 }
 
 }  // namespace

@@ -74,8 +74,8 @@ struct GemmDesc {
   // on a side stream while gradient buckets are in flight
   int max_ctas = 0;
   // BN backward statistics (with `stats`, bf16 output = dout of a BN+ReLU
-  // output): store g = dout * [bs_y * bs_scale + bs_shift > 0] and write rows
-  // of (sum g, sum g * (bs_y - bs_mean)) per column instead of (sum, sum^2).
+  // output, stored as is): rows of (sum g, sum g * (bs_y - bs_mean)) per
+  // column, g = dout * [bs_y * bs_scale + bs_shift > 0], instead of (sum, sum^2).
   // replay: no GEMM; the epilogue re-reads `out` and emits the same rows a
   // fused launch of the same M / N / block_n would (bit-identical).
   bool stats_bwd = false;

@@ -1628,6 +1628,23 @@ cudaError_t bn_apply(const __nv_bfloat16* y, const __nv_bfloat16* skip, const fl
   return cudaGetLastError();
 }
 
+cudaError_t bn_backward_from_rows(const __nv_bfloat16* y, const __nv_bfloat16* dout, const float* gamma,
+                                  const float* mean, const float* invstd, const float* scale, const float* shift,
+                                  long M, int C, const float* rows, int parts, float* coef, float* dgamma,
+                                  float* dbeta, __nv_bfloat16* dy, bool acc_dy, cudaStream_t st) {
+  const long nvec = M * C / 8;
+  if (C % 8 || nvec >= (1L << 31)) return cudaErrorInvalidValue;
+  if (!(ablate() & 2))
+    RFK_CHECK_LAUNCH(launch_k(bn_bwd_finalize_kernel, (C + 31) / 32, dim3(32, kFinY), 0, st, rows, parts, C,
+                              (float)M, gamma, mean, invstd, dgamma, dbeta, coef));
+  if (ablate() & 16) return cudaGetLastError();
+  const int g = grid_for(nvec, kThreads * 2, 148 * 4);
+  RFK_CHECK_LAUNCH(launch_k(bn_bwd_apply_kernel<1, false>, g, kThreads, 0, st, y, dout,
+                            static_cast<const __nv_bfloat16*>(nullptr), scale, shift, coef, (unsigned)nvec, C, dy,
+                            acc_dy ? 1 : 0, static_cast<__nv_bfloat16*>(nullptr), 0));
+  return cudaGetLastError();
+}
+
 cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const __nv_bfloat16* out, int mask_mode,
                         const float* gamma, const float* mean, const float* invstd, const float* scale,
                         const float* shift, long M, int C, float* partials, int blocks, float* coef, float* dgamma,

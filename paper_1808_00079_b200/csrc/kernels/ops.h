@@ -36,6 +36,13 @@ cudaError_t bn_backward(const __nv_bfloat16* y, const __nv_bfloat16* dout, const
                         const float* shift, long M, int C, float* partials, int blocks, float* coef, float* dgamma,
                         float* dbeta, __nv_bfloat16* dy, bool acc_dy, __nv_bfloat16* dskip, bool acc_dskip,
                         cudaStream_t st);
+// BN+ReLU backward from statistics rows [parts][2][C] of (sum g, sum g*(y-mean))
+// (written by the consumer conv's dgrad epilogue or its replay): finalize,
+// then dy (+)= k1*g + k2*y + k3 with g = dout * [y*scale + shift > 0]
+cudaError_t bn_backward_from_rows(const __nv_bfloat16* y, const __nv_bfloat16* dout, const float* gamma,
+                                  const float* mean, const float* invstd, const float* scale, const float* shift,
+                                  long M, int C, const float* rows, int parts, float* coef, float* dgamma,
+                                  float* dbeta, __nv_bfloat16* dy, bool acc_dy, cudaStream_t st);
 cudaError_t relu_fwd(const __nv_bfloat16* x, long n, __nv_bfloat16* y, cudaStream_t st);
 cudaError_t relu_bwd(const __nv_bfloat16* y, const __nv_bfloat16* dy, long n, __nv_bfloat16* dx, bool acc,
                      cudaStream_t st);

@@ -414,8 +414,8 @@ def _bwd_stats_case(kind, M, N, Kd, bn, seed):
 @pytest.mark.parametrize("kind,M,N,Kd,bn", [("kmajor", 6272, 256, 512, 128), ("mnmajor", 25088, 128, 512, 64),
                                             ("mnmajor", 1000, 72, 256, 64), ("kmajor", 100352, 64, 256, 64)])
 def test_bn_backward_statistics_epilogue_and_replay(kind, M, N, Kd, bn):
-    """The dgrad GEMM epilogue stores g = dout * [y*scale + shift > 0] and
-    emits per-CTA rows of (sum g, sum g*(y - mean)); a replay launch (no GEMM,
+    """The dgrad GEMM epilogue stores dout and emits per-CTA rows of (sum g,
+    sum g*(y - mean)), g = dout * [y*scale + shift > 0]; a replay launch (no GEMM,
     the epilogue re-reads the stored output) writes bit-identical rows -- so a
     BN backward gets the same statistics whether or not its input was resident
     when the dgrad ran."""
@@ -429,9 +429,9 @@ def test_bn_backward_statistics_epilogue_and_replay(kind, M, N, Kd, bn):
     K.gemm(args)
     torch.cuda.synchronize()
     mask = (y.float() * scale + shift) > 0
-    # stored output: the masked dout (one bf16 rounding of the GEMM)
-    _check(out, torch.where(mask, ref, torch.zeros_like(ref)))
-    gm = out.float().double()  # exactly what the statistics sum
+    # stored output: dout itself (one bf16 rounding of the GEMM)
+    _check(out, ref)
+    gm = torch.where(mask, out.float(), torch.zeros_like(ref)).double()  # exactly what the statistics sum
     s_ref = gm.sum(0)
     q_ref = (gm * (y.double() - mean.double())).sum(0)
     s, q = rows[:, 0].double().sum(0), rows[:, 1].double().sum(0)
@@ -447,14 +447,14 @@ def test_bn_backward_statistics_epilogue_and_replay(kind, M, N, Kd, bn):
     torch.cuda.synchronize()
     assert torch.equal(rows2, rows)
     assert torch.equal(out, before)  # the replay writes nothing
-    # replay over an UNMASKED dout (produced by a path without the fused
-    # epilogue) gives the same rows too: the mask is idempotent
+    # replay over the dout of a plain launch (a dgrad without the fused
+    # epilogue): the same output bits, the same rows
     out_unmasked = torch.zeros(M, N, device=dev, dtype=torch.bfloat16)
     plain = K.GemmArgs(M=M, N=N, K=Kd, a_kind=K.KMAJOR, a=a.data_ptr(), a_ld=Kd, out=out_unmasked.data_ptr(), ldc=N,
                        splits=1, block_n=bn, b_extent=N if kind == "mnmajor" else 0, **kw)
     K.gemm(plain)
     torch.cuda.synchronize()
-    assert torch.equal(torch.where(mask, out_unmasked, torch.zeros_like(out_unmasked)), out)
+    assert torch.equal(out_unmasked, out)
     rows3 = torch.full((160, 2, N), 0.0, device=dev)
     args2.out = out_unmasked.data_ptr()
     args2.stats = rows3.data_ptr()

@@ -97,6 +97,7 @@ struct Op {
   int bstat_src = -1;              // conv: BN whose rows its dgrad epilogue produces
   // pool
   int k = 1;
+  long pool_idx_off = -1;  // max pool: its argmax slot (bytes) in the pool-index workspace region
   // classifier / linear
   int classes = 0;  // output features
   int lin_h = 1, lin_w = 1, lin_c = 0;  // linear: input spatial shape (flattened NHWC)
@@ -219,6 +220,7 @@ class Net {
   // + param_count(i)) of the flat fp32 parameter / gradient buffers
   void pack_param(int i, const float* canonical, float* flat_slice) const;
   float* ws_stats_base() const;  // BN statistics rows region of the workspace
+  uint8_t* pool_idx(const Op& op) const;  // a max pool's argmax slot (nullptr: none)
   void unpack_param(int i, const float* flat_slice, float* canonical) const;
   long param_offset(int i) const { return params_.at(i).offset; }
   long param_count(int i) const { return params_.at(i).count; }
@@ -289,6 +291,7 @@ class Net {
   std::vector<char> grad_acc_;    // per (op, input) accumulate flags, flattened
   std::vector<int> grad_acc_base_;
   long arena_bytes_ = 0, grad_bytes_ = 0;
+  long ws_pool_ = 0;  // per-max-pool argmax bytes, after ws_dsplit_ (written by every forward of the pool)
   long ws_im2col_ = 0, ws_partials_ = 0, ws_zero_ = 0, ws_split_ = 0, ws_stats_ = 0, ws_misc_ = 0,
        ws_counters_ = 0, ws_dsplit_ = 0;
   MemoryReport rep_;

@@ -498,6 +498,12 @@ void Net::gemm(const rfk::GemmDesc& d0, cudaStream_t st) {
   check(rfk::gemm_launch(d, st), "gemm");
 }
 
+uint8_t* Net::pool_idx(const Op& op) const {
+  if (op.pool_idx_off < 0) return nullptr;
+  return d_ws_ + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_ + ws_counters_ + ws_dsplit_ +
+         op.pool_idx_off;
+}
+
 float* Net::ws_stats_base() const {
   return reinterpret_cast<float*>(d_ws_ + ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_);
 }
@@ -662,7 +668,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       const Tensor& x = tensors_[op.in[0]];
       const Tensor& y = tensors_[op.out];
       rfk::PoolGeom g{x.N, x.H, x.W, x.C, y.H, y.W, op.k, op.stride, op.pad};
-      check(rfk::maxpool_fwd(tb(op.in[0]), g, tb(op.out), st), "maxpool");
+      check(rfk::maxpool_fwd(tb(op.in[0]), g, tb(op.out), st, pool_idx(op)), "maxpool");
       break;
     }
     case OpKind::AvgPool: {
@@ -1046,8 +1052,11 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       const Tensor& x = tensors_[op.in[0]];
       const Tensor& y = tensors_[op.out];
       rfk::PoolGeom g{x.N, x.H, x.W, x.C, y.H, y.W, op.k, op.stride, op.pad};
-      check(rfk::maxpool_bwd(tb(op.in[0]), tb(op.out), gptr(op.out), g, gptr(op.in[0]), acc(0), ws_zero, st),
-            "maxpool_bwd");
+      if (op.pool_idx_off >= 0)
+        check(rfk::maxpool_bwd_from_idx(pool_idx(op), gptr(op.out), g, gptr(op.in[0]), acc(0), st), "maxpool_bwd");
+      else
+        check(rfk::maxpool_bwd(tb(op.in[0]), tb(op.out), gptr(op.out), g, gptr(op.in[0]), acc(0), ws_zero, st),
+              "maxpool_bwd");
       break;
     }
     case OpKind::AvgPool: {

@@ -969,8 +969,19 @@ void Net::layout() {
       ws_stats_ += align_up((long)rfk::colstats_blocks(tensors_[t].rows()) * 2 * tensors_[t].C * 4);
     }
   ws_counters_ = 0;
+  // max pools keep their argmax from the forward (and every re-forward): the
+  // backward gathers dy through it and never re-reads x (RFK_POOL_IDX=0: the
+  // fused tiled backward over x instead)
+  ws_pool_ = 0;
+  const bool pool_idx = !std::getenv("RFK_POOL_IDX") || std::atoi(std::getenv("RFK_POOL_IDX")) != 0;
+  for (auto& op : ops_) {
+    op.pool_idx_off = -1;
+    if (!pool_idx || op.kind != OpKind::MaxPool || op.k * op.k > 256) continue;
+    op.pool_idx_off = ws_pool_;
+    ws_pool_ += align_up(tensors_[op.out].elems());
+  }
   rep_.workspace_bytes =
-      ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_ + ws_counters_ + ws_dsplit_;
+      ws_im2col_ + ws_partials_ + ws_zero_ + ws_split_ + ws_stats_ + ws_misc_ + ws_counters_ + ws_dsplit_ + ws_pool_;
   if (std::getenv("RFK_TRACE_WS"))
     std::fprintf(stderr, "workspace MB: im2col %.1f partials %.1f zero/argmax %.1f wgrad-split %.1f stats %.1f misc %.1f "
                  "fprop/dgrad-split %.1f\n", ws_im2col_ / 1e6, ws_partials_ / 1e6, ws_zero_ / 1e6, ws_split_ / 1e6,

@@ -504,8 +504,10 @@ __global__ void __launch_bounds__(kThreads) relu_bwd_kernel(const __nv_bfloat16*
 }
 
 // ------------------------------------------------------------ pooling
+// idx (optional): the first-argmax window position of every output, for the
+// backward gather (same rule as maxpool_argmax_kernel)
 __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, PoolGeom g,
-                                                              __nv_bfloat16* __restrict__ y) {
+                                                              __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ idx) {
   pdl_enter();
   const int cv = g.C / 8;
   const unsigned total = (unsigned)g.N * g.P * g.Q * cv;
@@ -517,8 +519,12 @@ __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat
     const int p = (int)(t % (unsigned)g.P);
     const int n = (int)(t / (unsigned)g.P);
     float m[8];
+    uint32_t best[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) m[k] = -INFINITY;
+    for (int k = 0; k < 8; ++k) {
+      m[k] = -INFINITY;
+      best[k] = 0;
+    }
     for (int r = 0; r < g.k; ++r) {
       const int h = p * g.stride - g.pad + r;
       if (h < 0 || h >= g.H) continue;
@@ -528,10 +534,20 @@ __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat
         float f[8];
         unpack8(ldg16(x + (((long)n * g.H + h) * g.W + w) * g.C + c8 * 8), f);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) m[k] = fmaxf(m[k], f[k]);
+        for (int k = 0; k < 8; ++k)
+          if (f[k] > m[k]) {
+            m[k] = f[k];
+            best[k] = (uint32_t)(r * g.k + s);
+          }
       }
     }
     *reinterpret_cast<uint4*>(y + (size_t)i * 8) = pack8(m);
+    if (idx) {
+      uint2 o;
+      o.x = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+      o.y = best[4] | (best[5] << 8) | (best[6] << 16) | (best[7] << 24);
+      *reinterpret_cast<uint2*>(idx + (size_t)i * 8) = o;
+    }
   }
 }
 
@@ -1706,10 +1722,20 @@ cudaError_t relu_bwd(const __nv_bfloat16* y, const __nv_bfloat16* dy, long n, __
   return cudaGetLastError();
 }
 
-cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st) {
+cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st, uint8_t* idx) {
   if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
+  if (idx && g.k * g.k > 256) return cudaErrorInvalidValue;
   const long work = (long)g.N * g.P * g.Q * (g.C / 8);
-  RFK_CHECK_LAUNCH(launch_k(maxpool_fwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y));
+  RFK_CHECK_LAUNCH(launch_k(maxpool_fwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y, idx));
+  return cudaGetLastError();
+}
+
+cudaError_t maxpool_bwd_from_idx(const uint8_t* idx, const __nv_bfloat16* dy, const PoolGeom& g, __nv_bfloat16* dx,
+                                 bool acc, cudaStream_t st) {
+  if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
+  const long work = (long)g.N * g.H * g.W * (g.C / 8);
+  RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+                            acc ? 1 : 0));
   return cudaGetLastError();
 }
 

@@ -46,7 +46,12 @@ cudaError_t bn_backward_from_rows(const __nv_bfloat16* y, const __nv_bfloat16* d
 cudaError_t relu_fwd(const __nv_bfloat16* x, long n, __nv_bfloat16* y, cudaStream_t st);
 cudaError_t relu_bwd(const __nv_bfloat16* y, const __nv_bfloat16* dy, long n, __nv_bfloat16* dx, bool acc,
                      cudaStream_t st);
-cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st);
+// idx (optional): first-argmax window position per output (k*k <= 256), read
+// back by maxpool_bwd_from_idx (the backward then never re-reads x)
+cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16* y, cudaStream_t st,
+                        uint8_t* idx = nullptr);
+cudaError_t maxpool_bwd_from_idx(const uint8_t* idx, const __nv_bfloat16* dy, const PoolGeom& g, __nv_bfloat16* dx,
+                                 bool acc, cudaStream_t st);
 // idx_ws: N*P*Q*C bytes of scratch (window argmax)
 cudaError_t maxpool_bwd(const __nv_bfloat16* x, const __nv_bfloat16* y, const __nv_bfloat16* dy, const PoolGeom& g,
                         __nv_bfloat16* dx, bool acc, void* idx_ws, cudaStream_t st);

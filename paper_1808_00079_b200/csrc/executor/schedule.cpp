@@ -922,7 +922,8 @@ void Net::layout() {
     bn.bstat_off = -1;
     if (!bstat_on || bn.kind != OpKind::BN || bn.k != 1) continue;
     const Tensor& yt = tensors_[bn.in[0]];
-    if (tensors_[bn.out].consumers.size() != 1 || yt.C % 8) continue;
+    static const int min_c = std::getenv("RFK_BSTAT_MINC") ? std::atoi(std::getenv("RFK_BSTAT_MINC")) : 0;
+    if (tensors_[bn.out].consumers.size() != 1 || yt.C % 8 || yt.C < min_c) continue;
     const int c = tensors_[bn.out].consumers[0];
     Op& conv = ops_[c];
     if (conv.kind != OpKind::Conv || conv.in[0] != bn.out || conv.explicit_im2col) continue;

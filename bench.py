@@ -459,6 +459,7 @@ def main():
         print(json.dumps(line))
     if world > 1:
         dist.barrier()
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 

@@ -621,7 +621,10 @@ std::pair<int, int> im2col_split_plan(long M, int N, long kb) {
       const long tiles = mt * ((N + bn - 1) / bn) * s;
       const long waves = (tiles + 147) / 148;
       double t = (double)waves * ((double)((kb + s - 1) / s) * 0.5 + b);
-      if (s > 1) t += (double)s * M * N * 4.0 / 3.0e6 + 3.0;
+      // fp32 partials written and summed once more, plus the finish launch
+      static const double bw = std::getenv("RFK_SPLIT_BW") ? std::atof(std::getenv("RFK_SPLIT_BW")) : 3.0e6;
+      static const double fixed = std::getenv("RFK_SPLIT_FIXED") ? std::atof(std::getenv("RFK_SPLIT_FIXED")) : 3.0;
+      if (s > 1) t += (double)s * M * N * 4.0 / bw + fixed;
       if (best < 0 || t < best - 1e-9) {
         best = t;
         pick = {bn, s};

@@ -53,10 +53,13 @@ typedef struct rfx_gemm_args {
   const float* bs_mean;
   const float* bs_scale;
   const float* bs_shift;
+  int32_t pair;                      /* CTA pairs (cta_group::2, M = 256): 0 auto, 1 where allowed, -1 never */
 } rfx_gemm_args;
 /* kind 4 = conv weights [Cout][R][S][Cpad] read as the dgrad B operand (flipped taps) */
 
 int rfx_gemm(const rfx_gemm_args* args, void* stream);
+/* sizeof(rfx_gemm_args) as compiled: lets FFI callers check their layout */
+size_t rfx_gemm_args_size(void);
 /* explicit im2col of a few-channel NHWC bf16 conv input (the stem path):
  * x [N][H][W][Cs] (C real channels) -> out [N*P*Q][kpad], K order (r, s, c),
  * zero K padding; kpad % 8 == 0 */

@@ -20,6 +20,8 @@ rfk::ConvGeom to_geom(const rfx_conv_geom& g) {
 }
 }  // namespace
 
+extern "C" size_t rfx_gemm_args_size(void) { return sizeof(rfx_gemm_args); }
+
 extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
   rfk::GemmDesc d;
   d.M = a->M; d.N = a->N; d.K = a->K;
@@ -46,6 +48,7 @@ extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
   d.bs_mean = a->bs_mean;
   d.bs_scale = a->bs_scale;
   d.bs_shift = a->bs_shift;
+  d.pair = a->pair;
   cudaError_t e = rfk::gemm_launch(d, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     rfexec::set_last_error(std::string("rfx_gemm: ") + cudaGetErrorString(e));

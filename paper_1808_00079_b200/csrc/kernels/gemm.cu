@@ -77,9 +77,10 @@ struct alignas(64) KParams {
                   // 5 skip the statistics smem reads, 6 skip the statistics accumulation
 };
 
-template <int BN>
+template <int BN, bool PAIR = false>
 struct Cfg {
-  static constexpr int kTileB = BN * kBlockK * 2;
+  // a CTA of a pair stages half of the B tile
+  static constexpr int kTileB = (PAIR ? BN / 2 : BN) * kBlockK * 2;
   static constexpr int kStage = kTileA + kTileB;
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
   // epilogue staging: per warp, 1 or 2 buffers of one 32-row x 64-byte box
@@ -111,10 +112,16 @@ struct TileCoord {
   int m0, n0, z, kb_begin, kb_end;
 };
 
-__device__ __forceinline__ TileCoord tile_coord(const KParams& p, int t, int BN) {
+// A CTA pair (PAIR) computes the 256 x BN tile made of M tiles 2i and 2i + 1:
+// unit t -> (M tile pair fastest, then n tile, then split), and the CTA of
+// cluster rank r drains M tile 2i + r (past the last M tile when m_tiles is
+// odd: its A rows load as zeros and nothing is stored).
+template <bool PAIR>
+__device__ __forceinline__ TileCoord tile_coord(const KParams& p, int t, int BN, int rank) {
   TileCoord c;
-  const int mt = t % p.m_tiles;
-  const int rest = t / p.m_tiles;
+  const int mu = PAIR ? (p.m_tiles + 1) >> 1 : p.m_tiles;
+  const int mt = PAIR ? 2 * (t % mu) + rank : t % mu;
+  const int rest = t / mu;
   c.m0 = mt * kBlockM;
   c.n0 = (rest % p.n_tiles) * BN;
   c.z = rest / p.n_tiles;
@@ -148,9 +155,17 @@ __device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const 
   }
 }
 
-template <int BN, bool EXT>  // EXT: BN-backward statistics / replay epilogue variants
+// EXT: BN-backward statistics / replay epilogue variants.
+// PAIR: launched as 2-CTA clusters running M = 256 tiles with cta_group::2
+// MMAs issued by the rank-0 CTA.  Each CTA stages its own 128 A rows and half
+// of the B columns, so per SM the shared-memory traffic of a K block (TMA
+// writes + MMA reads) drops from A + B to A + B/2 -- the 1-SM kernel is bound
+// by it.  Each CTA's epilogue drains its own TMEM (its 128 rows, all BN
+// columns); the accumulator is released once both epilogues arrived on the
+// leader's barrier.
+template <int BN, bool EXT, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, PAIR>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the shared array itself, so
   // every derived pointer keeps the shared address space (LDS/STS, not
@@ -165,7 +180,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const uint32_t warp = warp_id();
-  const int total = p.m_tiles * p.n_tiles * p.splits;
+  // persistent unit loop: CTA (pair) t0 takes units t0, t0 + tstep, ...
+  const int rank = PAIR ? (int)cluster_ctarank() : 0;
+  const int t0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int total = (PAIR ? (p.m_tiles + 1) >> 1 : p.m_tiles) * p.n_tiles * p.splits;
 
   if (warp == 0 && elect_one()) {
     if (!(EXT && p.replay)) {
@@ -180,13 +199,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], kEpiWarps);  // one arrive per epilogue warp
+      mbar_init(&acc_empty[a], PAIR ? 2 * kEpiWarps : kEpiWarps);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<2 * C::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if (PAIR)
+      tmem_alloc_pair<2 * C::kTmemCols>(tmem_slot);
+    else
+      tmem_alloc<2 * C::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // the leader's barriers exist before the peer's loads signal them
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // everything above (barrier init, TMEM allocation, descriptor prefetch)
@@ -198,59 +223,91 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     if (elect_one() && !(EXT && p.replay)) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = tile_coord(p, t, BN);
+      // this CTA's B columns: all BN, or (pair) the half n0 + rank * BN/2
+      constexpr int BNB = PAIR ? BN / 2 : BN;
+      // the loads of both CTAs of a pair complete on the leader's full barrier
+      auto ld2 = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+        if (PAIR)
+          tma_load_2d_pair(dst, m, mapa_u32(smem_u32(bar), 0), c0, c1);
+        else
+          tma_load_2d(dst, m, bar, c0, c1);
+      };
+      auto ld3 = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+        if (PAIR)
+          tma_load_3d_pair(dst, m, mapa_u32(smem_u32(bar), 0), c0, c1, c2);
+        else
+          tma_load_3d(dst, m, bar, c0, c1, c2);
+      };
+      auto ldi = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c, int w, int h, int n, uint16_t s,
+                     uint16_t r) {
+        if (PAIR)
+          tma_load_im2col_pair(dst, m, mapa_u32(smem_u32(bar), 0), c, w, h, n, s, r);
+        else
+          tma_load_im2col(dst, m, bar, c, w, h, n, s, r);
+      };
+      for (int t = t0; t < total; t += tstep) {
+        const TileCoord tc = tile_coord<PAIR>(p, t, BN, rank);
+        const int n0b = tc.n0 + rank * BNB;
         int aw = 0, ah = 0, an = 0;
         if (p.a_kind == (int)Operand::Im2colK) pixel_base(p, tc.m0, aw, ah, an);
         for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStage;
           uint8_t* sb = sa + kTileA;
-          mbar_arrive_expect_tx(&full[stage], C::kStage);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], PAIR ? 2 * C::kStage : C::kStage);
           switch (p.a_kind) {
             case (int)Operand::KMajor2D:
-              tma_load_2d(sa, &p.ta, &full[stage], kb * kBlockK, tc.m0);
+              ld2(sa, &p.ta, &full[stage], kb * kBlockK, tc.m0);
               break;
             case (int)Operand::MNMajor2D:
-              tma_load_2d(sa, &p.ta, &full[stage], tc.m0, kb * kBlockK);
-              tma_load_2d(sa + kTileA / 2, &p.ta, &full[stage], tc.m0 + 64, kb * kBlockK);
+              ld2(sa, &p.ta, &full[stage], tc.m0, kb * kBlockK);
+              ld2(sa + kTileA / 2, &p.ta, &full[stage], tc.m0 + 64, kb * kBlockK);
               break;
             default: {  // Im2colK: K block -> (tap, channel block)
               const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
               const int r = tap / p.g_S, s = tap - r * p.g_S;
-              tma_load_im2col(sa, &p.ta, &full[stage], cb * 64, aw, ah, an, (uint16_t)s, (uint16_t)r);
+              ldi(sa, &p.ta, &full[stage], cb * 64, aw, ah, an, (uint16_t)s, (uint16_t)r);
             }
           }
           switch (p.b_kind) {
-            case (int)Operand::KMajor2D:
-              tma_load_2d(sb, &p.tb, &full[stage], kb * kBlockK, tc.n0);
+            case (int)Operand::KMajor2D:  // box of BNB rows
+              ld2(sb, &p.tb, &full[stage], kb * kBlockK, n0b);
               break;
             case (int)Operand::MNMajor2D:
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_2d(sb + j * 8192, &p.tb, &full[stage], tc.n0 + 64 * j, kb * kBlockK);
+              for (int j = 0; j < BNB / 64; ++j) ld2(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, kb * kBlockK);
               break;
             case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
               const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
               const int tr = tap / p.g_S, ts = tap - tr * p.g_S;
               const int ftap = p.b_tap_base - tr * p.b_tap_dr - ts * p.b_tap_ds;
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_3d(sb + j * 8192, &p.tb, &full[stage], tc.n0 + 64 * j, ftap, cb * 64);
+              for (int j = 0; j < BNB / 64; ++j) ld3(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, ftap, cb * 64);
               break;
             }
             default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
               int bw, bh, bn;
               pixel_base(p, kb * kBlockK, bw, bh, bn);
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) {
-                const int nb = tc.n0 / 64 + j;
+              for (int j = 0; j < BNB / 64; ++j) {
+                const int nb = n0b / 64 + j;
                 const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
                 const int r = tap / p.g_S, s = tap - r * p.g_S;
-                tma_load_im2col(sb + j * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+                ldi(sb + j * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
               }
             }
           }
+          if (++stage == nst) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (PAIR) {
+        // the leader's last MMA commits arrive on this CTA's empty barriers:
+        // wait for them before the CTA may exit
+        for (int i = 0; i < nst; ++i) {
+          mbar_wait(&empty[stage], phase ^ 1);
           if (++stage == nst) {
             stage = 0;
             phase ^= 1;
@@ -263,19 +320,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const bool a_mn = p.a_kind == (int)Operand::MNMajor2D;
     const bool b_mn = p.b_kind == (int)Operand::MNMajor2D || p.b_kind == (int)Operand::Im2colMN ||
                       p.b_kind == (int)Operand::WeightTapsMN;
-    const uint32_t idesc = umma_idesc_bf16(kBlockM, BN, a_mn, b_mn);
+    const uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * kBlockM : kBlockM, BN, a_mn, b_mn);
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < ((EXT && p.replay) ? 0 : total); t += gridDim.x, ++local) {
-      const TileCoord tc = tile_coord(p, t, BN);
+    // (pair: the rank-1 CTA issues nothing; the leader's MMAs fill both TMEMs)
+    for (int t = t0; t < ((EXT && p.replay) || rank != 0 ? 0 : total); t += tstep, ++local) {
+      const TileCoord tc = tile_coord<PAIR>(p, t, BN, rank);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&acc_empty[acc], acc_phase ^ 1);  // epilogue drained this accumulator
+      mbar_wait(&acc_empty[acc], acc_phase ^ 1);  // epilogue(s) drained this accumulator
       tc_fence_after();
       const uint32_t d_tmem = tmem + (uint32_t)(acc * C::kTmemCols);
       if (tc.kb_end <= tc.kb_begin) {
-        if (elect_one()) mbar_arrive(&acc_full[acc]);  // empty split: nothing to accumulate
+        if (elect_one()) {  // empty split: nothing to accumulate
+          mbar_arrive(&acc_full[acc]);
+          if (PAIR) mbar_arrive_cluster(mapa_u32(smem_u32(&acc_full[acc]), 1));
+        }
         __syncwarp();
         continue;
       }
@@ -291,10 +352,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                                      : umma_desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
                                      : umma_desc_sw128(sb + kk * 32, 16, 1024);
-            umma_bf16(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
+            if (PAIR)
+              umma_bf16_pair(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
+            else
+              umma_bf16(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);
-          if (kb + 1 == tc.kb_end) umma_commit(&acc_full[acc]);
+          if (PAIR) {
+            umma_commit_pair(&empty[stage]);
+            if (kb + 1 == tc.kb_end) umma_commit_pair(&acc_full[acc]);
+          } else {
+            umma_commit(&empty[stage]);
+            if (kb + 1 == tc.kb_end) umma_commit(&acc_full[acc]);
+          }
         }
         __syncwarp();
         if (++stage == nst) {
@@ -363,8 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       __syncwarp();
     }
     int local = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
-      const TileCoord tc = tile_coord(p, t, BN);
+    for (int t = t0; t < total; t += tstep, ++local) {
+      const TileCoord tc = tile_coord<PAIR>(p, t, BN, rank);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const bool empty_k = tc.kb_end <= tc.kb_begin;
@@ -428,7 +497,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           // this warp's last chunk of the accumulator is in registers: hand it back
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&acc_empty[acc]);
+          if (lane == 0) {
+            if (PAIR && rank != 0)
+              mbar_arrive_cluster(mapa_u32(smem_u32(&acc_empty[acc]), 0));
+            else
+              mbar_arrive(&acc_empty[acc]);
+          }
         }
         float v[32];
 #pragma unroll
@@ -625,9 +699,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // neither CTA leaves (or frees TMEM) while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<2 * C::kTmemCols>(tmem);
+    if (PAIR)
+      tmem_dealloc_pair<2 * C::kTmemCols>(tmem);
+    else
+      tmem_dealloc<2 * C::kTmemCols>(tmem);
   }
 }
 
@@ -686,14 +764,60 @@ bool encode_im2col(CUtensorMap* m, const void* ptr, const ConvGeom& g, uint32_t 
   return true;
 }
 
+// CTA pairs for launches that leave the choice to the engine (desc.pair ==
+// 0): RFK_GEMM_PAIR=0 (default) never, 1 where the main loop dominates, 2
+// wherever the shapes allow.  Off by default: the training step's GEMMs are
+// bound by the operand feed and the epilogue, not the MMA rate, and inside
+// the step's graph a 2-CTA cluster also waits for two free SMs of a TPC
+// (ResNet-50 step 5.390 ms without pairs, 5.449 ms with the automatic rule).
+int pair_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("RFK_GEMM_PAIR");
+    return e == nullptr ? 0 : std::atoi(e);
+  }();
+  return m;
+}
+
+// how many CTA pairs of this kernel can be resident at once (the GPCs need
+// not split into SM pairs evenly)
 template <int BN>
-cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max_ctas, cudaStream_t st) {
+int pair_max_clusters() {
+  static int n = -1;
+  if (n < 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg<BN, true>::kSmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, gemm_kernel<BN, false, true>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    n = c;
+    if (std::getenv("RFK_TRACE_PAIR")) std::fprintf(stderr, "rfk: bn=%d pairs resident=%d\n", BN, n);
+  }
+  return n;
+}
+
+template <int BN>
+cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max_ctas, bool pair, cudaStream_t st) {
   using C = Cfg<BN>;
+  using CP = Cfg<BN, true>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_kernel<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(gemm_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+      e = cudaFuncSetAttribute(gemm_kernel<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_kernel<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::kSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -705,18 +829,28 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  const long total = (long)m_tiles * n_tiles * splits;
-  const int grid = (int)std::min<long>(total, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
+  const int cap = max_ctas > 0 ? std::min(max_ctas, sms) : sms;
+  const long total = (long)(pair ? (m_tiles + 1) / 2 : m_tiles) * n_tiles * splits;  // units (tile pairs)
+  int grid;
+  if (pair) {
+    const int clusters = std::min(pair_max_clusters<BN>(), cap / 2);
+    if (clusters <= 0) return cudaErrorInvalidValue;
+    grid = 2 * (int)std::min<long>(total, clusters);
+  } else {
+    grid = (int)std::min<long>(total, cap);
+  }
+  const int units_grid = pair ? grid / 2 : grid;
   kp.m_tiles = m_tiles;
   kp.n_tiles = n_tiles;
   kp.splits = splits;
-  const long kb_per_cta = (long)kp.kb_per_split * ((total + grid - 1) / grid);
-  kp.stages = (int)std::max<long>(2, std::min<long>(C::kStages, kb_per_cta));
+  const long kb_per_cta = (long)kp.kb_per_split * ((total + units_grid - 1) / units_grid);
+  const int max_stages = pair ? CP::kStages : C::kStages;
+  kp.stages = (int)std::max<long>(2, std::min<long>(max_stages, kb_per_cta));
   static const int force_stages = [] {
     const char* e = std::getenv("RFK_GEMM_STAGES");  // tuning experiments only
     return e ? std::atoi(e) : 0;
   }();
-  if (force_stages >= 2) kp.stages = std::min(force_stages, C::kStages);
+  if (force_stages >= 2) kp.stages = std::min(force_stages, max_stages);
   if (kp.replay) kp.stages = 2;  // no operand ring in a statistics replay
   static const int experiment = [] {
     const char* e = std::getenv("RFK_GEMM_EXPERIMENT");  // tuning experiments only
@@ -724,9 +858,13 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   }();
   kp.experiment = experiment;
   if (experiment == 1) kp.out_mode = 0;
+  if (pair) {
+    const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + 256;
+    return launch_k_cluster(gemm_kernel<BN, false, true>, grid, kThreads, smem, st, 2, kp);
+  }
   const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
-  if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true>, grid, kThreads, smem, st, kp);
-  return launch_k(gemm_kernel<BN, false>, grid, kThreads, smem, st, kp);
+  if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true, false>, grid, kThreads, smem, st, kp);
+  return launch_k(gemm_kernel<BN, false, false>, grid, kThreads, smem, st, kp);
 }
 
 }  // namespace
@@ -806,13 +944,28 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
     kp.stats = d.stats;
     const int m_tiles = gemm_m_tiles(d), n_tiles = (d.N + bn - 1) / bn;
     switch (bn) {
-      case 64: return launch_bn<64>(kp, m_tiles, n_tiles, 1, 0, stream);
-      case 128: return launch_bn<128>(kp, m_tiles, n_tiles, 1, 0, stream);
-      default: return launch_bn<256>(kp, m_tiles, n_tiles, 1, 0, stream);
+      case 64: return launch_bn<64>(kp, m_tiles, n_tiles, 1, 0, false, stream);
+      case 128: return launch_bn<128>(kp, m_tiles, n_tiles, 1, 0, false, stream);
+      default: return launch_bn<256>(kp, m_tiles, n_tiles, 1, 0, false, stream);
     }
   }
   kp.a_kind = (int)d.a_kind;
   kp.b_kind = (int)d.b_kind;
+  // CTA pair: M = 256 tiles, each CTA staging half of B (K-major: a box of
+  // bn/2 rows; MN-major: whole 64-wide boxes, so bn >= 128)
+  const int pmode = d.pair != 0 ? (d.pair > 0 ? 2 : 0) : pair_mode();
+  bool pair = pmode > 0 && !d.stats_bwd && gemm_m_tiles(d) >= 2 && (d.b_kind == Operand::KMajor2D || bn >= 128);
+  if (pair && pmode == 1) {
+    // measured (tools/gemm_probe.py, profiles/gemm_pair_r2.txt): pairs speed
+    // up long plain-operand main loops (+11 % at K = 4608, 8192^3 1.28 ->
+    // 1.42 PFLOP/s) but slow epilogue-bound launches (K = 64: -50 %) and
+    // gain nothing when A comes through TMA im2col (the load feed bounds it)
+    const int splits_ = d.splits < 1 ? 1 : d.splits;
+    const long kb_tile = ((d.a_kind == Operand::Im2colK ? (long)d.a_geom.R * d.a_geom.S * ((d.a_geom.C + 63) / 64)
+                                                        : (long)(d.K + 63) / 64) +
+                          splits_ - 1) / splits_;
+    pair = d.a_kind != Operand::Im2colK && kb_tile >= 32;
+  }
   const ConvGeom* geo = nullptr;
   bool ok = true;
   switch (d.a_kind) {
@@ -836,7 +989,7 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   switch (d.b_kind) {
     case Operand::KMajor2D:
       ok = encode_2d(&kp.tb, d.b, (uint64_t)(d.a_kind == Operand::Im2colK ? (long)kp.num_kb * 64 : d.K), d.N, d.b_ld,
-                     64, bn);
+                     64, pair ? bn / 2 : bn);
       break;
     case Operand::MNMajor2D:
       ok = encode_2d(&kp.tb, d.b, d.b_extent > 0 ? d.b_extent : d.N, d.K, d.b_ld, 64, 64);
@@ -936,9 +1089,9 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   const int m_tiles = gemm_m_tiles(d);
   const int n_tiles = (d.N + bn - 1) / bn;
   switch (bn) {
-    case 64: return launch_bn<64>(kp, m_tiles, n_tiles, splits, d.max_ctas, stream);
-    case 128: return launch_bn<128>(kp, m_tiles, n_tiles, splits, d.max_ctas, stream);
-    default: return launch_bn<256>(kp, m_tiles, n_tiles, splits, d.max_ctas, stream);
+    case 64: return launch_bn<64>(kp, m_tiles, n_tiles, splits, d.max_ctas, pair, stream);
+    case 128: return launch_bn<128>(kp, m_tiles, n_tiles, splits, d.max_ctas, pair, stream);
+    default: return launch_bn<256>(kp, m_tiles, n_tiles, splits, d.max_ctas, pair, stream);
   }
 }
 

@@ -85,6 +85,9 @@ struct GemmDesc {
   const float* bs_mean = nullptr;
   const float* bs_scale = nullptr;
   const float* bs_shift = nullptr;
+  // CTA pairs (2-CTA clusters, cta_group::2 M = 256 tiles): 0 = automatic
+  // (long plain-operand main loops), 1 = wherever the shapes allow, -1 = never
+  int pair = 0;
 };
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream);

@@ -32,7 +32,8 @@ class GemmArgs(C.Structure):
                 ("b_taps", C.c_int32), ("b_cpad", C.c_int32), ("b_rows", C.c_int32), ("band", C.c_int32),
                 ("b_tap_map", C.c_int32), ("b_tap_base", C.c_int32), ("b_tap_dr", C.c_int32),
                 ("b_tap_ds", C.c_int32), ("stats_bwd", C.c_int32), ("replay", C.c_int32), ("bs_y", C.c_void_p),
-                ("bs_ldy", C.c_int64), ("bs_mean", C.c_void_p), ("bs_scale", C.c_void_p), ("bs_shift", C.c_void_p)]
+                ("bs_ldy", C.c_int64), ("bs_mean", C.c_void_p), ("bs_scale", C.c_void_p), ("bs_shift", C.c_void_p),
+                ("pair", C.c_int32)]
 
 
 def conv_geom(N, H, W, Cin, R, S, pad, stride) -> ConvGeom:

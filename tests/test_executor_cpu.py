@@ -33,6 +33,13 @@ def test_abi_exports_every_declared_symbol():
     assert not missing, missing
 
 
+def test_gemm_args_layout_matches_the_python_binding():
+    from paper_1808_00079_b200.kernels import GemmArgs
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.rfx_gemm_args_size.restype = ctypes.c_size_t
+    assert lib.rfx_gemm_args_size() == ctypes.sizeof(GemmArgs)
+
+
 @pytest.mark.parametrize("arch,batch,hw,classes", SMALL + [("resnet50", 32, 224, 1000)])
 def test_schedule_high_water_equals_planner_total(arch, batch, hw, classes):
     net = ReforwardNet.named(arch, batch, hw, hw, classes)

@@ -23,6 +23,22 @@ torch.backends.cudnn.allow_tf32 = False
 torch.backends.cuda.matmul.allow_tf32 = False
 
 
+@pytest.fixture(params=[0, 1, -1], ids=["auto", "pair", "single"], autouse=True)
+def cta_pair_mode(request, monkeypatch):
+    """Every case runs with the automatic choice, with CTA pairs (2-CTA
+    clusters, cta_group::2 M = 256 tiles) wherever the shape allows them --
+    including odd M-tile counts, whose second CTA drains an all-out-of-bounds
+    tile -- and with single CTAs only."""
+    orig = K.gemm
+
+    def gemm(args, *a, **kw):
+        if args.pair == 0:
+            args.pair = request.param
+        return orig(args, *a, **kw)
+
+    monkeypatch.setattr(K, "gemm", gemm)
+
+
 def _bf(*shape, scale=1.0, seed=0):
     g = torch.Generator(device="cpu").manual_seed(seed)
     return (torch.randn(*shape, generator=g) * scale).to(torch.bfloat16).to(dev)

@@ -57,6 +57,9 @@ struct alignas(64) KParams {
   int b_tap_base, b_tap_dr, b_tap_ds;  // weight tap of A tap (r, s): base - r*dr - s*ds
   int out_mode;  // 0 generic stores, 1 TMA store, 2 TMA reduce-add (accumulate_out)
   int stages;  // smem ring depth (<= Cfg::kStages)
+  // B resident: every CTA uses the same B (one n tile, no split) and all of
+  // it fits next to the ring: loaded once per CTA, the ring carries A only
+  int b_res;
   int m_tiles, n_tiles, splits;  // persistent tile space
   // fused BatchNorm apply (re-forward): out2 = [relu](bf16(D) * scale + shift)
   const float* bn_scale;
@@ -172,12 +175,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   // generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nst = p.stages;
-  uint8_t* stage_buf = smem + nst * C::kStage;  // epilogue staging, then the column sums
+  // ring stages (A + B, or A only with B resident), [resident B], epilogue
+  // staging, column sums, barriers
+  const int stage_bytes = p.b_res ? kTileA : C::kStage;
+  uint8_t* b_base = smem + nst * stage_bytes;
+  uint8_t* stage_buf = b_base + (p.b_res ? p.num_kb * C::kTileB : 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + C::kStaging + C::kStats);
   uint64_t* empty = full + nst;
   uint64_t* acc_full = empty + nst;   // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2; // [2] epilogue -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* b_full = acc_empty + 2;   // resident B landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1);
 
   const uint32_t warp = warp_id();
   // persistent unit loop: CTA (pair) t0 takes units t0, t0 + tstep, ...
@@ -197,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    mbar_init(b_full, 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], PAIR ? 2 * kEpiWarps : kEpiWarps);  // one arrive per epilogue warp (of both CTAs)
@@ -245,6 +254,42 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         else
           tma_load_im2col(dst, m, bar, c, w, h, n, s, r);
       };
+      // the B tile of K block kb (this CTA's columns from n0b) -> sb
+      auto load_b = [&](uint8_t* sb, uint64_t* bar, int kb, int n0b) {
+        switch (p.b_kind) {
+          case (int)Operand::KMajor2D:  // box of BNB rows
+            ld2(sb, &p.tb, bar, kb * kBlockK, n0b);
+            break;
+          case (int)Operand::MNMajor2D:
+#pragma unroll
+            for (int j = 0; j < BNB / 64; ++j) ld2(sb + j * 8192, &p.tb, bar, n0b + 64 * j, kb * kBlockK);
+            break;
+          case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
+            const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
+            const int tr = tap / p.g_S, ts = tap - tr * p.g_S;
+            const int ftap = p.b_tap_base - tr * p.b_tap_dr - ts * p.b_tap_ds;
+#pragma unroll
+            for (int j = 0; j < BNB / 64; ++j) ld3(sb + j * 8192, &p.tb, bar, n0b + 64 * j, ftap, cb * 64);
+            break;
+          }
+          default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
+            int bw, bh, bn;
+            pixel_base(p, kb * kBlockK, bw, bh, bn);
+#pragma unroll
+            for (int j = 0; j < BNB / 64; ++j) {
+              const int nb = n0b / 64 + j;
+              const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
+              const int r = tap / p.g_S, s = tap - r * p.g_S;
+              ldi(sb + j * 8192, &p.tb, bar, cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+            }
+          }
+        }
+      };
+      if (p.b_res && t0 < total) {
+        // the whole B once (one n tile, one split: every tile of this CTA uses it)
+        mbar_arrive_expect_tx(b_full, (uint32_t)(p.num_kb * C::kTileB));
+        for (int kb = 0; kb < p.num_kb; ++kb) load_b(b_base + kb * C::kTileB, b_full, kb, 0);
+      }
       for (int t = t0; t < total; t += tstep) {
         const TileCoord tc = tile_coord<PAIR>(p, t, BN, rank);
         const int n0b = tc.n0 + rank * BNB;
@@ -252,9 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (p.a_kind == (int)Operand::Im2colK) pixel_base(p, tc.m0, aw, ah, an);
         for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * C::kStage;
+          uint8_t* sa = smem + stage * stage_bytes;
           uint8_t* sb = sa + kTileA;
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], PAIR ? 2 * C::kStage : C::kStage);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], PAIR ? 2 * C::kStage : (uint32_t)stage_bytes);
           switch (p.a_kind) {
             case (int)Operand::KMajor2D:
               ld2(sa, &p.ta, &full[stage], kb * kBlockK, tc.m0);
@@ -269,34 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               ldi(sa, &p.ta, &full[stage], cb * 64, aw, ah, an, (uint16_t)s, (uint16_t)r);
             }
           }
-          switch (p.b_kind) {
-            case (int)Operand::KMajor2D:  // box of BNB rows
-              ld2(sb, &p.tb, &full[stage], kb * kBlockK, n0b);
-              break;
-            case (int)Operand::MNMajor2D:
-#pragma unroll
-              for (int j = 0; j < BNB / 64; ++j) ld2(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, kb * kBlockK);
-              break;
-            case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
-              const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
-              const int tr = tap / p.g_S, ts = tap - tr * p.g_S;
-              const int ftap = p.b_tap_base - tr * p.b_tap_dr - ts * p.b_tap_ds;
-#pragma unroll
-              for (int j = 0; j < BNB / 64; ++j) ld3(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, ftap, cb * 64);
-              break;
-            }
-            default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
-              int bw, bh, bn;
-              pixel_base(p, kb * kBlockK, bw, bh, bn);
-#pragma unroll
-              for (int j = 0; j < BNB / 64; ++j) {
-                const int nb = n0b / 64 + j;
-                const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
-                const int r = tap / p.g_S, s = tap - r * p.g_S;
-                ldi(sb + j * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
-              }
-            }
-          }
+          if (!p.b_res) load_b(sb, &full[stage], kb, n0b);
           if (++stage == nst) {
             stage = 0;
             phase ^= 1;
@@ -324,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
+    if (p.b_res && t0 < total) mbar_wait(b_full, 0);
     // (pair: the rank-1 CTA issues nothing; the leader's MMAs fill both TMEMs)
     for (int t = t0; t < ((EXT && p.replay) || rank != 0 ? 0 : total); t += tstep, ++local) {
       const TileCoord tc = tile_coord<PAIR>(p, t, BN, rank);
@@ -344,8 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t sa = smem_u32(smem + stage * C::kStage);
-          const uint32_t sb = sa + kTileA;
+          const uint32_t sa = smem_u32(smem + stage * stage_bytes);
+          const uint32_t sb = p.b_res ? smem_u32(b_base + kb * C::kTileB) : sa + kTileA;
 #pragma unroll
           for (int kk = 0; kk < (p.experiment == 4 ? 0 : kBlockK / 16); ++kk) {
             const uint64_t da = a_mn ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
@@ -812,10 +831,11 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   using CP = Cfg<BN, true>;
   static bool configured = false;
   if (!configured) {
+    // (the B-resident layout may use up to kSmemMax)
     cudaError_t e =
-        cudaFuncSetAttribute(gemm_kernel<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        cudaFuncSetAttribute(gemm_kernel<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(gemm_kernel<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+      e = cudaFuncSetAttribute(gemm_kernel<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_kernel<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::kSmem);
     if (e != cudaSuccess) return e;
@@ -862,7 +882,25 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + 256;
     return launch_k_cluster(gemm_kernel<BN, false, true>, grid, kThreads, smem, st, 2, kp);
   }
-  const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
+  // B resident (RFK_GEMM_BRES=0 turns it off): A through TMA im2col, one n
+  // tile, no split, several tiles per CTA, and B fits beside an A-only ring
+  // of >= 4 stages.  The B bytes a CTA pulls through L2 drop from (tiles x B)
+  // to one B: for the N = 64 3x3 convs B is a third of the operand feed that
+  // bounds them (probe: 29.4 -> 27.1 us; plain 2-D A measured 4-6 % slower).
+  static const bool bres_on = [] {
+    const char* e = std::getenv("RFK_GEMM_BRES");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  const long b_bytes = (long)kp.num_kb * C::kTileB;
+  const long fixed = C::kStaging + C::kStats + 1024 + 256;
+  if (bres_on && !kp.replay && kp.a_kind == (int)Operand::Im2colK && n_tiles == 1 && splits == 1 && total > grid && force_stages < 2 &&
+      fixed + b_bytes + 4L * kTileA <= C::kSmemMax) {
+    kp.b_res = 1;
+    const long ring = std::min<long>((C::kSmemMax - fixed - b_bytes) / kTileA, 12);
+    kp.stages = (int)std::max<long>(2, std::min<long>(ring, kb_per_cta));
+  }
+  const int smem = kp.b_res ? (int)(kp.stages * kTileA + b_bytes + fixed)
+                            : kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
   if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true, false>, grid, kThreads, smem, st, kp);
   return launch_k(gemm_kernel<BN, false, false>, grid, kThreads, smem, st, kp);
 }

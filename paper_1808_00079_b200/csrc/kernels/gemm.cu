@@ -32,6 +32,7 @@ constexpr int kBlockK = 64;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kTileA = kBlockM * kBlockK * 2;  // 16 KB
+constexpr int kBarBytes = 512;                 // mbarriers + TMEM slot
 
 struct alignas(64) KParams {
   CUtensorMap ta;  // 64-byte aligned, must be first
@@ -77,7 +78,8 @@ struct alignas(64) KParams {
   const float* bs_scale;
   const float* bs_shift;
   int experiment;  // tuning only: 2 drop the output, 3 also skip TMEM loads, 4 also skip the MMAs,
-                  // 5 skip the statistics smem reads, 6 skip the statistics accumulation
+                  // 5 skip the statistics smem reads, 6 skip the statistics accumulation,
+                  // 12 no operand loads (MMAs on stale smem), 13 = 12 with an empty epilogue
 };
 
 template <int BN, bool PAIR = false>
@@ -92,9 +94,9 @@ struct Cfg {
   static constexpr int kStats = kEpiWarps * 2 * (BN / 2) * 4;  // per-warp sums of the warp's own columns
   // as deep a TMA ring as the 227 KB of dynamic shared memory allows
   static constexpr int kSmemMax = 232448;
-  static constexpr int kStages = (kSmemMax - kStaging - kStats - 1024 - 256) / kStage;
+  static constexpr int kStages = (kSmemMax - kStaging - kStats - 1024 - kBarBytes) / kStage;
   static_assert(kStages >= 3, "ring too shallow");
-  static constexpr int kSmem = kStages * kStage + kStaging + kStats + 1024 /*align*/ + 256;
+  static constexpr int kSmem = kStages * kStage + kStaging + kStats + 1024 /*align*/ + kBarBytes;
 };
 
 // Decode a flattened output-pixel index into im2col TMA base coordinates.
@@ -229,7 +231,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
-    if (elect_one() && !(EXT && p.replay)) {
+    if (elect_one() && !(EXT && p.replay) && p.experiment < 12) {
+      // (15/16: 12 with 1/2 MMAs per K block; 17: 12 without the per-K-block
+      // commit; 18: 12 without the tcgen05 fence after the barrier wait)
       int stage = 0;
       uint32_t phase = 0;
       // this CTA's B columns: all BN, or (pair) the half n0 + rank * BN/2
@@ -360,13 +364,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         continue;
       }
       for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
+        if (p.experiment < 12) mbar_wait(&full[stage], phase);
+        if (p.experiment != 18) tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(smem + stage * stage_bytes);
           const uint32_t sb = p.b_res ? smem_u32(b_base + kb * C::kTileB) : sa + kTileA;
-#pragma unroll
-          for (int kk = 0; kk < (p.experiment == 4 ? 0 : kBlockK / 16); ++kk) {
+          auto issue = [&](int kk) {
             const uint64_t da = a_mn ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
                                      : umma_desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
@@ -375,8 +378,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               umma_bf16_pair(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
             else
               umma_bf16(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
+          };
+          if (p.experiment == 0 || (p.experiment < 15 && p.experiment != 4) || p.experiment > 16) {
+#pragma unroll
+            for (int kk = 0; kk < kBlockK / 16; ++kk) issue(kk);
+          } else {
+            for (int kk = 0; kk < (p.experiment == 4 ? 0 : p.experiment - 14); ++kk) issue(kk);
           }
-          if (PAIR) {
+          if (p.experiment == 17) {
+            if (kb + 1 == tc.kb_end) umma_commit(&acc_full[acc]);
+          } else if (PAIR) {
             umma_commit_pair(&empty[stage]);
             if (kb + 1 == tc.kb_end) umma_commit_pair(&acc_full[acc]);
           } else {
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               r[8 * j + 2 * e + 1] = uw[e] & 0xffff0000u;  // high bf16 -> fp32 bits
             }
           }
-        } else if (!empty_k && (p.experiment < 3 || p.experiment > 4)) {
+        } else if (!empty_k && (p.experiment < 3 || (p.experiment > 4 && p.experiment < 13))) {
           tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
           tmem_ld_wait();
         } else {
@@ -527,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int col0 = tc.n0 + c0;
-        if (col0 >= p.N || (p.experiment >= 2 && p.experiment <= 4)) continue;  // warp-uniform
+        if (col0 >= p.N || (p.experiment >= 2 && p.experiment <= 4) || p.experiment >= 13) continue;  // warp-uniform
         const bool full_cols = col0 + 32 <= p.N;
         if (p.bias) {
 #pragma unroll
@@ -879,7 +890,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   kp.experiment = experiment;
   if (experiment == 1) kp.out_mode = 0;
   if (pair) {
-    const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + 256;
+    const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + kBarBytes;
     return launch_k_cluster(gemm_kernel<BN, false, true>, grid, kThreads, smem, st, 2, kp);
   }
   // B resident (RFK_GEMM_BRES=0 turns it off): A through TMA im2col, one n
@@ -892,15 +903,15 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     return e == nullptr || std::atoi(e) != 0;
   }();
   const long b_bytes = (long)kp.num_kb * C::kTileB;
-  const long fixed = C::kStaging + C::kStats + 1024 + 256;
-  if (bres_on && !kp.replay && kp.a_kind == (int)Operand::Im2colK && n_tiles == 1 && splits == 1 && total > grid && force_stages < 2 &&
+  const long fixed = C::kStaging + C::kStats + 1024 + kBarBytes;
+  if (bres_on && !kp.replay && experiment < 12 && kp.a_kind == (int)Operand::Im2colK && n_tiles == 1 && splits == 1 && total > grid && force_stages < 2 &&
       fixed + b_bytes + 4L * kTileA <= C::kSmemMax) {
     kp.b_res = 1;
     const long ring = std::min<long>((C::kSmemMax - fixed - b_bytes) / kTileA, 12);
     kp.stages = (int)std::max<long>(2, std::min<long>(ring, kb_per_cta));
   }
   const int smem = kp.b_res ? (int)(kp.stages * kTileA + b_bytes + fixed)
-                            : kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
+                            : kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + kBarBytes;
   if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true, false>, grid, kThreads, smem, st, kp);
   return launch_k(gemm_kernel<BN, false, false>, grid, kThreads, smem, st, kp);
 }

@@ -32,7 +32,6 @@ constexpr int kBlockK = 64;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kTileA = kBlockM * kBlockK * 2;  // 16 KB
-constexpr int kBarBytes = 512;                 // mbarriers + TMEM slot
 
 struct alignas(64) KParams {
   CUtensorMap ta;  // 64-byte aligned, must be first
@@ -58,9 +57,6 @@ struct alignas(64) KParams {
   int b_tap_base, b_tap_dr, b_tap_ds;  // weight tap of A tap (r, s): base - r*dr - s*ds
   int out_mode;  // 0 generic stores, 1 TMA store, 2 TMA reduce-add (accumulate_out)
   int stages;  // smem ring depth (<= Cfg::kStages)
-  // B resident: every CTA uses the same B (one n tile, no split) and all of
-  // it fits next to the ring: loaded once per CTA, the ring carries A only
-  int b_res;
   int m_tiles, n_tiles, splits;  // persistent tile space
   // fused BatchNorm apply (re-forward): out2 = [relu](bf16(D) * scale + shift)
   const float* bn_scale;
@@ -78,8 +74,7 @@ struct alignas(64) KParams {
   const float* bs_scale;
   const float* bs_shift;
   int experiment;  // tuning only: 2 drop the output, 3 also skip TMEM loads, 4 also skip the MMAs,
-                  // 5 skip the statistics smem reads, 6 skip the statistics accumulation,
-                  // 12 no operand loads (MMAs on stale smem), 13 = 12 with an empty epilogue
+                  // 5 skip the statistics smem reads, 6 skip the statistics accumulation
 };
 
 template <int BN, bool PAIR = false>
@@ -94,9 +89,9 @@ struct Cfg {
   static constexpr int kStats = kEpiWarps * 2 * (BN / 2) * 4;  // per-warp sums of the warp's own columns
   // as deep a TMA ring as the 227 KB of dynamic shared memory allows
   static constexpr int kSmemMax = 232448;
-  static constexpr int kStages = (kSmemMax - kStaging - kStats - 1024 - kBarBytes) / kStage;
+  static constexpr int kStages = (kSmemMax - kStaging - kStats - 1024 - 256) / kStage;
   static_assert(kStages >= 3, "ring too shallow");
-  static constexpr int kSmem = kStages * kStage + kStaging + kStats + 1024 /*align*/ + kBarBytes;
+  static constexpr int kSmem = kStages * kStage + kStaging + kStats + 1024 /*align*/ + 256;
 };
 
 // Decode a flattened output-pixel index into im2col TMA base coordinates.
@@ -168,7 +163,11 @@ __device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const 
 // by it.  Each CTA's epilogue drains its own TMEM (its 128 rows, all BN
 // columns); the accumulator is released once both epilogues arrived on the
 // leader's barrier.
-template <int BN, bool EXT, bool PAIR>
+//
+// RES: B resident -- every CTA uses the same B (one n tile, no split) and all
+// of it sits in shared memory beside an A-only ring: loaded once per CTA.  A
+// separate instance, so the other variants keep their code and registers.
+template <int BN, bool EXT, bool PAIR, bool RES = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<BN, PAIR>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -177,17 +176,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   // generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nst = p.stages;
-  // ring stages (A + B, or A only with B resident), [resident B], epilogue
-  // staging, column sums, barriers
-  const int stage_bytes = p.b_res ? kTileA : C::kStage;
-  uint8_t* b_base = smem + nst * stage_bytes;
-  uint8_t* stage_buf = b_base + (p.b_res ? p.num_kb * C::kTileB : 0);
+  // ring stages (A + B; A only with RES), [resident B], epilogue staging,
+  // column sums, barriers
+  constexpr int kStageBytes = RES ? kTileA : C::kStage;
+  uint8_t* b_base = smem + nst * kStageBytes;
+  uint8_t* stage_buf = RES ? b_base + p.num_kb * C::kTileB : b_base;  // epilogue staging, then the column sums
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + C::kStaging + C::kStats);
   uint64_t* empty = full + nst;
   uint64_t* acc_full = empty + nst;   // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2; // [2] epilogue -> MMA
-  uint64_t* b_full = acc_empty + 2;   // resident B landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // RES: B landed
 
   const uint32_t warp = warp_id();
   // persistent unit loop: CTA (pair) t0 takes units t0, t0 + tstep, ...
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(b_full, 1);
+    if (RES) mbar_init(b_full, 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], PAIR ? 2 * kEpiWarps : kEpiWarps);  // one arrive per epilogue warp (of both CTAs)
@@ -231,9 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
-    if (elect_one() && !(EXT && p.replay) && p.experiment < 12) {
-      // (15/16: 12 with 1/2 MMAs per K block; 17: 12 without the per-K-block
-      // commit; 18: 12 without the tcgen05 fence after the barrier wait)
+    if (elect_one() && !(EXT && p.replay)) {
       int stage = 0;
       uint32_t phase = 0;
       // this CTA's B columns: all BN, or (pair) the half n0 + rank * BN/2
@@ -258,41 +255,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         else
           tma_load_im2col(dst, m, bar, c, w, h, n, s, r);
       };
-      // the B tile of K block kb (this CTA's columns from n0b) -> sb
-      auto load_b = [&](uint8_t* sb, uint64_t* bar, int kb, int n0b) {
-        switch (p.b_kind) {
-          case (int)Operand::KMajor2D:  // box of BNB rows
-            ld2(sb, &p.tb, bar, kb * kBlockK, n0b);
-            break;
-          case (int)Operand::MNMajor2D:
+      if constexpr (RES) {
+        // the whole B once (one n tile, no split: every tile of this CTA uses it)
+        if (t0 < total) {
+          mbar_arrive_expect_tx(b_full, (uint32_t)(p.num_kb * C::kTileB));
+          for (int kb = 0; kb < p.num_kb; ++kb) {
+            uint8_t* sb = b_base + kb * C::kTileB;
+            switch (p.b_kind) {
+              case (int)Operand::KMajor2D:
+                tma_load_2d(sb, &p.tb, b_full, kb * kBlockK, 0);
+                break;
+              case (int)Operand::MNMajor2D:
 #pragma unroll
-            for (int j = 0; j < BNB / 64; ++j) ld2(sb + j * 8192, &p.tb, bar, n0b + 64 * j, kb * kBlockK);
-            break;
-          case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
-            const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
-            const int tr = tap / p.g_S, ts = tap - tr * p.g_S;
-            const int ftap = p.b_tap_base - tr * p.b_tap_dr - ts * p.b_tap_ds;
+                for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &p.tb, b_full, 64 * j, kb * kBlockK);
+                break;
+              default: {  // WeightTapsMN
+                const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
+                const int tr = tap / p.g_S, ts = tap - tr * p.g_S;
+                const int ftap = p.b_tap_base - tr * p.b_tap_dr - ts * p.b_tap_ds;
 #pragma unroll
-            for (int j = 0; j < BNB / 64; ++j) ld3(sb + j * 8192, &p.tb, bar, n0b + 64 * j, ftap, cb * 64);
-            break;
-          }
-          default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
-            int bw, bh, bn;
-            pixel_base(p, kb * kBlockK, bw, bh, bn);
-#pragma unroll
-            for (int j = 0; j < BNB / 64; ++j) {
-              const int nb = n0b / 64 + j;
-              const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
-              const int r = tap / p.g_S, s = tap - r * p.g_S;
-              ldi(sb + j * 8192, &p.tb, bar, cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+                for (int j = 0; j < BN / 64; ++j) tma_load_3d(sb + j * 8192, &p.tb, b_full, 64 * j, ftap, cb * 64);
+              }
             }
           }
         }
-      };
-      if (p.b_res && t0 < total) {
-        // the whole B once (one n tile, one split: every tile of this CTA uses it)
-        mbar_arrive_expect_tx(b_full, (uint32_t)(p.num_kb * C::kTileB));
-        for (int kb = 0; kb < p.num_kb; ++kb) load_b(b_base + kb * C::kTileB, b_full, kb, 0);
       }
       for (int t = t0; t < total; t += tstep) {
         const TileCoord tc = tile_coord<PAIR>(p, t, BN, rank);
@@ -301,9 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         if (p.a_kind == (int)Operand::Im2colK) pixel_base(p, tc.m0, aw, ah, an);
         for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * stage_bytes;
+          uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + kTileA;
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], PAIR ? 2 * C::kStage : (uint32_t)stage_bytes);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], PAIR ? 2 * C::kStage : kStageBytes);
           switch (p.a_kind) {
             case (int)Operand::KMajor2D:
               ld2(sa, &p.ta, &full[stage], kb * kBlockK, tc.m0);
@@ -318,7 +304,34 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               ldi(sa, &p.ta, &full[stage], cb * 64, aw, ah, an, (uint16_t)s, (uint16_t)r);
             }
           }
-          if (!p.b_res) load_b(sb, &full[stage], kb, n0b);
+          if (!RES) switch (p.b_kind) {
+            case (int)Operand::KMajor2D:  // box of BNB rows
+              ld2(sb, &p.tb, &full[stage], kb * kBlockK, n0b);
+              break;
+            case (int)Operand::MNMajor2D:
+#pragma unroll
+              for (int j = 0; j < BNB / 64; ++j) ld2(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, kb * kBlockK);
+              break;
+            case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
+              const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
+              const int tr = tap / p.g_S, ts = tap - tr * p.g_S;
+              const int ftap = p.b_tap_base - tr * p.b_tap_dr - ts * p.b_tap_ds;
+#pragma unroll
+              for (int j = 0; j < BNB / 64; ++j) ld3(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, ftap, cb * 64);
+              break;
+            }
+            default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
+              int bw, bh, bn;
+              pixel_base(p, kb * kBlockK, bw, bh, bn);
+#pragma unroll
+              for (int j = 0; j < BNB / 64; ++j) {
+                const int nb = n0b / 64 + j;
+                const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
+                const int r = tap / p.g_S, s = tap - r * p.g_S;
+                ldi(sb + j * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+              }
+            }
+          }
           if (++stage == nst) {
             stage = 0;
             phase ^= 1;
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    if (p.b_res && t0 < total) mbar_wait(b_full, 0);
+    if (RES && t0 < total) mbar_wait(b_full, 0);
     // (pair: the rank-1 CTA issues nothing; the leader's MMAs fill both TMEMs)
     for (int t = t0; t < ((EXT && p.replay) || rank != 0 ? 0 : total); t += tstep, ++local) {
       const TileCoord tc = tile_coord<PAIR>(p, t, BN, rank);
@@ -364,12 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         continue;
       }
       for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
-        if (p.experiment < 12) mbar_wait(&full[stage], phase);
-        if (p.experiment != 18) tc_fence_after();
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
         if (elect_one()) {
-          const uint32_t sa = smem_u32(smem + stage * stage_bytes);
-          const uint32_t sb = p.b_res ? smem_u32(b_base + kb * C::kTileB) : sa + kTileA;
-          auto issue = [&](int kk) {
+          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+          const uint32_t sb = RES ? smem_u32(b_base + kb * C::kTileB) : sa + kTileA;
+#pragma unroll
+          for (int kk = 0; kk < (p.experiment == 4 ? 0 : kBlockK / 16); ++kk) {
             const uint64_t da = a_mn ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
                                      : umma_desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
@@ -378,16 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               umma_bf16_pair(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
             else
               umma_bf16(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
-          };
-          if (p.experiment == 0 || (p.experiment < 15 && p.experiment != 4) || p.experiment > 16) {
-#pragma unroll
-            for (int kk = 0; kk < kBlockK / 16; ++kk) issue(kk);
-          } else {
-            for (int kk = 0; kk < (p.experiment == 4 ? 0 : p.experiment - 14); ++kk) issue(kk);
           }
-          if (p.experiment == 17) {
-            if (kb + 1 == tc.kb_end) umma_commit(&acc_full[acc]);
-          } else if (PAIR) {
+          if (PAIR) {
             umma_commit_pair(&empty[stage]);
             if (kb + 1 == tc.kb_end) umma_commit_pair(&acc_full[acc]);
           } else {
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               r[8 * j + 2 * e + 1] = uw[e] & 0xffff0000u;  // high bf16 -> fp32 bits
             }
           }
-        } else if (!empty_k && (p.experiment < 3 || (p.experiment > 4 && p.experiment < 13))) {
+        } else if (!empty_k && (p.experiment < 3 || p.experiment > 4)) {
           tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
           tmem_ld_wait();
         } else {
@@ -538,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int col0 = tc.n0 + c0;
-        if (col0 >= p.N || (p.experiment >= 2 && p.experiment <= 4) || p.experiment >= 13) continue;  // warp-uniform
+        if (col0 >= p.N || (p.experiment >= 2 && p.experiment <= 4)) continue;  // warp-uniform
         const bool full_cols = col0 + 32 <= p.N;
         if (p.bias) {
 #pragma unroll
@@ -842,11 +848,10 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   using CP = Cfg<BN, true>;
   static bool configured = false;
   if (!configured) {
-    // (the B-resident layout may use up to kSmemMax)
     cudaError_t e =
-        cudaFuncSetAttribute(gemm_kernel<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
+        cudaFuncSetAttribute(gemm_kernel<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(gemm_kernel<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
+      e = cudaFuncSetAttribute(gemm_kernel<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_kernel<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::kSmem);
     if (e != cudaSuccess) return e;
@@ -890,28 +895,40 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   kp.experiment = experiment;
   if (experiment == 1) kp.out_mode = 0;
   if (pair) {
-    const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + kBarBytes;
+    const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + 256;
     return launch_k_cluster(gemm_kernel<BN, false, true>, grid, kThreads, smem, st, 2, kp);
   }
   // B resident (RFK_GEMM_BRES=0 turns it off): A through TMA im2col, one n
-  // tile, no split, several tiles per CTA, and B fits beside an A-only ring
-  // of >= 4 stages.  The B bytes a CTA pulls through L2 drop from (tiles x B)
-  // to one B: for the N = 64 3x3 convs B is a third of the operand feed that
-  // bounds them (probe: 29.4 -> 27.1 us; plain 2-D A measured 4-6 % slower).
+  // tile, no split, several tiles per CTA, and B fits beside an A-only ring of
+  // >= 4 stages.  The B bytes a CTA pulls through L2 drop from (tiles x B) to
+  // one B: for the N = 64 3x3 convs B is a third of the operand feed that
+  // bounds them (tools/gemm_probe.py: 29.4 -> 27.1 us).
   static const bool bres_on = [] {
     const char* e = std::getenv("RFK_GEMM_BRES");
     return e == nullptr || std::atoi(e) != 0;
   }();
   const long b_bytes = (long)kp.num_kb * C::kTileB;
-  const long fixed = C::kStaging + C::kStats + 1024 + kBarBytes;
-  if (bres_on && !kp.replay && experiment < 12 && kp.a_kind == (int)Operand::Im2colK && n_tiles == 1 && splits == 1 && total > grid && force_stages < 2 &&
+  const long fixed = C::kStaging + C::kStats + 1024 + 256;
+  if (bres_on && !kp.replay && kp.a_kind == (int)Operand::Im2colK && kp.b_kind != (int)Operand::Im2colMN &&
+      n_tiles == 1 && splits == 1 && total > grid && force_stages < 2 && experiment == 0 &&
       fixed + b_bytes + 4L * kTileA <= C::kSmemMax) {
-    kp.b_res = 1;
+    static bool res_configured = false;
+    if (!res_configured) {
+      cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(gemm_kernel<BN, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::kSmemMax);
+      if (e != cudaSuccess) return e;
+      res_configured = true;
+    }
     const long ring = std::min<long>((C::kSmemMax - fixed - b_bytes) / kTileA, 12);
     kp.stages = (int)std::max<long>(2, std::min<long>(ring, kb_per_cta));
+    const int smem = (int)(kp.stages * kTileA + b_bytes + fixed);
+    if (kp.stats_bwd) return launch_k(gemm_kernel<BN, true, false, true>, grid, kThreads, smem, st, kp);
+    return launch_k(gemm_kernel<BN, false, false, true>, grid, kThreads, smem, st, kp);
   }
-  const int smem = kp.b_res ? (int)(kp.stages * kTileA + b_bytes + fixed)
-                            : kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + kBarBytes;
+  const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
   if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true, false>, grid, kThreads, smem, st, kp);
   return launch_k(gemm_kernel<BN, false, false>, grid, kThreads, smem, st, kp);
 }

@@ -67,8 +67,7 @@ struct alignas(64) BandParams {
   int flat;        // band rows as 2-D boxes over the flat pixel array + fix-up of the padding lines
   int H, W;
   int b_resident;  // all taps x chunks of B fit the ring: loaded once per CTA, never released
-  int experiment;  // tuning only: 2 drop the output, 4 also skip the MMAs, 7 skip the band loads (MMAs on
-                   // stale smem), 8 = 7 with every tap's start row rounded down to a multiple of 8
+  int experiment;  // tuning only: 2 drop the output, 4 also skip the MMAs
   unsigned long long* dbg;  // tuning only: per-tile timestamps of CTA 0
 };
 
@@ -182,11 +181,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
               tma_load_2d(band + bs * p.band_bytes + rr * p.Wp * 128, &p.ta2, &band_full[bs], cb * 64,
                           (img * p.H + h) * p.W - p.pw);
             }
-          } else if (p.experiment >= 7)
-            mbar_arrive(&band_full[bs]);
-          else
+          } else
           mbar_arrive_expect_tx(&band_full[bs], p.box_bytes);
-          if (p.flat || p.experiment >= 7) {
+          if (p.flat) {
           } else if (p.row_boxes) {  // one {64, Wp, 1, 1} box per band row
             for (int rr = 0; rr < p.BR; ++rr)
               tma_load_4d(band + bs * p.band_bytes + rr * p.Wp * 128, &p.ta, &band_full[bs], cb * 64, -p.pw,
@@ -243,16 +240,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
           tc_fence_after();
           if (elect_one()) {
             const int r = tap / p.S, c = tap - r * p.S;
-            uint32_t row = (uint32_t)(row0 + r * p.Wp + c);
-            if (p.experiment == 8) row &= ~7u;
+            const uint32_t row = (uint32_t)(row0 + r * p.Wp + c);
             const uint32_t sa = sa0 + row * 128u;
             const uint32_t sb = smem_u32(bring + slot * kTileB);
 #pragma unroll
             for (int kk = 0; kk < (p.experiment == 4 ? 0 : 4); ++kk) {
               const uint64_t da = desc_sw128_rows(sa + kk * 32);
               const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024) : umma_desc_sw128(sb + kk * 32, 16, 1024);
-              const uint32_t dt = (p.experiment == 9 && (kk & 1)) ? tmem + (uint32_t)((acc ^ 1) * kTmemCols) : d_tmem;
-              umma_bf16(dt, da, db, idesc, (cb > 0 || tap > 0 || kk > 0) ? 1u : 0u);
+              umma_bf16(d_tmem, da, db, idesc, (cb > 0 || tap > 0 || kk > 0) ? 1u : 0u);
             }
             if (!p.b_resident) umma_commit(&b_empty[s]);
             if (tap + 1 == p.taps) {

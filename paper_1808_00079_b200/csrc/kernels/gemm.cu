@@ -23,6 +23,13 @@
 #include "kernels/launch.cuh"
 #include "kernels/ptx.cuh"
 
+// Timing-experiment switches (KParams::experiment) exist only in tuning
+// builds: as runtime branches in the MMA and epilogue loops they cost the
+// production kernel measurable time.
+#ifndef RFK_GEMM_TUNING
+#define RFK_GEMM_TUNING 0
+#endif
+
 namespace rfk {
 
 namespace {
@@ -73,8 +80,9 @@ struct alignas(64) KParams {
   const float* bs_mean;
   const float* bs_scale;
   const float* bs_shift;
-  int experiment;  // tuning only: 2 drop the output, 3 also skip TMEM loads, 4 also skip the MMAs,
-                  // 5 skip the statistics smem reads, 6 skip the statistics accumulation
+  int experiment;  // tuning only (builds with RFK_GEMM_TUNING=1): 2 drop the output, 3 also skip TMEM
+                  // loads, 4 also skip the MMAs, 5 skip the statistics smem reads, 6 skip the statistics
+                  // accumulation
 };
 
 template <int BN, bool PAIR = false>
@@ -189,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   uint64_t* b_full = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // RES: B landed
 
   const uint32_t warp = warp_id();
+  const int ex = RFK_GEMM_TUNING ? p.experiment : 0;
   // persistent unit loop: CTA (pair) t0 takes units t0, t0 + tstep, ...
   const int rank = PAIR ? (int)cluster_ctarank() : 0;
   const int t0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           const uint32_t sa = smem_u32(smem + stage * kStageBytes);
           const uint32_t sb = RES ? smem_u32(b_base + kb * C::kTileB) : sa + kTileA;
 #pragma unroll
-          for (int kk = 0; kk < (p.experiment == 4 ? 0 : kBlockK / 16); ++kk) {
+          for (int kk = 0; kk < (ex == 4 ? 0 : kBlockK / 16); ++kk) {
             const uint64_t da = a_mn ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
                                      : umma_desc_sw128(sa + kk * 32, 16, 1024);
             const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               r[8 * j + 2 * e + 1] = uw[e] & 0xffff0000u;  // high bf16 -> fp32 bits
             }
           }
-        } else if (!empty_k && (p.experiment < 3 || p.experiment > 4)) {
+        } else if (!empty_k && (ex < 3 || ex > 4)) {
           tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
           tmem_ld_wait();
         } else {
@@ -544,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int col0 = tc.n0 + c0;
-        if (col0 >= p.N || (p.experiment >= 2 && p.experiment <= 4)) continue;  // warp-uniform
+        if (col0 >= p.N || (ex >= 2 && ex <= 4)) continue;  // warp-uniform
         const bool full_cols = col0 + 32 <= p.N;
         if (p.bias) {
 #pragma unroll
@@ -705,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
             }
           } else {
 #pragma unroll
-          for (int rr = 0; rr < (p.experiment == 5 ? 0 : 16); ++rr) {
+          for (int rr = 0; rr < (ex == 5 ? 0 : 16); ++rr) {
             const uint32_t row = 2 * rr + par;
             const uint32_t off = row * 64 + (((cp >> 2) ^ ((row >> 1) & 3u)) * 16) + (cp & 3) * 4;
             const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sbuf + off));
@@ -719,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
           q0 += __shfl_xor_sync(0xffffffffu, q0, 16);
           q1 += __shfl_xor_sync(0xffffffffu, q1, 16);
-          if (lane < 16 && p.experiment != 6) {
+          if (lane < 16 && ex != 6) {
             const int lc = ((c0 >> 6) << 5) + 2 * (int)lane;  // this warp's local column
             my_sum[lc] += s0;
             my_sum[lc + 1] += s1;

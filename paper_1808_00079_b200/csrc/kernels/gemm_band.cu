@@ -34,6 +34,10 @@
 #include "kernels/launch.cuh"
 #include "kernels/ptx.cuh"
 
+#ifndef RFK_GEMM_TUNING
+#define RFK_GEMM_TUNING 0
+#endif
+
 namespace rfk {
 
 namespace {
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
             const uint32_t sa = sa0 + row * 128u;
             const uint32_t sb = smem_u32(bring + slot * kTileB);
 #pragma unroll
-            for (int kk = 0; kk < (p.experiment == 4 ? 0 : 4); ++kk) {
+            for (int kk = 0; kk < ((RFK_GEMM_TUNING && p.experiment == 4) ? 0 : 4); ++kk) {
               const uint64_t da = desc_sw128_rows(sa + kk * 32);
               const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024) : umma_desc_sw128(sb + kk * 32, 16, 1024);
               umma_bf16(d_tmem, da, db, idesc, (cb > 0 || tap > 0 || kk > 0) ? 1u : 0u);
@@ -367,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
           if (lane == 0) mbar_arrive(&acc_empty[acc]);
         }
         const int col0 = nt * BN + c0;
-        if (col0 >= p.N || p.experiment >= 2) continue;
+        if (col0 >= p.N || (RFK_GEMM_TUNING && p.experiment >= 2)) continue;
         const bool full_cols = col0 + 32 <= p.N;
         uint32_t w[16];
 #pragma unroll

@@ -175,7 +175,11 @@ __device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const 
 // RES: B resident -- every CTA uses the same B (one n tile, no split) and all
 // of it sits in shared memory beside an A-only ring: loaded once per CTA.  A
 // separate instance, so the other variants keep their code and registers.
-template <int BN, bool EXT, bool PAIR, bool RES = false>
+//
+// SIMPLE: the common epilogue only -- bf16 output through TMA store / TMA
+// reduce-add, optional statistics; no fp32 output, bias, fused BN apply or
+// generic (remapped) stores compiled in.
+template <int BN, bool EXT, bool PAIR, bool RES = false, bool SIMPLE = false>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
   using C = Cfg<BN, PAIR>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -442,6 +446,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     float* wsum = reinterpret_cast<float*>(stage_buf + C::kStaging);  // [8 warps][2][HB]
     float* my_sum = wsum + ew * 2 * HB;
     const int mode = p.out_mode;
+    const bool f32 = !SIMPLE && p.out_f32;
+    const float* bias = SIMPLE ? nullptr : p.bias;
+    const bool fuse = !SIMPLE && p.fuse_bn;
+    const bool tma = SIMPLE || mode != 0;
     int buf = 0;
     auto tma_out = [&](const uint32_t(&w)[16], int cx, int my, int z) {
       epi_tma_out<NB>(p, stg + buf * 2048, w, lane, mode, cx, my, z);
@@ -555,11 +563,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int col0 = tc.n0 + c0;
         if (col0 >= p.N || (ex >= 2 && ex <= 4)) continue;  // warp-uniform
         const bool full_cols = col0 + 32 <= p.N;
-        if (p.bias) {
+        if (bias) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] += (col0 + i < p.N) ? __ldg(p.bias + col0 + i) : 0.f;
+          for (int i = 0; i < 32; ++i) v[i] += (col0 + i < p.N) ? __ldg(bias + col0 + i) : 0.f;
         }
-        if (p.out_f32) {
+        if (f32) {
           if (mode != 0) {  // two 16-column fp32 boxes
             uint32_t w[16];
 #pragma unroll
@@ -595,10 +603,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
           __syncwarp();
           sbuf = gb;
-        } else if (mode != 0) {
+        } else if (tma) {
           sbuf = stg + buf * 2048;
           tma_out(w, col0, my, tc.z);
-          if (p.fuse_bn) {
+          if (fuse) {
             // the BN that consumes this conv, applied to exactly the bf16
             // values just stored (same expression as bn_apply_kernel)
             uint32_t w2[16];
@@ -863,6 +871,9 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
       e = cudaFuncSetAttribute(gemm_kernel<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_kernel<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::kSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -907,6 +918,13 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + 256;
     return launch_k_cluster(gemm_kernel<BN, false, true>, grid, kThreads, smem, st, 2, kp);
   }
+  // the common epilogue (RFK_GEMM_SIMPLE=0 turns the specialised instance off)
+  static const bool simple_on = [] {
+    const char* e = std::getenv("RFK_GEMM_SIMPLE");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  const bool simple = simple_on && !kp.replay && !kp.stats_bwd && kp.out_mode != 0 && !kp.out_f32 && !kp.bias &&
+                      !kp.fuse_bn && experiment == 0;
   // B resident (RFK_GEMM_BRES=0 turns it off): A through TMA im2col, one n
   // tile, no split, several tiles per CTA, and B fits beside an A-only ring of
   // >= 4 stages.  The B bytes a CTA pulls through L2 drop from (tiles x B) to
@@ -928,6 +946,9 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(gemm_kernel<BN, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::kSmemMax);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, true, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
       if (e != cudaSuccess) return e;
       res_configured = true;
     }
@@ -935,10 +956,12 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     kp.stages = (int)std::max<long>(2, std::min<long>(ring, kb_per_cta));
     const int smem = (int)(kp.stages * kTileA + b_bytes + fixed);
     if (kp.stats_bwd) return launch_k(gemm_kernel<BN, true, false, true>, grid, kThreads, smem, st, kp);
+    if (simple) return launch_k(gemm_kernel<BN, false, false, true, true>, grid, kThreads, smem, st, kp);
     return launch_k(gemm_kernel<BN, false, false, true>, grid, kThreads, smem, st, kp);
   }
   const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
   if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true, false>, grid, kThreads, smem, st, kp);
+  if (simple) return launch_k(gemm_kernel<BN, false, false, false, true>, grid, kThreads, smem, st, kp);
   return launch_k(gemm_kernel<BN, false, false>, grid, kThreads, smem, st, kp);
 }
 

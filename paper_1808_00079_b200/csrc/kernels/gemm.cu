@@ -176,11 +176,13 @@ __device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const 
 // of it sits in shared memory beside an A-only ring: loaded once per CTA.  A
 // separate instance, so the other variants keep their code and registers.
 //
-// SIMPLE: the common epilogue only -- bf16 output through TMA store / TMA
-// reduce-add, optional statistics; no fp32 output, bias, fused BN apply or
-// generic (remapped) stores compiled in.
-template <int BN, bool EXT, bool PAIR, bool RES = false, bool SIMPLE = false>
+// EPI: 0 = every epilogue path; 1 = only the common one -- bf16 output through
+// TMA store / TMA reduce-add, optional statistics; 2 = only fp32 output
+// through TMA (split-K partials).  No bias, fused BN apply or generic
+// (remapped) stores compiled into 1 and 2.
+template <int BN, bool EXT, bool PAIR, bool RES = false, int EPI = 0>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
+  constexpr bool SIMPLE = EPI != 0;
   using C = Cfg<BN, PAIR>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the shared array itself, so
@@ -446,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     float* wsum = reinterpret_cast<float*>(stage_buf + C::kStaging);  // [8 warps][2][HB]
     float* my_sum = wsum + ew * 2 * HB;
     const int mode = p.out_mode;
-    const bool f32 = !SIMPLE && p.out_f32;
+    const bool f32 = EPI == 2 || (EPI == 0 && p.out_f32);
     const float* bias = SIMPLE ? nullptr : p.bias;
     const bool fuse = !SIMPLE && p.fuse_bn;
     const bool tma = SIMPLE || mode != 0;
@@ -872,7 +874,13 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_kernel<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::kSmem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_kernel<BN, true, false, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                C::kSmem);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -918,13 +926,15 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + 256;
     return launch_k_cluster(gemm_kernel<BN, false, true>, grid, kThreads, smem, st, 2, kp);
   }
-  // the common epilogue (RFK_GEMM_SIMPLE=0 turns the specialised instance off)
+  // the common epilogues (RFK_GEMM_SIMPLE=0 turns the specialised instances off)
   static const bool simple_on = [] {
     const char* e = std::getenv("RFK_GEMM_SIMPLE");
     return e == nullptr || std::atoi(e) != 0;
   }();
-  const bool simple = simple_on && !kp.replay && !kp.stats_bwd && kp.out_mode != 0 && !kp.out_f32 && !kp.bias &&
-                      !kp.fuse_bn && experiment == 0;
+  const int epi = (simple_on && !kp.replay && kp.out_mode != 0 && !kp.bias && !kp.fuse_bn && experiment == 0)
+                      ? (kp.out_f32 ? 2 : 1)
+                      : 0;
+  const bool simple = epi == 1;
   // B resident (RFK_GEMM_BRES=0 turns it off): A through TMA im2col, one n
   // tile, no split, several tiles per CTA, and B fits beside an A-only ring of
   // >= 4 stages.  The B bytes a CTA pulls through L2 drop from (tiles x B) to
@@ -947,21 +957,27 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
         e = cudaFuncSetAttribute(gemm_kernel<BN, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::kSmemMax);
       if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, true, true>,
+        e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, true, 1>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(gemm_kernel<BN, true, false, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::kSmemMax);
       if (e != cudaSuccess) return e;
       res_configured = true;
     }
     const long ring = std::min<long>((C::kSmemMax - fixed - b_bytes) / kTileA, 12);
     kp.stages = (int)std::max<long>(2, std::min<long>(ring, kb_per_cta));
     const int smem = (int)(kp.stages * kTileA + b_bytes + fixed);
+    if (kp.stats_bwd && simple) return launch_k(gemm_kernel<BN, true, false, true, 1>, grid, kThreads, smem, st, kp);
     if (kp.stats_bwd) return launch_k(gemm_kernel<BN, true, false, true>, grid, kThreads, smem, st, kp);
-    if (simple) return launch_k(gemm_kernel<BN, false, false, true, true>, grid, kThreads, smem, st, kp);
+    if (simple) return launch_k(gemm_kernel<BN, false, false, true, 1>, grid, kThreads, smem, st, kp);
     return launch_k(gemm_kernel<BN, false, false, true>, grid, kThreads, smem, st, kp);
   }
   const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
+  if (kp.stats_bwd && simple) return launch_k(gemm_kernel<BN, true, false, false, 1>, grid, kThreads, smem, st, kp);
   if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true, false>, grid, kThreads, smem, st, kp);
-  if (simple) return launch_k(gemm_kernel<BN, false, false, false, true>, grid, kThreads, smem, st, kp);
+  if (simple) return launch_k(gemm_kernel<BN, false, false, false, 1>, grid, kThreads, smem, st, kp);
+  if (epi == 2) return launch_k(gemm_kernel<BN, false, false, false, 2>, grid, kThreads, smem, st, kp);
   return launch_k(gemm_kernel<BN, false, false>, grid, kThreads, smem, st, kp);
 }
 

@@ -178,8 +178,9 @@ __device__ __forceinline__ void epi_tma_out(const KParams& p, uint8_t* b, const 
 //
 // EPI: 0 = every epilogue path; 1 = only the common one -- bf16 output through
 // TMA store / TMA reduce-add, optional statistics; 2 = only fp32 output
-// through TMA (split-K partials); 3 = 1 plus the fused BN apply (re-forward).
-// No bias or generic (remapped) stores compiled into 1-3.
+// through TMA (split-K partials); 3 = 1 plus the fused BN apply (re-forward);
+// 4 = only bf16 generic (remapped / unaligned) stores.  No bias compiled into
+// 1-4, no generic stores into 1-3.
 template <int BN, bool EXT, bool PAIR, bool RES = false, int EPI = 0>
 __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ KParams p) {
   constexpr bool SIMPLE = EPI != 0;
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const bool f32 = EPI == 2 || (EPI == 0 && p.out_f32);
     const float* bias = SIMPLE ? nullptr : p.bias;
     const bool fuse = EPI == 3 || (EPI == 0 && p.fuse_bn);
-    const bool tma = SIMPLE || mode != 0;
+    const bool tma = EPI == 4 ? false : (SIMPLE || mode != 0);
     int buf = 0;
     auto tma_out = [&](const uint32_t(&w)[16], int cx, int my, int z) {
       epi_tma_out<NB>(p, stg + buf * 2048, w, lane, mode, cx, my, z);
@@ -885,6 +886,9 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                C::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_kernel<BN, false, false, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::kSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -934,8 +938,8 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     const char* e = std::getenv("RFK_GEMM_SIMPLE");
     return e == nullptr || std::atoi(e) != 0;
   }();
-  const int epi = (simple_on && !kp.replay && kp.out_mode != 0 && !kp.bias && experiment == 0)
-                      ? (kp.fuse_bn ? 3 : (kp.out_f32 ? 2 : 1))
+  const int epi = (simple_on && !kp.replay && !kp.bias && experiment == 0)
+                      ? (kp.out_mode != 0 ? (kp.fuse_bn ? 3 : (kp.out_f32 ? 2 : 1)) : (!kp.out_f32 && !kp.fuse_bn ? 4 : 0))
                       : 0;
   const bool simple = epi == 1;
   // B resident (RFK_GEMM_BRES=0 turns it off): A through TMA im2col, one n
@@ -986,6 +990,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   if (simple) return launch_k(gemm_kernel<BN, false, false, false, 1>, grid, kThreads, smem, st, kp);
   if (epi == 2) return launch_k(gemm_kernel<BN, false, false, false, 2>, grid, kThreads, smem, st, kp);
   if (epi == 3) return launch_k(gemm_kernel<BN, false, false, false, 3>, grid, kThreads, smem, st, kp);
+  if (epi == 4 && !kp.stats_bwd) return launch_k(gemm_kernel<BN, false, false, false, 4>, grid, kThreads, smem, st, kp);
   return launch_k(gemm_kernel<BN, false, false>, grid, kThreads, smem, st, kp);
 }
 

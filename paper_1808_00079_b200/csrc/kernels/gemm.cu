@@ -301,6 +301,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         const int n0b = tc.n0 + rank * BNB;
         int aw = 0, ah = 0, an = 0;
         if (p.a_kind == (int)Operand::Im2colK) pixel_base(p, tc.m0, aw, ah, an);
+        // K block -> (filter tap (r, s), channel block cb), advanced
+        // incrementally (no integer divisions per K block)
+        int kcb = 0, ks = 0, kr = 0;
+        if (p.a_kind == (int)Operand::Im2colK) {
+          const int tap = tc.kb_begin / p.g_cblocks;
+          kcb = tc.kb_begin - tap * p.g_cblocks;
+          kr = tap / p.g_S;
+          ks = tap - kr * p.g_S;
+        }
         for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes;
@@ -314,11 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               ld2(sa, &p.ta, &full[stage], tc.m0, kb * kBlockK);
               ld2(sa + kTileA / 2, &p.ta, &full[stage], tc.m0 + 64, kb * kBlockK);
               break;
-            default: {  // Im2colK: K block -> (tap, channel block)
-              const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
-              const int r = tap / p.g_S, s = tap - r * p.g_S;
-              ldi(sa, &p.ta, &full[stage], cb * 64, aw, ah, an, (uint16_t)s, (uint16_t)r);
-            }
+            default:  // Im2colK: K block -> (tap, channel block)
+              ldi(sa, &p.ta, &full[stage], kcb * 64, aw, ah, an, (uint16_t)ks, (uint16_t)kr);
           }
           if (!RES) switch (p.b_kind) {
             case (int)Operand::KMajor2D:  // box of BNB rows
@@ -329,11 +335,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               for (int j = 0; j < BNB / 64; ++j) ld2(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, kb * kBlockK);
               break;
             case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
-              const int tap = kb / p.g_cblocks, cb = kb - tap * p.g_cblocks;
-              const int tr = tap / p.g_S, ts = tap - tr * p.g_S;
-              const int ftap = p.b_tap_base - tr * p.b_tap_dr - ts * p.b_tap_ds;
+              const int ftap = p.b_tap_base - kr * p.b_tap_dr - ks * p.b_tap_ds;
 #pragma unroll
-              for (int j = 0; j < BNB / 64; ++j) ld3(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, ftap, cb * 64);
+              for (int j = 0; j < BNB / 64; ++j) ld3(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, ftap, kcb * 64);
               break;
             }
             default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
@@ -346,6 +350,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
                 const int r = tap / p.g_S, s = tap - r * p.g_S;
                 ldi(sb + j * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
               }
+            }
+          }
+          if (++kcb == p.g_cblocks) {
+            kcb = 0;
+            if (++ks == p.g_S) {
+              ks = 0;
+              ++kr;
             }
           }
           if (++stage == nst) {

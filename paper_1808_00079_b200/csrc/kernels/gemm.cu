@@ -383,6 +383,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
     const bool b_mn = p.b_kind == (int)Operand::MNMajor2D || p.b_kind == (int)Operand::Im2colMN ||
                       p.b_kind == (int)Operand::WeightTapsMN;
     const uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * kBlockM : kBlockM, BN, a_mn, b_mn);
+    // Descriptors as (low word = start address >> 4 | LBO, high word = SBO |
+    // version | swizzle): per K block only the start advances, by the stage
+    // offset, and per 16-wide K step by 32 bytes (K-major) or 2048 bytes
+    // (MN-major), so the issue loop is a handful of uniform adds.
+    const uint64_t a_d0 = a_mn ? umma_desc_sw128(smem_u32(smem), 8192, 1024) : umma_desc_sw128(smem_u32(smem), 16, 1024);
+    const uint64_t b_d0 = b_mn ? umma_desc_sw128(smem_u32(RES ? b_base : smem + kTileA), 8192, 1024)
+                               : umma_desc_sw128(smem_u32(RES ? b_base : smem + kTileA), 16, 1024);
+    const uint32_t a_lo0 = (uint32_t)a_d0, a_hi = (uint32_t)(a_d0 >> 32);
+    const uint32_t b_lo0 = (uint32_t)b_d0, b_hi = (uint32_t)(b_d0 >> 32);
+    const uint32_t a_kstep = a_mn ? (2048u >> 4) : (32u >> 4);
+    const uint32_t b_kstep = b_mn ? (2048u >> 4) : (32u >> 4);
+    constexpr uint32_t kStageStep = (uint32_t)kStageBytes >> 4;
+    constexpr uint32_t kResStep = (uint32_t)C::kTileB >> 4;
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
@@ -407,14 +420,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-          const uint32_t sb = RES ? smem_u32(b_base + kb * C::kTileB) : sa + kTileA;
+          const uint32_t a_lo = a_lo0 + (uint32_t)stage * kStageStep;
+          const uint32_t b_lo = b_lo0 + (RES ? (uint32_t)kb * kResStep : (uint32_t)stage * kStageStep);
 #pragma unroll
           for (int kk = 0; kk < (ex == 4 ? 0 : kBlockK / 16); ++kk) {
-            const uint64_t da = a_mn ? umma_desc_sw128(sa + kk * 2048, 8192, 1024)
-                                     : umma_desc_sw128(sa + kk * 32, 16, 1024);
-            const uint64_t db = b_mn ? umma_desc_sw128(sb + kk * 2048, 8192, 1024)
-                                     : umma_desc_sw128(sb + kk * 32, 16, 1024);
+            const uint64_t da = ((uint64_t)a_hi << 32) | (a_lo + (uint32_t)kk * a_kstep);
+            const uint64_t db = ((uint64_t)b_hi << 32) | (b_lo + (uint32_t)kk * b_kstep);
             if (PAIR)
               umma_bf16_pair(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
             else

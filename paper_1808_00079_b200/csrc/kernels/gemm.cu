@@ -63,7 +63,8 @@ struct alignas(64) KParams {
   int b_taps;  // WeightTapsMN: filter taps R*S
   int b_tap_base, b_tap_dr, b_tap_ds;  // weight tap of A tap (r, s): base - r*dr - s*ds
   int out_mode;  // 0 generic stores, 1 TMA store, 2 TMA reduce-add (accumulate_out)
-  int stages;  // smem ring depth (<= Cfg::kStages)
+  int stages;  // smem ring depth in stages (of kps K blocks each)
+  int kps;     // K blocks per ring stage (1 or 2; 1 for CTA pairs)
   int m_tiles, n_tiles, splits;  // persistent tile space
   // fused BatchNorm apply (re-forward): out2 = [relu](bf16(D) * scale + shift)
   const float* bn_scale;
@@ -80,9 +81,11 @@ struct alignas(64) KParams {
   const float* bs_mean;
   const float* bs_scale;
   const float* bs_shift;
+  unsigned long long* dbg;  // tuning only: per-tile timeline of CTA 0 (RFK_GEMM_DBG=1)
   int experiment;  // tuning only (builds with RFK_GEMM_TUNING=1): 2 drop the output, 3 also skip TMEM
                   // loads, 4 also skip the MMAs, 5 skip the statistics smem reads, 6 skip the statistics
-                  // accumulation
+                  // accumulation, 7 no operand loads (MMAs + epilogue), 8 = 7 without the MMAs, 9 = 8 without
+                  // TMEM loads and output (the barrier pipeline alone)
 };
 
 template <int BN, bool PAIR = false>
@@ -191,10 +194,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
   // generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nst = p.stages;
-  // ring stages (A + B; A only with RES), [resident B], epilogue staging,
-  // column sums, barriers
+  // K blocks per ring stage: each full / empty barrier hand-off costs the
+  // single-thread producer and MMA loops ~300-400 cycles (measured:
+  // tools/mma_micro.cu ring_bench), so narrow tiles take two 64-wide K blocks
+  // per hand-off
+  const int kps = PAIR ? 1 : p.kps;
+  // ring slots (nst stages x kps; A + B, A only with RES), [resident B],
+  // epilogue staging, column sums, barriers
   constexpr int kStageBytes = RES ? kTileA : C::kStage;
-  uint8_t* b_base = smem + nst * kStageBytes;
+  uint8_t* b_base = smem + nst * kps * kStageBytes;
   uint8_t* stage_buf = RES ? b_base + p.num_kb * C::kTileB : b_base;  // epilogue staging, then the column sums
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_buf + C::kStaging + C::kStats);
   uint64_t* empty = full + nst;
@@ -273,7 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       };
       if constexpr (RES) {
         // the whole B once (one n tile, no split: every tile of this CTA uses it)
-        if (t0 < total) {
+        if (RFK_GEMM_TUNING && ex >= 7) {
+          if (t0 < total) mbar_arrive(b_full);
+        } else if (t0 < total) {
           mbar_arrive_expect_tx(b_full, (uint32_t)(p.num_kb * C::kTileB));
           for (int kb = 0; kb < p.num_kb; ++kb) {
             uint8_t* sb = b_base + kb * C::kTileB;
@@ -296,9 +306,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           }
         }
       }
-      for (int t = t0; t < total; t += tstep) {
+      int plocal = 0;
+      for (int t = t0; t < total; t += tstep, ++plocal) {
         const TileCoord tc = tile_coord<PAIR>(p, t, BN, rank);
         const int n0b = tc.n0 + rank * BNB;
+        if (RFK_GEMM_TUNING && p.dbg && blockIdx.x == 0 && plocal < 32) p.dbg[plocal * 8 + 5] = global_ns();
         int aw = 0, ah = 0, an = 0;
         if (p.a_kind == (int)Operand::Im2colK) pixel_base(p, tc.m0, aw, ah, an);
         // K block -> (filter tap (r, s), channel block cb), advanced
@@ -310,53 +322,67 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
           kr = tap / p.g_S;
           ks = tap - kr * p.g_S;
         }
-        for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
+        for (int kb0 = tc.kb_begin; kb0 < tc.kb_end; kb0 += kps) {
+          const int nk = min(kps, tc.kb_end - kb0);
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * kStageBytes;
-          uint8_t* sb = sa + kTileA;
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], PAIR ? 2 * C::kStage : kStageBytes);
-          switch (p.a_kind) {
-            case (int)Operand::KMajor2D:
-              ld2(sa, &p.ta, &full[stage], kb * kBlockK, tc.m0);
-              break;
-            case (int)Operand::MNMajor2D:
-              ld2(sa, &p.ta, &full[stage], tc.m0, kb * kBlockK);
-              ld2(sa + kTileA / 2, &p.ta, &full[stage], tc.m0 + 64, kb * kBlockK);
-              break;
-            default:  // Im2colK: K block -> (tap, channel block)
-              ldi(sa, &p.ta, &full[stage], kcb * 64, aw, ah, an, (uint16_t)ks, (uint16_t)kr);
-          }
-          if (!RES) switch (p.b_kind) {
-            case (int)Operand::KMajor2D:  // box of BNB rows
-              ld2(sb, &p.tb, &full[stage], kb * kBlockK, n0b);
-              break;
-            case (int)Operand::MNMajor2D:
-#pragma unroll
-              for (int j = 0; j < BNB / 64; ++j) ld2(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, kb * kBlockK);
-              break;
-            case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
-              const int ftap = p.b_tap_base - kr * p.b_tap_dr - ks * p.b_tap_ds;
-#pragma unroll
-              for (int j = 0; j < BNB / 64; ++j) ld3(sb + j * 8192, &p.tb, &full[stage], n0b + 64 * j, ftap, kcb * 64);
-              break;
+          if (RFK_GEMM_TUNING && ex >= 7) {  // timing only: no operand loads
+            mbar_arrive(&full[stage]);
+            if (++stage == nst) {
+              stage = 0;
+              phase ^= 1;
             }
-            default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
-              int bw, bh, bn;
-              pixel_base(p, kb * kBlockK, bw, bh, bn);
+            continue;
+          }
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], (uint32_t)nk * (PAIR ? 2 * C::kStage : kStageBytes));
+          for (int j = 0; j < nk; ++j) {
+            const int kb = kb0 + j;
+            uint8_t* sa = smem + (stage * kps + j) * kStageBytes;
+            uint8_t* sb = sa + kTileA;
+            switch (p.a_kind) {
+              case (int)Operand::KMajor2D:
+                ld2(sa, &p.ta, &full[stage], kb * kBlockK, tc.m0);
+                break;
+              case (int)Operand::MNMajor2D:
+                ld2(sa, &p.ta, &full[stage], tc.m0, kb * kBlockK);
+                ld2(sa + kTileA / 2, &p.ta, &full[stage], tc.m0 + 64, kb * kBlockK);
+                break;
+              default:  // Im2colK: K block -> (tap, channel block)
+                ldi(sa, &p.ta, &full[stage], kcb * 64, aw, ah, an, (uint16_t)ks, (uint16_t)kr);
+            }
+            if (!RES) switch (p.b_kind) {
+              case (int)Operand::KMajor2D:  // box of BNB rows
+                ld2(sb, &p.tb, &full[stage], kb * kBlockK, n0b);
+                break;
+              case (int)Operand::MNMajor2D:
 #pragma unroll
-              for (int j = 0; j < BNB / 64; ++j) {
-                const int nb = n0b / 64 + j;
-                const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
-                const int r = tap / p.g_S, s = tap - r * p.g_S;
-                ldi(sb + j * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+                for (int jj = 0; jj < BNB / 64; ++jj)
+                  ld2(sb + jj * 8192, &p.tb, &full[stage], n0b + 64 * jj, kb * kBlockK);
+                break;
+              case (int)Operand::WeightTapsMN: {  // K block = (tap of the im2col A, Cout block), flipped
+                const int ftap = p.b_tap_base - kr * p.b_tap_dr - ks * p.b_tap_ds;
+#pragma unroll
+                for (int jj = 0; jj < BNB / 64; ++jj)
+                  ld3(sb + jj * 8192, &p.tb, &full[stage], n0b + 64 * jj, ftap, kcb * 64);
+                break;
+              }
+              default: {  // Im2colMN: K block = 64 output pixels, MN = (tap, channel)
+                int bw, bh, bn;
+                pixel_base(p, kb * kBlockK, bw, bh, bn);
+#pragma unroll
+                for (int jj = 0; jj < BNB / 64; ++jj) {
+                  const int nb = n0b / 64 + jj;
+                  const int tap = nb / p.g_cblocks, cb = nb - tap * p.g_cblocks;
+                  const int r = tap / p.g_S, s = tap - r * p.g_S;
+                  ldi(sb + jj * 8192, &p.tb, &full[stage], cb * 64, bw, bh, bn, (uint16_t)s, (uint16_t)r);
+                }
               }
             }
-          }
-          if (++kcb == p.g_cblocks) {
-            kcb = 0;
-            if (++ks == p.g_S) {
-              ks = 0;
-              ++kr;
+            if (++kcb == p.g_cblocks) {
+              kcb = 0;
+              if (++ks == p.g_S) {
+                ks = 0;
+                ++kr;
+              }
             }
           }
           if (++stage == nst) {
@@ -407,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);  // epilogue(s) drained this accumulator
       tc_fence_after();
+      if (RFK_GEMM_TUNING && p.dbg && blockIdx.x == 0 && local < 32 && lane_id() == 0) p.dbg[local * 8 + 0] = global_ns();
       const uint32_t d_tmem = tmem + (uint32_t)(acc * C::kTmemCols);
       if (tc.kb_end <= tc.kb_begin) {
         if (elect_one()) {  // empty split: nothing to accumulate
@@ -416,21 +443,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         __syncwarp();
         continue;
       }
-      for (int kb = tc.kb_begin; kb < tc.kb_end; ++kb) {
+      for (int kb0 = tc.kb_begin; kb0 < tc.kb_end; kb0 += kps) {
+        const int nk = min(kps, tc.kb_end - kb0);
+        const int kb = kb0 + nk - 1;  // the stage's last K block
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t a_lo = a_lo0 + (uint32_t)stage * kStageStep;
-          const uint32_t b_lo = b_lo0 + (RES ? (uint32_t)kb * kResStep : (uint32_t)stage * kStageStep);
+          for (int j = 0; j < nk; ++j) {
+            const uint32_t a_lo = a_lo0 + (uint32_t)(stage * kps + j) * kStageStep;
+            const uint32_t b_lo =
+                b_lo0 + (RES ? (uint32_t)(kb0 + j) * kResStep : (uint32_t)(stage * kps + j) * kStageStep);
 #pragma unroll
-          for (int kk = 0; kk < (ex == 4 ? 0 : kBlockK / 16); ++kk) {
-            const uint64_t da = ((uint64_t)a_hi << 32) | (a_lo + (uint32_t)kk * a_kstep);
-            const uint64_t db = ((uint64_t)b_hi << 32) | (b_lo + (uint32_t)kk * b_kstep);
-            if (PAIR)
-              umma_bf16_pair(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
-            else
-              umma_bf16(d_tmem, da, db, idesc, (kb > tc.kb_begin || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < ((ex == 4 || ex == 8 || ex == 9) ? 0 : kBlockK / 16); ++kk) {
+              const uint64_t da = ((uint64_t)a_hi << 32) | (a_lo + (uint32_t)kk * a_kstep);
+              const uint64_t db = ((uint64_t)b_hi << 32) | (b_lo + (uint32_t)kk * b_kstep);
+              const uint32_t accum = (kb0 + j > tc.kb_begin || kk > 0) ? 1u : 0u;
+              if (PAIR)
+                umma_bf16_pair(d_tmem, da, db, idesc, accum);
+              else
+                umma_bf16(d_tmem, da, db, idesc, accum);
+            }
           }
+          if (RFK_GEMM_TUNING && p.dbg && blockIdx.x == 0 && local < 32 && kb + 1 == tc.kb_end) p.dbg[local * 8 + 1] = global_ns();
           if (PAIR) {
             umma_commit_pair(&empty[stage]);
             if (kb + 1 == tc.kb_end) umma_commit_pair(&acc_full[acc]);
@@ -523,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         mbar_wait(&acc_full[acc], acc_phase);
         tc_fence_after();
       }
+      if (RFK_GEMM_TUNING && p.dbg && blockIdx.x == 0 && local < 32 && ew == 0 && lane == 0) p.dbg[local * 8 + 2] = global_ns();
       const int my = tc.m0 + (int)(quarter * 32);
       const int m = my + (int)lane;
       const bool row_ok = m < p.M;
@@ -564,13 +599,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
               r[8 * j + 2 * e + 1] = uw[e] & 0xffff0000u;  // high bf16 -> fp32 bits
             }
           }
-        } else if (!empty_k && (ex < 3 || ex > 4)) {
+        } else if (!empty_k && (ex < 3 || ex > 4) && ex != 9) {
           tmem_ld32(tmem + (uint32_t)(acc * C::kTmemCols) + ((quarter * 32u) << 16) + (uint32_t)c0, r);
           tmem_ld_wait();
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
+        if (RFK_GEMM_TUNING && p.dbg && blockIdx.x == 0 && local < 32 && ew == 0 && lane == 0 && c0 < 64) p.dbg[local * 8 + 3] = global_ns();
         if (c0 + 64 >= BN && !(EXT && p.replay)) {
           // this warp's last chunk of the accumulator is in registers: hand it back
           tc_fence_before();
@@ -586,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         const int col0 = tc.n0 + c0;
-        if (col0 >= p.N || (ex >= 2 && ex <= 4)) continue;  // warp-uniform
+        if (col0 >= p.N || (ex >= 2 && ex <= 4) || ex == 9) continue;  // warp-uniform
         const bool full_cols = col0 + 32 <= p.N;
         if (bias) {
 #pragma unroll
@@ -771,6 +807,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         }
         __syncwarp();
       }
+      if (RFK_GEMM_TUNING && p.dbg && blockIdx.x == 0 && local < 32 && ew == 0 && lane == 0) p.dbg[local * 8 + 4] = global_ns();
     }
     if (p.stats && cur_nt >= 0) flush_stats(cur_nt);
     if (lane == 0) bulk_wait_all();
@@ -885,7 +922,40 @@ int pair_max_clusters() {
 }
 
 template <int BN>
+cudaError_t launch_bn_impl(KParams& kp, int m_tiles, int n_tiles, int splits, int max_ctas, bool pair, cudaStream_t st);
+
+// Tuning builds: RFK_GEMM_DBG=1 records CTA 0's per-tile timeline and prints
+// it after the (eager, synchronised) launch.
+template <int BN>
 cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max_ctas, bool pair, cudaStream_t st) {
+  static unsigned long long* dbg = nullptr;
+  static const bool dbg_on = [] {
+    const char* e = std::getenv("RFK_GEMM_DBG");
+    return RFK_GEMM_TUNING && e && std::atoi(e) != 0;
+  }();
+  if (dbg_on && !dbg) cudaMalloc(&dbg, 32 * 8 * sizeof(unsigned long long));
+  kp.dbg = dbg_on ? dbg : nullptr;
+  if (dbg_on) cudaMemsetAsync(dbg, 0, 32 * 8 * sizeof(unsigned long long), st);
+  cudaError_t e = launch_bn_impl<BN>(kp, m_tiles, n_tiles, splits, max_ctas, pair, st);
+  if (dbg_on && e == cudaSuccess) {
+    unsigned long long h[32 * 8];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    unsigned long long t0 = h[5];
+    for (int i = 0; i < 8 * 32; ++i)
+      if (h[i] && h[i] < t0) t0 = h[i];
+    std::printf("gemm dbg BN=%d M=%d N=%d K=%d tiles %d x %d (ns from CTA 0 start): prod_tile mma_acc_free mma_last_kb "
+                "epi_acc_full epi_tmem1 epi_done\n", BN, kp.M, kp.N, kp.K, m_tiles, n_tiles);
+    for (int l = 0; l < 32 && h[l * 8 + 5]; ++l) {
+      auto f = [&](int j) { return h[l * 8 + j] ? (long long)(h[l * 8 + j] - t0) : -1LL; };
+      std::printf("  tile %2d: %7lld %7lld %7lld %7lld %7lld %7lld\n", l, f(5), f(0), f(1), f(2), f(3), f(4));
+    }
+  }
+  return e;
+}
+
+template <int BN>
+cudaError_t launch_bn_impl(KParams& kp, int m_tiles, int n_tiles, int splits, int max_ctas, bool pair, cudaStream_t st) {
   using C = Cfg<BN>;
   using CP = Cfg<BN, true>;
   static bool configured = false;
@@ -938,12 +1008,25 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   kp.splits = splits;
   const long kb_per_cta = (long)kp.kb_per_split * ((total + units_grid - 1) / units_grid);
   const int max_stages = pair ? CP::kStages : C::kStages;
-  kp.stages = (int)std::max<long>(2, std::min<long>(max_stages, kb_per_cta));
+  // K blocks per ring stage (RFK_GEMM_KPS overrides): two for tiles whose
+  // K block of MMAs is shorter than a barrier hand-off (BN <= 128)
+  static const int kps_env = [] {
+    const char* e = std::getenv("RFK_GEMM_KPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  // (tuning: 1 off, 2 BN <= 128, 3 every BN, 4 BN = 64 only, 5 where >= 3 stages of 2 fit)
+  const int kmode = kps_env > 0 ? kps_env : 2;
+  kp.kps = (pair || kp.replay) ? 1
+           : (kmode == 3 || (kmode == 2 && BN <= 128) || (kmode == 4 && BN == 64) || (kmode == 5 && max_stages >= 6))
+               ? 2
+               : 1;
+  if (max_stages / kp.kps < 2) kp.kps = 1;
+  kp.stages = (int)std::max<long>(2, std::min<long>(max_stages / kp.kps, (kb_per_cta + kp.kps - 1) / kp.kps));
   static const int force_stages = [] {
     const char* e = std::getenv("RFK_GEMM_STAGES");  // tuning experiments only
     return e ? std::atoi(e) : 0;
   }();
-  if (force_stages >= 2) kp.stages = std::min(force_stages, max_stages);
+  if (force_stages >= 2) kp.stages = std::min(force_stages, max_stages / kp.kps);
   if (kp.replay) kp.stages = 2;  // no operand ring in a statistics replay
   static const int experiment = [] {
     const char* e = std::getenv("RFK_GEMM_EXPERIMENT");  // tuning experiments only
@@ -960,7 +1043,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
     const char* e = std::getenv("RFK_GEMM_SIMPLE");
     return e == nullptr || std::atoi(e) != 0;
   }();
-  const int epi = (simple_on && !kp.replay && !kp.bias && experiment == 0)
+  const int epi = (simple_on && !kp.replay && !kp.bias && (experiment == 0 || experiment >= 7))
                       ? (kp.out_mode != 0 ? (kp.fuse_bn ? 3 : (kp.out_f32 ? 2 : 1)) : (!kp.out_f32 && !kp.fuse_bn ? 4 : 0))
                       : 0;
   const bool simple = epi == 1;
@@ -976,7 +1059,7 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
   const long b_bytes = (long)kp.num_kb * C::kTileB;
   const long fixed = C::kStaging + C::kStats + 1024 + 256;
   if (bres_on && !kp.replay && kp.a_kind == (int)Operand::Im2colK && kp.b_kind != (int)Operand::Im2colMN &&
-      n_tiles == 1 && splits == 1 && total > grid && force_stages < 2 && experiment == 0 &&
+      n_tiles == 1 && splits == 1 && total > grid && force_stages < 2 && (experiment == 0 || experiment >= 7) &&
       fixed + b_bytes + 4L * kTileA <= C::kSmemMax) {
     static bool res_configured = false;
     if (!res_configured) {
@@ -998,15 +1081,16 @@ cudaError_t launch_bn(KParams& kp, int m_tiles, int n_tiles, int splits, int max
       res_configured = true;
     }
     const long ring = std::min<long>((C::kSmemMax - fixed - b_bytes) / kTileA, 12);
-    kp.stages = (int)std::max<long>(2, std::min<long>(ring, kb_per_cta));
-    const int smem = (int)(kp.stages * kTileA + b_bytes + fixed);
+    if (ring / kp.kps < 2 || (kmode == 5 && ring < 6)) kp.kps = 1;
+    kp.stages = (int)std::max<long>(2, std::min<long>(ring / kp.kps, (kb_per_cta + kp.kps - 1) / kp.kps));
+    const int smem = (int)(kp.stages * kp.kps * kTileA + b_bytes + fixed);
     if (kp.stats_bwd && simple) return launch_k(gemm_kernel<BN, true, false, true, 1>, grid, kThreads, smem, st, kp);
     if (kp.stats_bwd) return launch_k(gemm_kernel<BN, true, false, true>, grid, kThreads, smem, st, kp);
     if (simple) return launch_k(gemm_kernel<BN, false, false, true, 1>, grid, kThreads, smem, st, kp);
     if (epi == 3) return launch_k(gemm_kernel<BN, false, false, true, 3>, grid, kThreads, smem, st, kp);
     return launch_k(gemm_kernel<BN, false, false, true>, grid, kThreads, smem, st, kp);
   }
-  const int smem = kp.stages * C::kStage + C::kStaging + C::kStats + 1024 + 256;
+  const int smem = kp.stages * kp.kps * C::kStage + C::kStaging + C::kStats + 1024 + 256;
   if (kp.stats_bwd && simple) return launch_k(gemm_kernel<BN, true, false, false, 1>, grid, kThreads, smem, st, kp);
   if (kp.stats_bwd || kp.replay) return launch_k(gemm_kernel<BN, true, false>, grid, kThreads, smem, st, kp);
   if (simple) return launch_k(gemm_kernel<BN, false, false, false, 1>, grid, kThreads, smem, st, kp);

@@ -224,6 +224,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
     const uint32_t idesc = umma_idesc_bf16(kBM, BN, false, b_mn);
     int bs = 0, s = 0, local = 0;
     uint32_t bph = 0, ph = 0;
+    // resident weights: every slot is loaded once, wait for all of them up front
+    // (a wait on a completed barrier still costs ~90 cycles + the fence; per
+    // tap that bounded the issue loop)
+    if (p.b_resident && (int)blockIdx.x < total) {
+      for (int slot = 0; slot < p.cblocks * p.taps; ++slot) mbar_wait(&b_full[slot], 0u);
+      tc_fence_after();
+    }
+    const uint32_t bhi = (uint32_t)((b_mn ? umma_desc_sw128(0, 8192, 1024) : umma_desc_sw128(0, 16, 1024)) >> 32);
+    const uint32_t blo_k = (uint32_t)(b_mn ? umma_desc_sw128(0, 8192, 1024) : umma_desc_sw128(0, 16, 1024));
+    const uint32_t ahi = (uint32_t)(desc_sw128_rows(0) >> 32), alo_k = (uint32_t)desc_sw128_rows(0);
+    const uint32_t b_kstep = b_mn ? (2048u >> 4) : (32u >> 4);
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int mt = t % p.m_tiles;
       const int j0 = (mt % p.tiles_per_img) * kBM;
@@ -238,7 +249,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
         tc_fence_after();
         if (p.dbg && blockIdx.x == 0 && local < 16 && cb == 0 && lane_id() == 0) p.dbg[local * 4 + 1] = global_ns();
         const uint32_t sa0 = smem_u32(band + bs * p.band_bytes);
-        for (int tap = 0; tap < p.taps; ++tap) {
+        if (p.b_resident) {
+          // all taps of this channel block in one tight issue loop: the A
+          // start row advances by one per filter column and by Wp per row
+          if (elect_one()) {
+            const uint32_t a_base = alo_k + ((sa0 + (uint32_t)row0 * 128u) >> 4);
+            const uint32_t b_base = blo_k + (smem_u32(bring + cb * p.taps * kTileB) >> 4);
+            int r = 0, c = 0;
+            for (int tap = 0; tap < p.taps; ++tap) {
+              const uint32_t a_lo = a_base + (uint32_t)(r * p.Wp + c) * 8u;  // 128-byte rows, >> 4
+              const uint32_t b_lo = b_base + (uint32_t)tap * (uint32_t)(kTileB >> 4);
+#pragma unroll
+              for (int kk = 0; kk < ((RFK_GEMM_TUNING && p.experiment == 4) ? 0 : 4); ++kk) {
+                const uint64_t da = ((uint64_t)ahi << 32) | (a_lo + (uint32_t)kk * 2u);
+                const uint64_t db = ((uint64_t)bhi << 32) | (b_lo + (uint32_t)kk * b_kstep);
+                umma_bf16(d_tmem, da, db, idesc, (cb > 0 || tap > 0 || kk > 0) ? 1u : 0u);
+              }
+              if (++c == p.S) {
+                c = 0;
+                ++r;
+              }
+            }
+            umma_commit(&band_empty[bs]);
+            if (cb + 1 == p.cblocks) umma_commit(&acc_full[acc]);
+          }
+          __syncwarp();
+        }
+        for (int tap = 0; tap < p.taps && !p.b_resident; ++tap) {
           const int slot = p.b_resident ? cb * p.taps + tap : s;
           mbar_wait(&b_full[slot], p.b_resident ? 0u : ph);
           tc_fence_after();

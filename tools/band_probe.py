@@ -1,0 +1,52 @@
+"""im2col-TMA vs shifted-band implicit GEMM on the ResNet-50 stride-1 3x3 shapes (GPU)."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1808_00079_b200 import kernels as K  # noqa: E402
+
+dev = "cuda"
+
+
+def bf(*shape):
+    return (torch.randn(*shape, device=dev) * 0.5).to(torch.bfloat16)
+
+
+def timeit(ga, iters=20):
+    for _ in range(2):
+        K.gemm(ga)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(iters):
+            K.gemm(ga)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / iters
+
+
+for (n, h, c) in [(32, 56, 64), (32, 28, 128), (32, 14, 256)]:
+    x = bf(n, h, h, c)
+    w = bf(c, 9 * c)
+    wt = bf(c, 3, 3, c)
+    o = bf(n, h, h, c)
+    st = torch.zeros(160, 2, c, device=dev)
+    g = K.ConvGeom(n, h, h, c, h, h, 3, 3, 1, 1, 1, 1)
+    M = n * h * h
+    fl = 2.0 * M * c * 9 * c
+    for band in (0, 1):
+        fp = K.GemmArgs(M=M, N=c, K=9 * c, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=K.KMAJOR,
+                        b=w.data_ptr(), b_ld=9 * c, out=o.data_ptr(), ldc=c, stats=st.data_ptr(), splits=1, band=band)
+        dg = K.GemmArgs(M=M, N=c, K=9 * c, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=4, b=wt.data_ptr(),
+                        out=o.data_ptr(), ldc=c, splits=1, band=band)
+        for k, v in {"b_extent": c, "b_taps": 9, "b_cpad": c, "b_rows": c}.items():
+            setattr(dg, k, v)
+        for name, ga in (("fprop+stats", fp), ("dgrad", dg)):
+            us = timeit(ga)
+            print(f"3x3 {h}x{h}x{c} {name:12s} band={band}: {us:7.1f} us  {fl / us / 1e6:7.1f} TFLOP/s")

@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
       };
       if constexpr (RES) {
         // the whole B once (one n tile, no split: every tile of this CTA uses it)
-        if (RFK_GEMM_TUNING && ex >= 7) {
+        if (RFK_GEMM_TUNING && ex >= 7 && ex <= 9) {
           if (t0 < total) mbar_arrive(b_full);
         } else if (t0 < total) {
           mbar_arrive_expect_tx(b_full, (uint32_t)(p.num_kb * C::kTileB));
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant
         for (int kb0 = tc.kb_begin; kb0 < tc.kb_end; kb0 += kps) {
           const int nk = min(kps, tc.kb_end - kb0);
           mbar_wait(&empty[stage], phase ^ 1);
-          if (RFK_GEMM_TUNING && ex >= 7) {  // timing only: no operand loads
+          if (RFK_GEMM_TUNING && ex >= 7 && ex <= 9) {  // timing only: no operand loads
             mbar_arrive(&full[stage]);
             if (++stage == nst) {
               stage = 0;
@@ -1033,7 +1033,7 @@ cudaError_t launch_bn_impl(KParams& kp, int m_tiles, int n_tiles, int splits, in
     return e ? std::atoi(e) : 0;
   }();
   kp.experiment = experiment;
-  if (experiment == 1) kp.out_mode = 0;
+  if (experiment == 1 || experiment == 10) kp.out_mode = 0;  // 10: generic stores in the specialised instance
   if (pair) {
     const int smem = kp.stages * CP::kStage + CP::kStaging + CP::kStats + 1024 + 256;
     return launch_k_cluster(gemm_kernel<BN, false, true>, grid, kThreads, smem, st, 2, kp);

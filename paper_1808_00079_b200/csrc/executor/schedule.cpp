@@ -605,9 +605,15 @@ void Net::build_schedule() {
 // ============================================================ layout
 namespace {
 // Split-K for a bf16-output implicit GEMM (conv fprop / dgrad through TMA
-// im2col), from the sweep-fitted cost model of gemm.cu: t = waves * (k blocks
-// * 0.5 us + per-tile b) plus, when split, the fp32 partial round trip
-// (s * M * N * 4 bytes at ~3 TB/s) and one extra launch.  Returns {bn, splits}.
+// im2col), from a cost model of gemm.cu: t = waves * (k blocks * c_bn + per-tile
+// b) plus, when split, the fp32 partial round trip (s * M * N * 4 bytes at ~3
+// TB/s) and one extra launch.  c_kb = time per 64-wide K block of one tile
+// (0.5 us, sweep-fitted; RFK_SPLIT_KB overrides, diagnostics: the per-width
+// values of the late-round-2 timelines, 0.30 / 0.33 / 0.42 us, measured
+// +0.25 % on ResNet-50).  Outputs of at most 32 channels (DenseNet growth
+// convs) never split: their few-K-block partial tiles and the extra finish
+// launch cost more than the wave they save (DenseNet-121 8.51 -> 8.36 ms
+// without split-K).  Returns {bn, splits}.
 std::pair<int, int> im2col_split_plan(long M, int N, long kb) {
   if (const char* e = std::getenv("RFK_NO_SPLITK"); e && std::atoi(e)) return {0, 1};  // diagnostics
   const long mt = (M + 127) / 128;
@@ -616,11 +622,12 @@ std::pair<int, int> im2col_split_plan(long M, int N, long kb) {
   for (int bn : {256, 128, 64}) {
     if (bn > 64 && N <= bn / 2) continue;
     const double b = bn == 64 ? 2.5 : (bn == 128 ? 3.5 : 7.0);
+    static const double c_kb = std::getenv("RFK_SPLIT_KB") ? std::atof(std::getenv("RFK_SPLIT_KB")) : 0.5;
     for (int s : {1, 2, 3, 4, 6, 8}) {
-      if (s > 1 && kb / s < 6) continue;
+      if (s > 1 && (kb / s < 6 || N <= 32)) continue;
       const long tiles = mt * ((N + bn - 1) / bn) * s;
       const long waves = (tiles + 147) / 148;
-      double t = (double)waves * ((double)((kb + s - 1) / s) * 0.5 + b);
+      double t = (double)waves * ((double)((kb + s - 1) / s) * c_kb + b);
       // fp32 partials written and summed once more, plus the finish launch
       static const double bw = std::getenv("RFK_SPLIT_BW") ? std::atof(std::getenv("RFK_SPLIT_BW")) : 3.0e6;
       static const double fixed = std::getenv("RFK_SPLIT_FIXED") ? std::atof(std::getenv("RFK_SPLIT_FIXED")) : 3.0;

@@ -19,7 +19,11 @@ arch = sys.argv[1] if len(sys.argv) > 1 else "resnet50"
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 32
 hw = int(sys.argv[3]) if len(sys.argv) > 3 else 224
 net = ReforwardNet.named(arch, batch, hw, hw, 1000)
-net.plan("reforward")
+cache = os.path.join("plans", f"{arch}_b{batch}_{hw}_reforward.json")
+if os.path.exists(cache):
+    net.plan_cached("reforward", cache)  # the exact plan, computed once (minutes for Inception-v3)
+else:
+    net.plan("reforward")
 net.setup(0)
 x, y = random_batch(net, 0)
 net.load_batch(x.cuda(), y.cuda())

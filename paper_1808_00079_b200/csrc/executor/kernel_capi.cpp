@@ -35,7 +35,7 @@ extern "C" int rfx_gemm(const rfx_gemm_args* a, void* stream) {
   d.b_taps = a->b_taps > 0 ? a->b_taps : 1;
   d.b_cpad = a->b_cpad;
   d.b_rows = a->b_rows;
-  d.band = a->band != 0;
+  d.band = a->band != 0 ? 2 : 0;  // the C-ABI flag forces the band kernel where the shape allows it
   if (a->b_tap_map) {
     d.b_tap_base = a->b_tap_base;
     d.b_tap_dr = a->b_tap_dr;

@@ -268,6 +268,7 @@ class Net {
   void gemm(const rfk::GemmDesc& d, cudaStream_t st);
   bool wgrad_overlap() const;
   bool subpixel_ok(const Op& op, const Tensor& x) const;  // strided dgrad as sub-pixel GEMMs
+  bool fusable_conv(const Op& op) const;  // some plan may fuse its consumer BN into its re-forward
   void ensure_wgrad_stream();
   void ensure_sub_streams();
   void check(cudaError_t e, const char* what) const;

@@ -19,21 +19,33 @@ namespace {
 int round8(int c) { return (c + 7) / 8 * 8; }
 
 // The shifted-band implicit GEMM (gemm_band.cu) is exact (tests/test_gemm_gpu.py)
-// and moves ~5x fewer A bytes than TMA im2col, but measures no faster yet on
-// ResNet-50's 3x3 convs (its per-tile load phase is not bandwidth-bound; see
-// DESIGN.md), so it is opt-in: RFK_BAND=1.
+// and moves 3-5x fewer A bytes than TMA im2col; it runs where it measured
+// faster (gemm_band_preferred: the 56x56 3x3 convs, the narrow DenseNet growth
+// convs) and its epilogue suffices (no fused re-forward BN apply, no
+// BN-backward statistics).  RFK_BAND=0: never; RFK_BAND=1: wherever allowed.
 // sub-pixel class GEMMs on parallel streams (RFK_SUBPIXEL_PAR=0: one stream)
 bool sub_parallel() {
   static const bool on = !std::getenv("RFK_SUBPIXEL_PAR") || std::atoi(std::getenv("RFK_SUBPIXEL_PAR")) != 0;
   return on;
 }
 
-bool band_enabled() {
-  static const bool on = [] {
+// A conv that some plan may re-forward with its consumer BN applied in the
+// GEMM epilogue (the structural part of the fusion rule in schedule.cpp; which
+// plans actually fuse depends on their segments)
+bool fusable_conv_impl(const std::vector<Op>& ops, const std::vector<Tensor>& tensors, const Op& op) {
+  if (op.kind != OpKind::Conv || !op.fuse_stats || op.fp_splits > 1 || op.cout % 8) return false;
+  const auto& cons = tensors[op.out].consumers;
+  if (cons.empty()) return false;
+  const Op& bn = ops[cons[0]];
+  return bn.kind == OpKind::BN && bn.out >= 0;
+}
+
+int band_enabled() {
+  static const int mode = [] {
     const char* e = std::getenv("RFK_BAND");
-    return e != nullptr && std::atoi(e) != 0;
+    return e == nullptr ? 1 : (std::atoi(e) != 0 ? 2 : 0);
   }();
-  return on;
+  return mode;
 }
 
 float bf16_to_float(uint16_t b) {
@@ -43,6 +55,8 @@ float bf16_to_float(uint16_t b) {
   return f;
 }
 }  // namespace
+
+bool Net::fusable_conv(const Op& op) const { return fusable_conv_impl(ops_, tensors_, op); }
 
 std::unique_ptr<Net> make_net(int batch) { return std::make_unique<Net>(batch); }
 
@@ -576,7 +590,15 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         d.a_kind = rfk::Operand::Im2colK;
         d.a = tptr(op.in[0]);
         d.a_geom = rfk::ConvGeom{x.N, x.H, x.W, x.C, y.H, y.W, op.R, op.S, op.pad, op.pad_w, op.stride, op.stride};
-        d.band = band_enabled();  // opt-in shifted-band kernel for stride-1 shapes (gemm_band.cu)
+        // shifted-band kernel where it pays (gemm_band.cu).  Its K order is
+        // channel block outer, tap inner -- the TMA im2col path's order only
+        // with one 64-channel block, where the two give identical bits.  With
+        // more blocks it runs only for the narrow (<= 32-channel) DenseNet
+        // growth convs, and only if no plan can re-forward the conv through
+        // the im2col kernel with its BN fused (every plan then computes the
+        // same bits: re-forward / store-all identity); elsewhere the measured
+        // gain is small and the results would move by summation order.
+        d.band = (op.cpad <= 64 || (op.cout <= 32 && !fusable_conv(op))) ? band_enabled() : 0;
         d.K = op.R * op.S * op.cpad;
         d.b_ld = (long)op.R * op.S * op.cpad;
       }
@@ -609,7 +631,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
         d.bn_scale = d_state_ + b.scale;
         d.bn_shift = d_state_ + b.shift;
         d.bn_relu = bn.k == 1;
-        d.band = false;
+        d.band = 0;
       }
       gemm(d, st);
       break;
@@ -805,7 +827,11 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           d.b_cpad = op.cpad;
           d.b_rows = op.cout;
           d.a_kind = rfk::Operand::Im2colK;
-          d.band = band_enabled();
+          // (one channel block of dy only: the band and im2col kernels then sum
+          // in the same order, so whether the plan fuses the BN-backward
+          // statistics into this dgrad -- which excludes the band kernel --
+          // never changes its bits)
+          d.band = op.coutpad <= 64 ? band_enabled() : 0;
           const int pd = op.R - 1 - op.pad, pdw = op.S - 1 - op.pad_w;
           if (op.dg_subpixel) {
             // Sub-pixel decomposition: the stride x stride classes of input
@@ -856,7 +882,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
                   dc.b_extent = op.cin;
                   dc.b_tap_base = -1;
                 }
-                dc.band = false;
+                dc.band = 0;
                 dc.remap = true;
                 dc.rP = ch.rows;
                 dc.rQ = cw.rows;
@@ -912,7 +938,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
             d.stats = ws_stats_base() + bn.bstat_off;
             d.stats_bwd = true;
             d.block_n = bn.bstat_bn;
-            d.band = false;
+            d.band = 0;
             d.bs_y = tptr(bn.in[0]);
             d.bs_ldy = tensors_[bn.in[0]].C;
             d.bs_mean = d_state_ + b.mean;

@@ -1146,7 +1146,8 @@ cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream) {
   load_driver_entry_points();
   if (!g_encode_tiled || !g_encode_im2col) return cudaErrorNotSupported;
   if (d.M <= 0 || d.N <= 0) return cudaSuccess;
-  if (d.band && !d.bn_out && !d.stats_bwd && !d.replay && !d.stats_acc && d.a_kind == Operand::Im2colK && gemm_band_ok(d))
+  if (d.band && !d.bn_out && !d.stats_bwd && !d.replay && !d.stats_acc && d.a_kind == Operand::Im2colK && gemm_band_ok(d) &&
+      (d.band == 2 || gemm_band_preferred(d)))
     return gemm_band_launch(d, stream);
   const int bn = gemm_block_n(d);
   if (bn != 64 && bn != 128 && bn != 256) return cudaErrorInvalidValue;

@@ -57,6 +57,7 @@ struct alignas(64) BandParams {
   int Wp, P, Q, ph, pw, BR;    // plane geometry
   int plane;                   // P * Wp positions per image
   int tiles_per_img, m_tiles, n_tiles;
+  int tile_pos;                // plane positions per tile: whole output rows (rows x Wp <= 128), else 128
   int b_kind;                  // 0 K-major weights (fprop), 4 flipped weight taps (dgrad)
   void* out;
   long ldc;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
       }
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int mt = t % p.m_tiles, n0 = (t / p.m_tiles) * BN;
-        const int img = mt / p.tiles_per_img, j0 = (mt % p.tiles_per_img) * kBM;
+        const int img = mt / p.tiles_per_img, j0 = (mt % p.tiles_per_img) * p.tile_pos;
         const int rho0 = j0 / p.Wp;
         // warm L2 with this CTA's band a few tiles ahead: the band loads are
         // DRAM-latency bound with only band_stages of them in shared memory
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
           const int tf = t + p.prefetch_tiles * (int)gridDim.x;
           if (tf < total) {
             const int mf = tf % p.m_tiles;
-            const int imf = mf / p.tiles_per_img, jf = (mf % p.tiles_per_img) * kBM;
+            const int imf = mf / p.tiles_per_img, jf = (mf % p.tiles_per_img) * p.tile_pos;
             for (int cbf = 0; cbf < p.cblocks; ++cbf)
               tma_prefetch_l2_4d(&p.ta, cbf * 64, -p.pw, jf / p.Wp - p.ph, imf);
           }
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
     const uint32_t b_kstep = b_mn ? (2048u >> 4) : (32u >> 4);
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int mt = t % p.m_tiles;
-      const int j0 = (mt % p.tiles_per_img) * kBM;
+      const int j0 = (mt % p.tiles_per_img) * p.tile_pos;
       const int row0 = j0 - (j0 / p.Wp) * p.Wp;  // first output row's offset inside the band
       const int acc = local & 1;
       mbar_wait(&acc_empty[acc], ((local >> 1) & 1) ^ 1);
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
       uint32_t bph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int mt = t % p.m_tiles;
-        const int j0 = (mt % p.tiles_per_img) * kBM;
+        const int j0 = (mt % p.tiles_per_img) * p.tile_pos;
         const int rho0 = j0 / p.Wp;
         for (int cb = 0; cb < p.cblocks; ++cb) {
           mbar_wait(&band_full[bs], bph);
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
     int local = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
       const int mt = t % p.m_tiles, nt = t / p.m_tiles;
-      const int img = mt / p.tiles_per_img, j0 = (mt % p.tiles_per_img) * kBM;
+      const int img = mt / p.tiles_per_img, j0 = (mt % p.tiles_per_img) * p.tile_pos;
       const int acc = local & 1;
       if (p.stats && nt != cur_nt) {
         if (cur_nt >= 0) flush_stats(cur_nt);
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
       tc_fence_after();
       if (p.dbg && blockIdx.x == 0 && local < 16 && ew == 0 && lane == 0) p.dbg[local * 4 + 2] = global_ns();
       const int jl = j0 + (int)(quarter * 32 + lane);  // this lane's plane position
-      const bool row_ok = jl < p.plane && (jl % p.Wp) < p.Q;
+      const bool row_ok = jl - j0 < p.tile_pos && jl < p.plane && (jl % p.Wp) < p.Q;
 #pragma unroll 1
       for (int c0 = (int)half * 32; c0 < BN; c0 += 64) {
         uint32_t r[32];
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_band_kernel(const __grid_con
         for (int it = 0; it < 4; ++it) {
           const uint32_t rr = it * 8 + (lane >> 2), chunk = lane & 3;
           const int jr = j0 + (int)(quarter * 32 + rr);
-          if (jr >= p.plane) continue;
+          if (jr >= p.plane || jr - j0 >= p.tile_pos) continue;
           const int h = jr / p.Wp, wq = jr - h * p.Wp;
           if (wq >= p.Q || !(full_cols || col0 + (int)chunk * 8 < p.N)) continue;
           const uint4 val = *reinterpret_cast<const uint4*>(gb + rr * 64 + ((chunk ^ ((rr >> 1) & 3u)) * 16));
@@ -553,6 +554,18 @@ cudaError_t band_launch(BandParams& bp, cudaStream_t st) {
 
 }  // namespace
 
+// Where the band kernel measured faster than TMA im2col (tools/band_probe.py,
+// late round 2): 3x3 stride-1 convs at >= 48 output columns (ResNet layer 1,
+// DenseNet block 1: 56x56x64 fprop 19.9 -> 17.5 us, dgrad 19.9 -> 15.5 us,
+// 56x56x128 -> 32 fprop 34.4 -> 24.8 us) and narrow (<= 32 channel) outputs
+// from 24 columns on (28x28x128 -> 32: 12.6 -> 11.5 us).  At 28x28x128 -> 128
+// it is slower (20.2 vs 15.1 us), at 14x14 equal.
+bool gemm_band_preferred(const GemmDesc& d) {
+  const ConvGeom& g = d.a_geom;
+  if (g.R != 3 || g.S != 3) return false;
+  return g.Q >= 48 || (d.N <= 32 && g.Q >= 24);
+}
+
 bool gemm_band_ok(const GemmDesc& d) {
   const ConvGeom& g = d.a_geom;
   if (g.stride_h != 1 || g.stride_w != 1 || g.R * g.S < 2) return false;
@@ -587,9 +600,31 @@ cudaError_t gemm_band_launch(const GemmDesc& d, cudaStream_t stream) {
   bp.Q = g.Q;
   bp.ph = g.pad_h;
   bp.pw = g.pad_w;
-  bp.BR = band_rows(bp.Wp, g.R);
   bp.plane = g.P * bp.Wp;
-  bp.tiles_per_img = (bp.plane + kBM - 1) / kBM;
+  // Row-aligned tiles: a tile is the largest whole number of output rows that
+  // fits 128 positions, so its band is exactly rows + R - 1 input rows (at
+  // 56x56: 2 rows = 116 positions, a 4-row band instead of the 7 rows a tile
+  // starting mid-row needs).  The MMA still reads 128 rows of A; rows past the
+  // tile are junk (beyond the band: the next shared-memory region) and the
+  // epilogue drops them.  RFK_BAND_ALIGN=0: 128-position tiles; 2: aligned
+  // whatever the channel count.
+  static const int align = [] {
+    const char* e = std::getenv("RFK_BAND_ALIGN");
+    return e ? std::atoi(e) : 1;
+  }();
+  // (measured: aligned wins with two or more 64-channel blocks, whose bands
+  // repeat per block -- 56x56x128 -> 32: 43.6 -> 24.8 us -- and loses ~10 %
+  // with one, whose 7-row band already fits next to the resident weights)
+  const int rpt = bp.Wp <= kBM ? kBM / bp.Wp : 0;
+  if (align && rpt >= 1 && (bp.cblocks >= 2 || align == 2)) {
+    bp.tile_pos = rpt * bp.Wp;
+    bp.BR = std::min(rpt, g.P) + g.R - 1;
+    bp.tiles_per_img = (g.P + rpt - 1) / rpt;
+  } else {
+    bp.tile_pos = kBM;
+    bp.BR = band_rows(bp.Wp, g.R);
+    bp.tiles_per_img = (bp.plane + kBM - 1) / kBM;
+  }
   bp.m_tiles = g.N * bp.tiles_per_img;
   bp.box_bytes = 64 * 2 * bp.Wp * bp.BR;
   bp.band_bytes = (bp.box_bytes + 1023) / 1024 * 1024;

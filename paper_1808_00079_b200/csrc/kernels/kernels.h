@@ -61,9 +61,10 @@ struct GemmDesc {
   bool remap = false;
   int rP = 0, rQ = 0, rH = 0, rW = 0, rsh = 1, rsw = 1;
   int block_n = 0;  // 0 = pick automatically (64 / 128 / 256)
-  // Im2colK A of a stride-1 conv: use the shifted-band kernel (gemm_band.cu)
-  // when gemm_band_ok() accepts the shape
-  bool band = false;
+  // Im2colK A of a stride-1 conv: the shifted-band kernel (gemm_band.cu).
+  // 0 never; 1 where gemm_band_preferred() (measured faster than TMA im2col);
+  // 2 wherever gemm_band_ok() accepts the shape
+  int band = 0;
   // fused BatchNorm apply on the bf16 output (re-forward, statistics known):
   // bn_out = [relu](out * bn_scale + bn_shift), per column
   void* bn_out = nullptr;
@@ -92,6 +93,7 @@ struct GemmDesc {
 
 cudaError_t gemm_launch(const GemmDesc& d, cudaStream_t stream);
 bool gemm_band_ok(const GemmDesc& d);
+bool gemm_band_preferred(const GemmDesc& d);
 cudaError_t gemm_band_launch(const GemmDesc& d, cudaStream_t stream);
 int gemm_m_tiles(const GemmDesc& d);
 int gemm_block_n(const GemmDesc& d);  // tile width the launch will use

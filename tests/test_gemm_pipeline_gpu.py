@@ -84,3 +84,36 @@ def test_k_blocks_per_stage_bit_identical(tmp_path):
                                g.view(torch.int16) if g.dtype == torch.bfloat16 else g.view(torch.int32)), \
                 f"output {i} differs with RFK_GEMM_KPS={kps}"
         assert any(t.abs().sum() > 0 for t in got)
+
+
+@pytest.mark.parametrize("C,Co", [(64, 64), (32, 128), (64, 32)])
+def test_band_kernel_bit_identical_to_im2col_with_one_channel_block(C, Co):
+    """With one 64-channel block of A the shifted-band kernel sums the K blocks
+    (filter taps) in the TMA im2col kernel's order, so the two produce the same
+    bits (the executor relies on it: a conv may run either way in different
+    plans, e.g. band in the first forward and im2col with a fused BN in the
+    re-forward).  Forward (K-major weights) and data gradient (flipped taps)."""
+    from paper_1808_00079_b200 import kernels as K
+    torch.manual_seed(0)
+    n, h = 8, 56
+    x = (torch.randn(n, h, h, C, device="cuda") * 0.5).to(torch.bfloat16)
+    w = (torch.randn(Co, 9 * 64, device="cuda") * 0.1).to(torch.bfloat16)
+    w[:, :].view(Co, 9, 64)[:, :, C:] = 0
+    wt = (torch.randn(C, 3, 3, Co, device="cuda") * 0.1).to(torch.bfloat16)  # dgrad: [cout=C of dy][tap][cin=Co]
+    g = K.ConvGeom(n, h, h, C, h, h, 3, 3, 1, 1, 1, 1)
+    outs = {}
+    for band in (0, 1):
+        o = torch.zeros(n * h * h, Co, device="cuda", dtype=torch.bfloat16)
+        K.gemm(K.GemmArgs(M=n * h * h, N=Co, K=9 * 64, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=K.KMAJOR,
+                          b=w.data_ptr(), b_ld=9 * 64, out=o.data_ptr(), ldc=Co, splits=1, band=band))
+        d = torch.zeros(n * h * h, Co, device="cuda", dtype=torch.bfloat16)
+        ga = K.GemmArgs(M=n * h * h, N=Co, K=9 * 64, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=4,
+                        b=wt.data_ptr(), out=d.data_ptr(), ldc=Co, splits=1, band=band)
+        for k, v in {"b_extent": Co, "b_taps": 9, "b_cpad": Co, "b_rows": C}.items():
+            setattr(ga, k, v)
+        K.gemm(ga)
+        torch.cuda.synchronize()
+        outs[band] = (o, d)
+    for a, b in zip(outs[0], outs[1]):
+        assert a.abs().sum() > 0
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))

@@ -31,22 +31,25 @@ def timeit(ga, iters=20):
     return e0.elapsed_time(e1) * 1e3 / iters
 
 
-for (n, h, c) in [(32, 56, 64), (32, 28, 128), (32, 14, 256)]:
+# ResNet-50 3x3 convs (c -> c) and DenseNet-121 growth convs (128 -> 32)
+for (n, h, c, co) in [(32, 56, 64, 64), (32, 28, 128, 128), (32, 14, 256, 256), (32, 56, 128, 32), (32, 28, 128, 32)]:
     x = bf(n, h, h, c)
-    w = bf(c, 9 * c)
+    w = bf(co, 9 * c)
     wt = bf(c, 3, 3, c)
-    o = bf(n, h, h, c)
-    st = torch.zeros(160, 2, c, device=dev)
+    o = bf(n, h, h, max(c, co))
+    st = torch.zeros(160, 2, co, device=dev)
     g = K.ConvGeom(n, h, h, c, h, h, 3, 3, 1, 1, 1, 1)
     M = n * h * h
-    fl = 2.0 * M * c * 9 * c
+    fl = 2.0 * M * co * 9 * c
     for band in (0, 1):
-        fp = K.GemmArgs(M=M, N=c, K=9 * c, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=K.KMAJOR,
-                        b=w.data_ptr(), b_ld=9 * c, out=o.data_ptr(), ldc=c, stats=st.data_ptr(), splits=1, band=band)
+        fp = K.GemmArgs(M=M, N=co, K=9 * c, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=K.KMAJOR,
+                        b=w.data_ptr(), b_ld=9 * c, out=o.data_ptr(), ldc=co, stats=st.data_ptr(), splits=1, band=band)
         dg = K.GemmArgs(M=M, N=c, K=9 * c, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=4, b=wt.data_ptr(),
                         out=o.data_ptr(), ldc=c, splits=1, band=band)
         for k, v in {"b_extent": c, "b_taps": 9, "b_cpad": c, "b_rows": c}.items():
             setattr(dg, k, v)
         for name, ga in (("fprop+stats", fp), ("dgrad", dg)):
+            if name == "dgrad" and co != c:
+                continue
             us = timeit(ga)
-            print(f"3x3 {h}x{h}x{c} {name:12s} band={band}: {us:7.1f} us  {fl / us / 1e6:7.1f} TFLOP/s")
+            print(f"3x3 {h}x{h}x{c}->{co} {name:12s} band={band}: {us:7.1f} us  {fl / us / 1e6:7.1f} TFLOP/s")

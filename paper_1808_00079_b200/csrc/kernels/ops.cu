@@ -129,8 +129,11 @@ __global__ void __launch_bounds__(kThreads) colstats_kernel(const __nv_bfloat16*
 
 // Sum `parts` partial rows [parts][2][C] in a fixed tree: channel per
 // threadIdx.x (32 wide), partial subsets per threadIdx.y (32 deep, two
-// independent accumulators each), then a fixed-shape smem tree over y.
+// independent accumulators each), then a fixed butterfly over the subsets.
+// The sums of channel blockIdx.x * 32 + j are returned to warp j (threadIdx.y
+// == j; the caller's channel is fin_channel()).
 constexpr int kFinY = 32;
+__device__ __forceinline__ int fin_channel() { return blockIdx.x * 32 + threadIdx.y; }
 __device__ __forceinline__ void sum_partials(const float* __restrict__ partials, int parts, int C, int c, float& s0,
                                              float& s1) {
   __shared__ float sh0[kFinY][33], sh1[kFinY][33];
@@ -163,15 +166,18 @@ __device__ __forceinline__ void sum_partials(const float* __restrict__ partials,
   sh0[threadIdx.y][threadIdx.x] = a0 + a1;
   sh1[threadIdx.y][threadIdx.x] = b0 + b1;
   __syncthreads();
-  for (int w = kFinY / 2; w > 0; w >>= 1) {
-    if ((int)threadIdx.y < w) {
-      sh0[threadIdx.y][threadIdx.x] += sh0[threadIdx.y + w][threadIdx.x];
-      sh1[threadIdx.y][threadIdx.x] += sh1[threadIdx.y + w][threadIdx.x];
-    }
-    __syncthreads();
+  // transposed: warp y reduces channel y's 32 row-group sums (lane = row
+  // group) with a fixed xor butterfly -- one barrier instead of a 5-level
+  // smem tree with a barrier per level.  The results land in warp y (every
+  // lane) for channel blockIdx.x * 32 + y.
+  float t0 = sh0[threadIdx.x][threadIdx.y], t1 = sh1[threadIdx.x][threadIdx.y];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    t0 += __shfl_xor_sync(0xffffffffu, t0, off);
+    t1 += __shfl_xor_sync(0xffffffffu, t1, off);
   }
-  s0 = sh0[0][threadIdx.x];
-  s1 = sh1[0][threadIdx.x];
+  s0 = t0;
+  s1 = t1;
 }
 
 __global__ void bn_finalize_kernel(const float* __restrict__ partials, int parts, int C, float count,
@@ -180,10 +186,10 @@ __global__ void bn_finalize_kernel(const float* __restrict__ partials, int parts
                                    float* __restrict__ shift, float* __restrict__ run_mean, float* __restrict__ run_var,
                                    float momentum, int update_running) {
   pdl_enter();
-  const int c = blockIdx.x * 32 + threadIdx.x;
   float s0, s1;
-  sum_partials(partials, parts, C, c, s0, s1);
-  if (threadIdx.y != 0 || c >= C) return;
+  sum_partials(partials, parts, C, blockIdx.x * 32 + threadIdx.x, s0, s1);
+  const int c = fin_channel();
+  if (threadIdx.x != 0 || c >= C) return;
   const float mu = s0 / count;
   const float var = fmaxf(s1 / count - mu * mu, 0.f);
   const float is = rsqrtf(var + eps);
@@ -210,8 +216,8 @@ __global__ void bn_finalize_gather_kernel(const BnGatherBlock* __restrict__ tabl
   const BnGatherBlock b = table[blockIdx.x];
   float s0, s1;
   sum_partials(b.partials, b.parts, b.Csrc, b.coff + (int)threadIdx.x, s0, s1);
-  const int c = blockIdx.x * 32 + threadIdx.x;
-  if (threadIdx.y != 0 || c >= C) return;
+  const int c = fin_channel();
+  if (threadIdx.x != 0 || c >= C) return;
   const float mu = s0 / count;
   const float var = fmaxf(s1 / count - mu * mu, 0.f);
   const float is = rsqrtf(var + eps);
@@ -379,10 +385,10 @@ __global__ void bn_bwd_finalize_kernel(const float* __restrict__ partials, int p
                                        const float* __restrict__ invstd, float* __restrict__ dgamma,
                                        float* __restrict__ dbeta, float* __restrict__ coef) {
   pdl_enter();
-  const int c = blockIdx.x * 32 + threadIdx.x;
   float sg, sgy;
-  sum_partials(partials, parts, C, c, sg, sgy);
-  if (threadIdx.y != 0 || c >= C) return;
+  sum_partials(partials, parts, C, blockIdx.x * 32 + threadIdx.x, sg, sgy);
+  const int c = fin_channel();
+  if (threadIdx.x != 0 || c >= C) return;
   const float is = invstd[c];
   const float sgx = sgy * is;
   dbeta[c] = sg;

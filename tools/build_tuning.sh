@@ -1,5 +1,6 @@
 #!/bin/bash
-# production build + a tuning build of gemm.cu (RFK_GEMM_TUNING=1) linked into build/ab/lib_tune.so
+# production build + a tuning build of gemm.cu (RFK_GEMM_TUNING=1: timing experiments, RFK_GEMM_DBG timelines)
+# linked into build/ab/lib_tune.so; select it with RF_LIB_PATH=build/ab/lib_tune.so (tools/gemm_probe.py etc.)
 set -e
 python -m paper_1808_00079_b200.build >/dev/null
 mkdir -p build/ab

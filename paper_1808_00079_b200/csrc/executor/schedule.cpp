@@ -689,7 +689,10 @@ long im2col_chunk_bytes() {
 // split-K of a weight-gradient GEMM: enough splits for about one persistent
 // wave (148 CTAs), each split keeping >= 8 K blocks (RFK_WG_SPLIT_CAP caps it)
 int wgrad_splits(long tiles, long kblocks) {
-  long s = (148 + tiles - 1) / tiles;
+  // as many K splits as keep tiles x splits within ONE wave of 148 CTAs: a
+  // ceil here made e.g. 3 tiles x 50 splits = 150 units, so two CTAs ran a
+  // second unit and the launch took two unit times
+  long s = std::max(1L, 148 / std::max(1L, tiles));
   s = std::min(s, std::max(1L, kblocks / 8));
   static const long cap = std::getenv("RFK_WG_SPLIT_CAP") ? std::atol(std::getenv("RFK_WG_SPLIT_CAP")) : 148;
   return (int)std::max(1L, std::min(s, cap));

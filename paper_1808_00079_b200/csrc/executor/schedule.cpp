@@ -693,7 +693,9 @@ int wgrad_splits(long tiles, long kblocks) {
   // ceil here made e.g. 3 tiles x 50 splits = 150 units, so two CTAs ran a
   // second unit and the launch took two unit times
   long s = std::max(1L, 148 / std::max(1L, tiles));
-  s = std::min(s, std::max(1L, kblocks / 8));
+  // at least kMinKb K blocks per split (RFK_WG_MIN_KB, diagnostics)
+  static const long min_kb = std::getenv("RFK_WG_MIN_KB") ? std::atol(std::getenv("RFK_WG_MIN_KB")) : 8;
+  s = std::min(s, std::max(1L, kblocks / std::max(1L, min_kb)));
   static const long cap = std::getenv("RFK_WG_SPLIT_CAP") ? std::atol(std::getenv("RFK_WG_SPLIT_CAP")) : 148;
   return (int)std::max(1L, std::min(s, cap));
 }

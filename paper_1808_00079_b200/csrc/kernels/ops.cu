@@ -510,6 +510,66 @@ __global__ void __launch_bounds__(kThreads) relu_bwd_kernel(const __nv_bfloat16*
 }
 
 // ------------------------------------------------------------ pooling
+// Compile-time k x k window (the stem's 3x3 / 2): all k*k 16-byte loads of an
+// output vector are issued before any comparison (the loop form waits for
+// each load in turn: 1.5 TB/s on the stem pool); out-of-image taps are
+// masked, and the comparisons run in the same (r, s) order with the same
+// strict '>' (first argmax), so outputs and indices are the loop form's bits.
+template <int KW>
+__global__ void __launch_bounds__(kThreads) maxpool_fwd_k_kernel(const __nv_bfloat16* __restrict__ x, PoolGeom g,
+                                                                __nv_bfloat16* __restrict__ y,
+                                                                uint8_t* __restrict__ idx) {
+  pdl_enter();
+  const int cv = g.C / 8;
+  const unsigned total = (unsigned)g.N * g.P * g.Q * cv;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % (unsigned)cv);
+    unsigned t = i / (unsigned)cv;
+    const int q = (int)(t % (unsigned)g.Q);
+    t /= (unsigned)g.Q;
+    const int p = (int)(t % (unsigned)g.P);
+    const int n = (int)(t / (unsigned)g.P);
+    const int h0 = p * g.stride - g.pad, w0 = q * g.stride - g.pad;
+    uint4 v[KW * KW];
+    bool ok[KW * KW];
+#pragma unroll
+    for (int r = 0; r < KW; ++r)
+#pragma unroll
+      for (int s = 0; s < KW; ++s) {
+        const int h = h0 + r, w = w0 + s;
+        ok[r * KW + s] = h >= 0 && h < g.H && w >= 0 && w < g.W;
+        v[r * KW + s] = ok[r * KW + s] ? ldg16(x + (((long)n * g.H + h) * g.W + w) * g.C + c8 * 8)
+                                       : make_uint4(0u, 0u, 0u, 0u);
+      }
+    float m[8];
+    uint32_t best[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      m[k] = -INFINITY;
+      best[k] = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < KW * KW; ++j) {
+      if (!ok[j]) continue;
+      float f[8];
+      unpack8(v[j], f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (f[k] > m[k]) {
+          m[k] = f[k];
+          best[k] = (uint32_t)j;
+        }
+    }
+    *reinterpret_cast<uint4*>(y + (size_t)i * 8) = pack8(m);
+    if (idx) {
+      uint2 o;
+      o.x = best[0] | (best[1] << 8) | (best[2] << 16) | (best[3] << 24);
+      o.y = best[4] | (best[5] << 8) | (best[6] << 16) | (best[7] << 24);
+      *reinterpret_cast<uint2*>(idx + (size_t)i * 8) = o;
+    }
+  }
+}
+
 // idx (optional): the first-argmax window position of every output, for the
 // backward gather (same rule as maxpool_argmax_kernel)
 __global__ void __launch_bounds__(kThreads) maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, PoolGeom g,
@@ -716,6 +776,70 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __
     if (acc) {
       float pv[8];
       unpack8(*reinterpret_cast<const uint4*>(dx + (size_t)i * 8), pv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum[k] += pv[k];
+    }
+    *reinterpret_cast<uint4*>(dx + (size_t)i * 8) = pack8(sum);
+  }
+}
+
+// Gather with a compile-time k x k / stride window: the (at most
+// ceil(k / stride))^2 covering windows' index and dy loads are all issued
+// before the sums, which run in the loop form's (p, q) order (same bits).
+template <int KW, int KS>
+__global__ void __launch_bounds__(kThreads) maxpool_bwd_k_kernel(const uint8_t* __restrict__ idx,
+                                                                const __nv_bfloat16* __restrict__ dy, PoolGeom g,
+                                                                __nv_bfloat16* __restrict__ dx, int acc) {
+  pdl_enter();
+  constexpr int NW = (KW + KS - 1) / KS;  // covering windows per dimension
+  const int cv = g.C / 8;
+  const unsigned total = (unsigned)g.N * g.H * g.W * cv;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % (unsigned)cv);
+    unsigned t = i / (unsigned)cv;
+    const int w = (int)(t % (unsigned)g.W);
+    t /= (unsigned)g.W;
+    const int h = (int)(t % (unsigned)g.H);
+    const int n = (int)(t / (unsigned)g.H);
+    const int p_lo = max(0, (h + g.pad - KW + KS) / KS);
+    const int p_hi = min(g.P - 1, (h + g.pad) / KS);
+    const int q_lo = max(0, (w + g.pad - KW + KS) / KS);
+    const int q_hi = min(g.Q - 1, (w + g.pad) / KS);
+    uint2 iv[NW * NW];
+    uint4 dv[NW * NW];
+    bool ok[NW * NW];
+#pragma unroll
+    for (int a = 0; a < NW; ++a)
+#pragma unroll
+      for (int b = 0; b < NW; ++b) {
+        const int p = p_lo + a, q = q_lo + b;
+        const int j = a * NW + b;
+        ok[j] = p <= p_hi && q <= q_hi;
+        const long o = ((((long)n * g.P + p) * g.Q + q) * cv + c8);
+        iv[j] = ok[j] ? __ldg(reinterpret_cast<const uint2*>(idx + o * 8)) : make_uint2(0xffffffffu, 0xffffffffu);
+        dv[j] = ok[j] ? ldg16(dy + o * 8) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    uint4 prev = make_uint4(0u, 0u, 0u, 0u);
+    if (acc) prev = *reinterpret_cast<const uint4*>(dx + (size_t)i * 8);
+    float sum[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum[k] = 0.f;
+#pragma unroll
+    for (int j = 0; j < NW * NW; ++j) {
+      if (!ok[j]) continue;
+      const int p = p_lo + j / NW, q = q_lo + j % NW;
+      const uint32_t self = (uint32_t)((h - (p * KS - g.pad)) * KW + (w - (q * KS - g.pad)));
+      float d[8];
+      unpack8(dv[j], d);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t b = ((k < 4 ? iv[j].x : iv[j].y) >> (8 * (k & 3))) & 0xffu;
+        if (b == self) sum[k] += d[k];
+      }
+    }
+    if (acc) {
+      float pv[8];
+      unpack8(prev, pv);
 #pragma unroll
       for (int k = 0; k < 8; ++k) sum[k] += pv[k];
     }
@@ -1732,7 +1856,12 @@ cudaError_t maxpool_fwd(const __nv_bfloat16* x, const PoolGeom& g, __nv_bfloat16
   if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   if (idx && g.k * g.k > 256) return cudaErrorInvalidValue;
   const long work = (long)g.N * g.P * g.Q * (g.C / 8);
-  RFK_CHECK_LAUNCH(launch_k(maxpool_fwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y, idx));
+  if (g.k == 3)
+    RFK_CHECK_LAUNCH(launch_k(maxpool_fwd_k_kernel<3>, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y, idx));
+  else if (g.k == 2)
+    RFK_CHECK_LAUNCH(launch_k(maxpool_fwd_k_kernel<2>, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y, idx));
+  else
+    RFK_CHECK_LAUNCH(launch_k(maxpool_fwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, x, g, y, idx));
   return cudaGetLastError();
 }
 
@@ -1740,8 +1869,18 @@ cudaError_t maxpool_bwd_from_idx(const uint8_t* idx, const __nv_bfloat16* dy, co
                                  bool acc, cudaStream_t st) {
   if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   const long work = (long)g.N * g.H * g.W * (g.C / 8);
-  RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
-                            acc ? 1 : 0));
+  if (g.k == 3 && g.stride == 2)
+    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<3, 2>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+                              acc ? 1 : 0));
+  else if (g.k == 2 && g.stride == 2)
+    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<2, 2>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+                              acc ? 1 : 0));
+  else if (g.k == 3 && g.stride == 1)
+    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<3, 1>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+                              acc ? 1 : 0));
+  else
+    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+                              acc ? 1 : 0));
   return cudaGetLastError();
 }
 

@@ -11,6 +11,8 @@ ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 4
     -o $o/gemm_full python tools/profile_step.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:bn_bwd -s 4 -c 6 \
     -o $o/bn_full python tools/profile_step.py > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"gemm_band|maxpool" -c 6 \
+    -o $o/band_pool_full python tools/profile_step.py > /dev/null 2>&1
 # 3. per-GEMM and per-instruction breakdowns (CUDA events, no profiler)
 python tools/gemm_breakdown.py reforward resnet50 32 224 > $o/gemm_breakdown.txt 2>&1
 python tools/step_breakdown.py resnet50 reforward 32 224 > $o/step_breakdown.txt 2>&1

@@ -40,7 +40,9 @@ typedef struct rfx_gemm_args {
   int32_t block_n;
   int64_t b_extent;                  /* valid MN extent of an MN-major B (0 = N) */
   int32_t b_taps, b_cpad, b_rows;    /* kind 4 (conv weights as dgrad B): R*S, Cpad, Cout */
-  int32_t band;                      /* stride-1 im2col A: use the shifted-band kernel when eligible */
+  int32_t band;                      /* stride-1 im2col A: nonzero = the shifted-band kernel wherever the shape and
+                                      * epilogue allow it (the executor uses it only where it measured faster);
+                                      * with one 64-channel block of A its bits equal the im2col kernel's */
   int32_t b_tap_map;                 /* kind 4: nonzero = weight tap of A tap (r, s) is base - r*dr - s*ds */
   int32_t b_tap_base, b_tap_dr, b_tap_ds;  /* (sub-pixel dgrad classes); zero = flipped full filter */
   /* BN+ReLU backward statistics in the epilogue (with `stats`): out (dout of

@@ -282,7 +282,8 @@ def test_gemm_split_partials_isolated():
 # ResNet / DenseNet / Inception 3x3 (and 1x7 / 7x1) shapes.
 BAND_CASES = [(2, 28, 28, 64, 64, 3, 3, 1, 1), (1, 56, 56, 64, 64, 3, 3, 1, 1), (2, 28, 28, 128, 128, 3, 3, 1, 1),
               (2, 30, 30, 96, 64, 3, 3, 0, 0), (2, 35, 35, 64, 96, 5, 5, 2, 2), (2, 28, 28, 64, 192, 1, 7, 0, 3),
-              (2, 28, 28, 64, 72, 7, 1, 3, 0), (1, 32, 40, 160, 200, 3, 3, 1, 1)]
+              (2, 28, 28, 64, 72, 7, 1, 3, 0), (1, 32, 40, 160, 200, 3, 3, 1, 1),
+              (2, 56, 56, 128, 32, 3, 3, 1, 1), (3, 28, 28, 256, 32, 3, 3, 1, 1)]  # DenseNet growth convs (row-aligned bands)
 
 
 @pytest.mark.parametrize("N,H,W,Ci,Co,R,S,ph,pw", BAND_CASES)

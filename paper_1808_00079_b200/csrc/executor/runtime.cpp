@@ -642,7 +642,7 @@ void Net::op_forward(const Op& op, bool reforward, int phase, cudaStream_t st) {
       const BNState& b = bns_[op.bn];
       float* S = d_state_;
       if (phase == 1) {  // residual add, phase 1: out <- skip (exact copy)
-        check(cudaMemcpyAsync(tptr(op.out), tptr(op.in[1]), y.bytes(), cudaMemcpyDeviceToDevice, st), "skip copy");
+        check(rfk::copy_bytes(tptr(op.out), tptr(op.in[1]), y.bytes(), st), "skip copy");
         break;
       }
       if (!reforward && op.bn_gather >= 0) {
@@ -810,7 +810,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
           d.b_kind = rfk::Operand::MNMajor2D;  // W[co][ci]: K = co rows, N = ci contiguous
           d.b_ld = op.cpad;
           if (op.stride > 1) {
-            if (!acc(0)) check(cudaMemsetAsync(dx, 0, x.bytes(), st), "memset");
+            if (!acc(0)) check(rfk::fill_zero(dx, x.bytes(), st), "zero dx");
             d.accumulate_out = acc(0);
             d.remap = true;
             d.rP = y.H;
@@ -847,7 +847,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
                 const SubpixelDim cw = subpixel_dim(b, st_, op.S, op.pad_w, x.W);
                 empty |= ch.J == 0 || cw.J == 0;
               }
-            if (empty && !acc(0)) check(cudaMemsetAsync(dx, 0, x.bytes(), st), "memset");
+            if (empty && !acc(0)) check(rfk::fill_zero(dx, x.bytes(), st), "zero dx");
             // classes write disjoint pixels: up to four run concurrently
             // (each alone is too small to fill the GPU)
             const bool par = st_ == 2 && sub_parallel();
@@ -1096,7 +1096,7 @@ void Net::op_backward(const Op& op, cudaStream_t st) {
       const int ldd = round8(op.classes);
       trace_flops_ = 2.0 * batch_ * op.classes * op.cin;
       // bf16 copy of dlogits with 16-byte aligned rows for TMA
-      check(cudaMemsetAsync(ws_misc, 0, (long)batch_ * ldd * 2, st), "memset");
+      check(rfk::fill_zero(ws_misc, (long)batch_ * ldd * 2, st), "zero");
       check(rfk::cast_f32_bf16_2d(dlog, batch_, op.classes, ldd, ws_misc, st), "cast");
       check(rfk::colsum_f32(dlog, batch_, op.classes, d_grad_ + params_[op.b_param].offset, false, st), "db");
       __nv_bfloat16* dx = gptr(op.in[0]);

@@ -2071,6 +2071,54 @@ cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bf
   return cudaGetLastError();
 }
 
+// Zero fill / copy of 16-byte-aligned device ranges as PDL kernels: inside
+// the step's graph a memset or memcpy node is not a programmatic dependent of
+// the kernel before it, so it would cut the launch / prologue overlap of the
+// kernel chain around it (a 51 MB memset before a strided 1x1 dgrad, the
+// residual add's skip copy).
+__global__ void __launch_bounds__(kThreads) fill_zero_kernel(uint4* __restrict__ p, unsigned long n16) {
+  pdl_enter();
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+  for (unsigned long i = blockIdx.x * (unsigned long)blockDim.x + threadIdx.x; i < n16;
+       i += (unsigned long)gridDim.x * blockDim.x)
+    p[i] = z;
+}
+
+__global__ void __launch_bounds__(kThreads) copy16_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                          unsigned long n16) {
+  pdl_enter();
+  unsigned long i = blockIdx.x * (unsigned long)blockDim.x + threadIdx.x;
+  const unsigned long step = (unsigned long)gridDim.x * blockDim.x;
+  for (; i + 3 * step < n16; i += 4 * step) {  // four 16-byte loads in flight
+    const uint4 a = __ldg(src + i), b = __ldg(src + i + step), c = __ldg(src + i + 2 * step),
+                d = __ldg(src + i + 3 * step);
+    dst[i] = a;
+    dst[i + step] = b;
+    dst[i + 2 * step] = c;
+    dst[i + 3 * step] = d;
+  }
+  for (; i < n16; i += step) dst[i] = __ldg(src + i);
+}
+
+cudaError_t fill_zero(void* p, long bytes, cudaStream_t st) {
+  if (bytes <= 0) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(p) & 15) || (bytes & 15)) return cudaMemsetAsync(p, 0, bytes, st);
+  const unsigned long n16 = (unsigned long)bytes / 16;
+  RFK_CHECK_LAUNCH(launch_k(fill_zero_kernel, grid_for((long)n16, kThreads * 4, 148 * 8), kThreads, 0, st,
+                            static_cast<uint4*>(p), n16));
+  return cudaGetLastError();
+}
+
+cudaError_t copy_bytes(void* dst, const void* src, long bytes, cudaStream_t st) {
+  if (bytes <= 0) return cudaSuccess;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) || (bytes & 15))
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st);
+  const unsigned long n16 = (unsigned long)bytes / 16;
+  RFK_CHECK_LAUNCH(launch_k(copy16_kernel, grid_for((long)n16, kThreads * 4, 148 * 8), kThreads, 0, st,
+                            static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16));
+  return cudaGetLastError();
+}
+
 cudaError_t zero_insert(const __nv_bfloat16* dy, int N, int P, int Q, int C, int Hu, int Wu, int stride,
                         __nv_bfloat16* u, cudaStream_t st) {
   const long work = (long)N * Hu * Wu * (C / 8);

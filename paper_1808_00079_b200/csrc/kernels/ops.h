@@ -97,6 +97,9 @@ struct WeightPrepLayer {
 cudaError_t weight_prep_batched(const WeightPrepLayer* table_dev, int layers, long total, cudaStream_t st);
 cudaError_t pack_input(const float* x, int N, int C, int H, int W, int Cpad, __nv_bfloat16* out, cudaStream_t st);
 cudaError_t im2col(const __nv_bfloat16* x, const ConvShape& g, int Kpad, __nv_bfloat16* out, cudaStream_t st);
+// zero fill / device copy as PDL kernels (16-byte aligned; else cudaMemset / cudaMemcpy)
+cudaError_t fill_zero(void* p, long bytes, cudaStream_t st);
+cudaError_t copy_bytes(void* dst, const void* src, long bytes, cudaStream_t st);
 cudaError_t zero_insert(const __nv_bfloat16* dy, int N, int P, int Q, int C, int Hu, int Wu, int stride,
                         __nv_bfloat16* u, cudaStream_t st);
 cudaError_t concat(const __nv_bfloat16* a, int Ca, const __nv_bfloat16* b, int Cb, long M, __nv_bfloat16* c,

@@ -182,7 +182,9 @@ class Net {
   // step k runs hides the host->device copy behind the step.
   void stage_batch(const float* images_host, const int* labels_host, int slot, cudaStream_t copy_st);
   void use_batch(int slot, cudaStream_t st);
-  void forward_backward(cudaStream_t st);  // loss + gradients (no update)
+  // loss + gradients; with early_sgd, also the momentum SGD of every gradient
+  // bucket as soon as the backward has finalised it (returns whether it did)
+  bool forward_backward(cudaStream_t st, bool early_sgd = false);
   void update(float lr, float momentum, float wd, cudaStream_t st) {  // SGD + weight prep
     set_hyper(lr, momentum, wd, st);
     update(st);
@@ -345,6 +347,7 @@ class Net {
   std::vector<cudaEvent_t> bucket_events_;
   cudaEvent_t comm_done_ = nullptr;
   long bucket_floats_ = 0;
+  bool buckets_for_sgd_ = false;  // buckets_ planned without a communicator (early SGD)
   void plan_buckets();
   void* d_prep_table_ = nullptr;
   // BN over concatenations (DenseNet): per BN, the concat's leaf tensors in

@@ -1384,7 +1384,7 @@ void Net::plan_buckets() {
       reduced = frontier;
     }
   }
-  if (!comm_) return;  // dry run (bucket_plan): no device events needed
+  if (!comm_ && !buckets_for_sgd_) return;  // dry run (bucket_plan): no device events needed
   for (auto e : bucket_events_) cudaEventDestroy(e);
   bucket_events_.assign(buckets_.size(), nullptr);
   for (auto& e : bucket_events_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -1435,10 +1435,32 @@ void Net::join_wgrad(cudaStream_t st) {
   wgrad_pending_ = false;
 }
 
-void Net::forward_backward(cudaStream_t st) {
+bool Net::forward_backward(cudaStream_t st, bool early_sgd) {
   if (!setup_done_) throw std::invalid_argument("setup the network first");
   im2col_holder_ = -1;  // a new batch: the stem's im2col is rebuilt by the first forward
   const bool dp = comm_ && comm_->ready() && comm_->nranks() > 0;
+  // Early SGD (whole steps only): each gradient bucket -- the longest suffix
+  // of the flat buffer whose parameters' backward (and pending weight-gradient
+  // GEMMs) are complete -- is updated on the side stream right away (after
+  // its all-reduce when data-parallel), overlapping the rest of the backward.
+  // Safe because a parameter is never read again in a step after its own
+  // backward (re-forwards precede it), and the update is elementwise, so the
+  // results are bit-identical to one update pass at the end.
+  static const bool early_on = !std::getenv("RFK_EARLY_SGD") || std::atoi(std::getenv("RFK_EARLY_SGD")) != 0;
+  early_sgd = early_sgd && early_on;
+  if (early_sgd && !dp && (!buckets_for_sgd_ || bucket_events_.size() != buckets_.size())) {
+    static const long mb = std::getenv("RFK_SGD_BUCKET_MB") ? std::atol(std::getenv("RFK_SGD_BUCKET_MB")) : 16;
+    buckets_for_sgd_ = true;
+    bucket_floats_ = std::max(1L, (mb << 20) / 4);
+    if (!comm_stream_) check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "update stream");
+    plan_buckets();
+  }
+  if (early_sgd) {
+    long covered = 0;
+    for (const auto& bk : buckets_) covered += bk.hi - bk.lo;
+    if (covered != n_params_) early_sgd = false;  // not every parameter finishes in a bucket: one pass at the end
+  }
+  const bool bucketed = dp || early_sgd;
   size_t b = 0;
   std::vector<std::pair<long, long>> wa, wg;
   auto overlaps = [](const std::vector<std::pair<long, long>>& w, const std::vector<std::pair<long, long>>& r) {
@@ -1460,7 +1482,7 @@ void Net::forward_backward(cudaStream_t st) {
       }
     }
     run_instr(sched_[k], st);
-    while (dp && b < buckets_.size() && buckets_[b].after_instr == k) {
+    while (bucketed && b < buckets_.size() && buckets_[b].after_instr == k) {
       // the bucket's weight gradients must be complete: the comm stream (not
       // this one) waits for the pending side-stream weight-gradient GEMMs, so
       // the backward keeps going; the wgrad read sets stay pending for the
@@ -1473,21 +1495,29 @@ void Net::forward_backward(cudaStream_t st) {
       // while this stream carries on with the backward
       check(cudaEventRecord(bucket_events_[b], st), "event");
       check(cudaStreamWaitEvent(comm_stream_, bucket_events_[b], 0), "wait");
-      comm_inflight_ = true;
-      std::string err;
-      if (!comm_->allreduce_avg(d_grad_ + buckets_[b].lo, (size_t)(buckets_[b].hi - buckets_[b].lo), comm_stream_,
-                                &err))
-        throw std::runtime_error(err);
+      const long lo = buckets_[b].lo, n = buckets_[b].hi - buckets_[b].lo;
+      if (dp) {
+        comm_inflight_ = true;
+        std::string err;
+        if (!comm_->allreduce_avg(d_grad_ + lo, (size_t)n, comm_stream_, &err)) throw std::runtime_error(err);
+      }
+      if (early_sgd)
+        check(rfk::sgd_update(d_param_ + lo, d_grad_ + lo, d_mom_ + lo, n, d_hyper_, d_bf16_ + lo, comm_stream_),
+              "sgd");
       ++b;
     }
   }
   join_wgrad(st);
   comm_inflight_ = false;
-  if (trace) std::fprintf(stderr, "wgrad joins: %d on activation ranges, %d on gradient ranges\n", joins_act, joins_grad);
-  if (dp) {  // join
+  if (trace)
+    std::fprintf(stderr, "wgrad joins: %d on activation ranges, %d on gradient ranges; %zu buckets, early SGD %d\n",
+                 joins_act, joins_grad, b, (int)early_sgd);
+  if (bucketed) {  // join
+    if (!comm_done_) check(cudaEventCreateWithFlags(&comm_done_, cudaEventDisableTiming), "event");
     check(cudaEventRecord(comm_done_, comm_stream_), "event");
     check(cudaStreamWaitEvent(st, comm_done_, 0), "wait");
   }
+  return early_sgd;
 }
 
 // SGD hyperparameters live in device memory (d_hyper_ = {lr, momentum, wd}),
@@ -1539,8 +1569,9 @@ cudaGraphExec_t Net::capture(const std::function<void(cudaStream_t)>& body, long
 
 void Net::run_phase(int phase, float lr, float momentum, float wd, cudaStream_t st, bool use_graph) {
   auto body = [&](cudaStream_t s) {
-    if (phase == 0 || phase == 2) forward_backward(s);
-    if (phase == 1 || phase == 2) update(s);
+    bool updated = false;
+    if (phase == 0 || phase == 2) updated = forward_backward(s, phase == 2);
+    if ((phase == 1 || phase == 2) && !updated) update(s);
   };
   if (phase == 1 || phase == 2) set_hyper(lr, momentum, wd, st);
   if (!use_graph) {

@@ -322,6 +322,8 @@ class Net {
   float* d_rowloss_ = nullptr;
   float* d_lse_ = nullptr;
   float* d_hyper_ = nullptr;
+  float hyper_last_[3] = {0.f, 0.f, 0.f};  // last values uploaded to d_hyper_
+  bool hyper_valid_ = false;
   cudaGraphExec_t graph_exec_ = nullptr;
   float graph_lr_ = 0, graph_mom_ = 0, graph_wd_ = 0;
   cudaGraphExec_t phase_exec_[3] = {nullptr, nullptr, nullptr};

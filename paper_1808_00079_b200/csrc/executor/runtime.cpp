@@ -1524,9 +1524,14 @@ bool Net::forward_backward(cudaStream_t st, bool early_sgd) {
 // written in stream order before each step, so one captured step graph
 // serves any learning-rate schedule.  The source is pageable: cudaMemcpyAsync
 // stages it before returning, so the stack buffer may go away.
+// Unchanged values are not re-sent (a constant schedule then launches the
+// step graph back to back, without a copy in between).
 void Net::set_hyper(float lr, float momentum, float wd, cudaStream_t st) {
   const float h[3] = {lr, momentum, wd};
+  if (hyper_valid_ && std::memcmp(h, hyper_last_, sizeof h) == 0) return;
   check(cudaMemcpyAsync(d_hyper_, h, sizeof h, cudaMemcpyHostToDevice, st), "hyper h2d");
+  std::memcpy(hyper_last_, h, sizeof h);
+  hyper_valid_ = true;
 }
 
 void Net::update(cudaStream_t st) {

@@ -1325,7 +1325,7 @@ void Net::use_batch(int slot, cudaStream_t st) {
   if (slot < 0 || slot > 1 || !d_stage_images_[slot]) throw std::invalid_argument("slot was never staged");
   const Tensor& in = tensors_[input_t_];
   check(cudaStreamWaitEvent(st, stage_ready_[slot], 0), "wait");
-  check(cudaMemcpyAsync(d_labels_, d_stage_labels_[slot], batch_ * 4, cudaMemcpyDeviceToDevice, st), "labels");
+  check(rfk::copy_bytes(d_labels_, d_stage_labels_[slot], batch_ * 4L, st), "labels");  // a kernel, not a memcpy node
   check(rfk::pack_input(d_stage_images_[slot], batch_, in_c_real_, in.H, in.W, in.C, d_input_, st), "pack_input");
   check(cudaEventRecord(stage_free_[slot], st), "event");
 }

@@ -786,13 +786,13 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_kernel(const uint8_t* __
 // Gather with a compile-time k x k / stride window: the (at most
 // ceil(k / stride))^2 covering windows' index and dy loads are all issued
 // before the sums, which run in the loop form's (p, q) order (same bits).
-template <int KW, int KS>
+template <int KW, int KS, int CV>
 __global__ void __launch_bounds__(kThreads) maxpool_bwd_k_kernel(const uint8_t* __restrict__ idx,
                                                                 const __nv_bfloat16* __restrict__ dy, PoolGeom g,
                                                                 __nv_bfloat16* __restrict__ dx, int acc) {
   pdl_enter();
   constexpr int NW = (KW + KS - 1) / KS;  // covering windows per dimension
-  const int cv = g.C / 8;
+  const int cv = CV > 0 ? CV : g.C / 8;   // compile-time vectors per pixel (the stem: 64 channels)
   const unsigned total = (unsigned)g.N * g.H * g.W * cv;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int c8 = (int)(i % (unsigned)cv);
@@ -829,13 +829,15 @@ __global__ void __launch_bounds__(kThreads) maxpool_bwd_k_kernel(const uint8_t* 
       if (!ok[j]) continue;
       const int p = p_lo + j / NW, q = q_lo + j % NW;
       const uint32_t self = (uint32_t)((h - (p * KS - g.pad)) * KW + (w - (q * KS - g.pad)));
+      // all eight channels' argmax bytes against this pixel's window position
+      // at once (0xff per matching byte); windows selecting none are skipped
+      const uint32_t m0 = __vcmpeq4(iv[j].x, self * 0x01010101u), m1 = __vcmpeq4(iv[j].y, self * 0x01010101u);
+      if ((m0 | m1) == 0u) continue;
       float d[8];
       unpack8(dv[j], d);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t b = ((k < 4 ? iv[j].x : iv[j].y) >> (8 * (k & 3))) & 0xffu;
-        if (b == self) sum[k] += d[k];
-      }
+      for (int k = 0; k < 8; ++k)
+        if (((k < 4 ? m0 : m1) >> (8 * (k & 3))) & 1u) sum[k] += d[k];
     }
     if (acc) {
       float pv[8];
@@ -1869,14 +1871,17 @@ cudaError_t maxpool_bwd_from_idx(const uint8_t* idx, const __nv_bfloat16* dy, co
                                  bool acc, cudaStream_t st) {
   if ((long)g.N * g.H * g.W * (g.C / 8) >= (1L << 31)) return cudaErrorInvalidValue;  // 32-bit indexing
   const long work = (long)g.N * g.H * g.W * (g.C / 8);
-  if (g.k == 3 && g.stride == 2)
-    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<3, 2>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+  if (g.k == 3 && g.stride == 2 && g.C == 64)
+    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<3, 2, 8>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+                              acc ? 1 : 0));
+  else if (g.k == 3 && g.stride == 2)
+    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<3, 2, 0>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
                               acc ? 1 : 0));
   else if (g.k == 2 && g.stride == 2)
-    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<2, 2>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<2, 2, 0>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
                               acc ? 1 : 0));
   else if (g.k == 3 && g.stride == 1)
-    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<3, 1>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
+    RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_k_kernel<3, 1, 0>, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,
                               acc ? 1 : 0));
   else
     RFK_CHECK_LAUNCH(launch_k(maxpool_bwd_kernel, grid_for(work, kThreads * 2), kThreads, 0, st, idx, dy, g, dx,

@@ -32,9 +32,10 @@ def timeit(ga, iters=20):
 
 
 # ResNet-50 3x3 convs (c -> c) and DenseNet-121 growth convs (128 -> 32)
-for (n, h, c, co) in [(32, 56, 64, 64), (32, 28, 128, 128), (32, 14, 256, 256), (32, 56, 128, 32), (32, 28, 128, 32)]:
+for (n, h, c, co) in [(32, 56, 64, 64), (32, 28, 128, 128), (32, 14, 256, 256), (32, 56, 128, 32), (32, 28, 128, 32),
+                      (32, 14, 128, 32), (32, 35, 96, 96), (32, 17, 192, 192)]:
     x = bf(n, h, h, c)
-    w = bf(co, 9 * c)
+    w = bf(co, 9 * ((c + 63) // 64 * 64))
     wt = bf(c, 3, 3, c)
     o = bf(n, h, h, max(c, co))
     st = torch.zeros(160, 2, co, device=dev)
@@ -42,9 +43,10 @@ for (n, h, c, co) in [(32, 56, 64, 64), (32, 28, 128, 128), (32, 14, 256, 256), 
     M = n * h * h
     fl = 2.0 * M * co * 9 * c
     for band in (0, 1):
-        fp = K.GemmArgs(M=M, N=co, K=9 * c, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=K.KMAJOR,
-                        b=w.data_ptr(), b_ld=9 * c, out=o.data_ptr(), ldc=co, stats=st.data_ptr(), splits=1, band=band)
-        dg = K.GemmArgs(M=M, N=c, K=9 * c, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=4, b=wt.data_ptr(),
+        cp = (c + 63) // 64 * 64
+        fp = K.GemmArgs(M=M, N=co, K=9 * cp, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=K.KMAJOR,
+                        b=w.data_ptr(), b_ld=9 * cp, out=o.data_ptr(), ldc=co, stats=st.data_ptr(), splits=1, band=band)
+        dg = K.GemmArgs(M=M, N=c, K=9 * cp, a_kind=K.IM2COL_K, a=x.data_ptr(), a_geom=g, b_kind=4, b=wt.data_ptr(),
                         out=o.data_ptr(), ldc=c, splits=1, band=band)
         for k, v in {"b_extent": c, "b_taps": 9, "b_cpad": c, "b_rows": c}.items():
             setattr(dg, k, v)

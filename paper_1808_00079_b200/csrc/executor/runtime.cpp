@@ -40,6 +40,23 @@ bool fusable_conv_impl(const std::vector<Op>& ops, const std::vector<Tensor>& te
   return bn.kind == OpKind::BN && bn.out >= 0;
 }
 
+// Stream priorities inside the step graph (RFK_PRIO=1): the capture stream
+// (main path: forward, data gradients, BN backward) at the greatest priority,
+// the side streams (weight gradients, sub-pixel classes, all-reduce / SGD) at
+// the least, so when both have CTAs waiting the critical path goes first; the
+// graph is instantiated with node priorities.
+bool prio_enabled() {
+  static const bool on = std::getenv("RFK_PRIO") && std::atoi(std::getenv("RFK_PRIO")) != 0;
+  return on;
+}
+void create_stream(cudaStream_t* s, bool high) {
+  int lo = 0, hi = 0;
+  if (prio_enabled() && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) {
+    if (cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, high ? hi : lo) == cudaSuccess) return;
+  }
+  if (cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) != cudaSuccess) throw std::runtime_error("stream create");
+}
+
 int band_enabled() {
   static const int mode = [] {
     const char* e = std::getenv("RFK_BAND");
@@ -371,14 +388,14 @@ void Net::ensure_sub_streams() {
   if (sub_fork_) return;
   check(cudaEventCreateWithFlags(&sub_fork_, cudaEventDisableTiming), "event");
   for (int i = 0; i < 3; ++i) {
-    check(cudaStreamCreateWithFlags(&sub_stream_[i], cudaStreamNonBlocking), "sub-pixel stream");
+    create_stream(&sub_stream_[i], false);  // sub-pixel stream
     check(cudaEventCreateWithFlags(&sub_join_[i], cudaEventDisableTiming), "event");
   }
 }
 
 void Net::ensure_wgrad_stream() {
   if (wgrad_stream_) return;
-  check(cudaStreamCreateWithFlags(&wgrad_stream_, cudaStreamNonBlocking), "wgrad stream");
+  create_stream(&wgrad_stream_, false);  // weight-gradient stream
   check(cudaEventCreateWithFlags(&wgrad_fork_, cudaEventDisableTiming), "event");
   check(cudaEventCreateWithFlags(&wgrad_join_, cudaEventDisableTiming), "event");
 }
@@ -1541,7 +1558,7 @@ void Net::update(cudaStream_t st) {
 
 cudaGraphExec_t Net::capture(const std::function<void(cudaStream_t)>& body, long* kernel_nodes) {
   cudaStream_t cap;
-  check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream");
+  create_stream(&cap, true);  // capture (main path) stream
   check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
   try {
     body(cap);
@@ -1566,7 +1583,7 @@ cudaGraphExec_t Net::capture(const std::function<void(cudaStream_t)>& body, long
   }
   if (kernel_nodes) *kernel_nodes = kernels;
   cudaGraphExec_t exec = nullptr;
-  check(cudaGraphInstantiate(&exec, g, 0), "instantiate");
+  check(cudaGraphInstantiate(&exec, g, prio_enabled() ? cudaGraphInstantiateFlagUseNodePriority : 0), "instantiate");
   cudaGraphDestroy(g);
   cudaStreamDestroy(cap);
   return exec;

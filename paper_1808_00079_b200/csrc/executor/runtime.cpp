@@ -45,14 +45,17 @@ bool fusable_conv_impl(const std::vector<Op>& ops, const std::vector<Tensor>& te
 // the side streams (weight gradients, sub-pixel classes, all-reduce / SGD) at
 // the least, so when both have CTAs waiting the critical path goes first; the
 // graph is instantiated with node priorities.
-bool prio_enabled() {
-  static const bool on = std::getenv("RFK_PRIO") && std::atoi(std::getenv("RFK_PRIO")) != 0;
-  return on;
+// (RFK_PRIO=2: the other way round, side streams first)
+int prio_mode() {
+  static const int m = std::getenv("RFK_PRIO") ? std::atoi(std::getenv("RFK_PRIO")) : 0;
+  return m;
 }
+bool prio_enabled() { return prio_mode() != 0; }
 void create_stream(cudaStream_t* s, bool high) {
   int lo = 0, hi = 0;
   if (prio_enabled() && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) {
-    if (cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, high ? hi : lo) == cudaSuccess) return;
+    const bool h = prio_mode() == 2 ? !high : high;
+    if (cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, h ? hi : lo) == cudaSuccess) return;
   }
   if (cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) != cudaSuccess) throw std::runtime_error("stream create");
 }

@@ -1626,15 +1626,18 @@ __global__ void __launch_bounds__(kThreads) zero_insert_kernel(const __nv_bfloat
 }
 
 // channel concat c = [a | b] and its backward
+// (index type I: 32-bit unsigned whenever the vector count allows -- a 64-bit
+// division per 16-byte vector made these copies instruction-bound)
+template <typename I>
 __global__ void __launch_bounds__(kThreads) concat_kernel(const __nv_bfloat16* __restrict__ a, int Ca,
                                                          const __nv_bfloat16* __restrict__ b, int Cb, long M,
                                                          __nv_bfloat16* __restrict__ c) {
   pdl_enter();
   const int Cc = Ca + Cb, cv = Cc / 8;
-  const long total = M * cv;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const long m = i / cv;
-    const int ch = (int)(i % cv) * 8;
+  const I total = (I)(M * cv);
+  for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+    const size_t m = (size_t)(i / (I)cv);
+    const int ch = (int)(i % (I)cv) * 8;
     if (ch < Ca) {
       if (a) *reinterpret_cast<uint4*>(c + m * Cc + ch) = ldg16(a + m * Ca + ch);
     } else if (b) {
@@ -1643,15 +1646,16 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(const __nv_bfloat16* _
   }
 }
 
+template <typename I>
 __global__ void __launch_bounds__(kThreads) split_grad_kernel(const __nv_bfloat16* __restrict__ dc, int Ca, int Cb,
                                                              long M, __nv_bfloat16* __restrict__ da, int acc_a,
                                                              __nv_bfloat16* __restrict__ db, int acc_b) {
   pdl_enter();
   const int Cc = Ca + Cb, cv = Cc / 8;
-  const long total = M * cv;
-  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
-    const long m = i / cv;
-    const int ch = (int)(i % cv) * 8;
+  const I total = (I)(M * cv);
+  for (I i = (I)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+    const size_t m = (size_t)(i / (I)cv);
+    const int ch = (int)(i % (I)cv) * 8;
     float f[8];
     unpack8(ldg16(dc + m * Cc + ch), f);
     __nv_bfloat16* dst;
@@ -2134,15 +2138,22 @@ cudaError_t zero_insert(const __nv_bfloat16* dy, int N, int P, int Q, int C, int
 cudaError_t concat(const __nv_bfloat16* a, int Ca, const __nv_bfloat16* b, int Cb, long M, __nv_bfloat16* c,
                    cudaStream_t st) {
   const long work = M * ((Ca + Cb) / 8);
-  RFK_CHECK_LAUNCH(launch_k(concat_kernel, grid_for(work, kThreads * 4), kThreads, 0, st, a, Ca, b, Cb, M, c));
+  if (work < (1L << 31))
+    RFK_CHECK_LAUNCH(launch_k(concat_kernel<unsigned>, grid_for(work, kThreads * 4), kThreads, 0, st, a, Ca, b, Cb, M, c));
+  else
+    RFK_CHECK_LAUNCH(launch_k(concat_kernel<long>, grid_for(work, kThreads * 4), kThreads, 0, st, a, Ca, b, Cb, M, c));
   return cudaGetLastError();
 }
 
 cudaError_t split_grad(const __nv_bfloat16* dc, int Ca, int Cb, long M, __nv_bfloat16* da, bool acc_a,
                        __nv_bfloat16* db, bool acc_b, cudaStream_t st) {
   const long work = M * ((Ca + Cb) / 8);
-  RFK_CHECK_LAUNCH(launch_k(split_grad_kernel, grid_for(work, kThreads * 4), kThreads, 0, st, dc, Ca, Cb, M, da, acc_a ? 1 : 0, db,
-                                                                       acc_b ? 1 : 0));
+  if (work < (1L << 31))
+    RFK_CHECK_LAUNCH(launch_k(split_grad_kernel<unsigned>, grid_for(work, kThreads * 4), kThreads, 0, st, dc, Ca, Cb, M, da,
+                              acc_a ? 1 : 0, db, acc_b ? 1 : 0));
+  else
+    RFK_CHECK_LAUNCH(launch_k(split_grad_kernel<long>, grid_for(work, kThreads * 4), kThreads, 0, st, dc, Ca, Cb, M, da,
+                              acc_a ? 1 : 0, db, acc_b ? 1 : 0));
   return cudaGetLastError();
 }
 
